@@ -1,0 +1,174 @@
+/*
+ * neob200.h - C ABI of libneob200.so, the sm_100a kernels behind the
+ * NCHW[x]c CNN-inference hot path (NeoCPU, arXiv 1809.02697).
+ *
+ * The reference (`neoplan`, /root/reference/pkg/src/neoplan) has no FFI: its
+ * "operator API" is the Python surface in __init__.py:5-31 and executor.py is
+ * the single dispatch point.  Each entry point below replaces one compute site
+ * of that surface; the interface it replaces is cited beside it.  The Python
+ * host package (paper_1809_02697_b200) binds these with ctypes.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes; every pointer argument is a DEVICE pointer
+ *     unless stated otherwise; callers allocate outputs (no call allocates);
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and returns before the work completes;
+ *   - return value: NEO_OK (0) or a neo_status; neo_last_error() returns the
+ *     thread-local message of the last failure.  The Python shim maps codes to
+ *     the reference exception taxonomy (errors.py:4-59).
+ *   - data types: NEO_F32 = IEEE float32, NEO_BF16 = bfloat16.  "tf32" values
+ *     are float32 containers whose low 13 mantissa bits are zero.
+ */
+#ifndef NEOB200_H
+#define NEOB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* neo_stream_t; /* cudaStream_t */
+
+typedef enum {
+  NEO_OK = 0,
+  NEO_ERR_SCHEDULE_INVALID = 1,   /* errors.ScheduleInvalid     */
+  NEO_ERR_SHAPE_MISMATCH = 2,     /* errors.ShapeMismatch       */
+  NEO_ERR_WRONG_LAYOUT = 3,       /* errors.WrongLayout         */
+  NEO_ERR_INDIVISIBLE_CHANNEL = 4,/* errors.IndivisibleChannel  */
+  NEO_ERR_UNSUPPORTED = 5,        /* configuration the kernels do not cover */
+  NEO_ERR_CUDA = 6,               /* CUDA runtime/driver failure */
+  NEO_ERR_INVALID_ARG = 7         /* bad pointer / size          */
+} neo_status;
+
+typedef enum { NEO_F32 = 0, NEO_BF16 = 1 } neo_dtype;
+
+/* feature-map layout tags (layout.py:21-71).  NCHW == NCHW[1]c in memory. */
+typedef enum { NEO_NCHW = 0, NEO_NHWC = 1, NEO_NCHWC = 2 } neo_layout_tag;
+
+/* conv arithmetic */
+typedef enum {
+  NEO_MODE_FP32 = 0, /* SIMT fp32 direct conv (parity anchor; conv_reference) */
+  NEO_MODE_TF32 = 1, /* tcgen05 kind::tf32, fp32 activations rounded to tf32 */
+  NEO_MODE_BF16 = 2  /* tcgen05 kind::f16 (bf16 in, fp32 accumulate)        */
+} neo_conv_mode;
+
+typedef enum { NEO_POOL_MAX = 0, NEO_POOL_AVG = 1 } neo_pool_mode;
+
+typedef enum {
+  NEO_ELT_RELU = 0,             /* out = max(a, 0)                           */
+  NEO_ELT_ADD = 1,              /* out = a + b                               */
+  NEO_ELT_ADD_RELU = 2,         /* out = max(a + b, 0)                       */
+  NEO_ELT_SCALE_SHIFT = 3,      /* out = a * scale[c] + shift[c]   (BN)      */
+  NEO_ELT_SCALE_SHIFT_RELU = 4  /* out = max(a * scale[c] + shift[c], 0)     */
+} neo_eltwise_op;
+
+/* flag bits */
+#define NEO_FLAG_ROUND_TF32 0x1   /* round fp32 results to tf32 (RN)        */
+#define NEO_FLAG_PAD_CHANNELS 0x2 /* allow C % x != 0: zero-filled pad lanes */
+
+const char* neo_last_error(void);
+int neo_abi_version(void);
+/* "name|sm_count|cc_major.cc_minor|hbm_bytes" of `device` into buf */
+int neo_device_info(int device, char* buf, int buflen);
+
+/* ---- layout transforms (layout.py:131-235) ------------------------------
+ * Feature map (n, c, h, w) logical; src/dst tags NCHW, NHWC (src only) or
+ * NCHW[x]c.  Replaces transform_array (layout.py:219-235): pack_nchw_array
+ * :131, unpack_nchw_array :140, retile_nchw_array :163, nhwc_to_nchw_array
+ * :180.  Bit-exact when src_dtype == dst_dtype and flags == 0.  With
+ * NEO_FLAG_PAD_CHANNELS a blocked side may carry ceil(c/x) blocks whose pad
+ * lanes are zero (pack) or dropped (unpack); without it c % x != 0 returns
+ * NEO_ERR_INDIVISIBLE_CHANNEL like the reference. */
+int neo_layout_transform(int src_dtype, int dst_dtype, const void* src, void* dst, int64_t n,
+                         int64_t c, int64_t h, int64_t w, int src_tag, int src_x, int dst_tag,
+                         int dst_x, int flags, neo_stream_t stream);
+
+/* KCRS <-> KCRS[x]c[y]k, bit-exact (pack_kcrs_array layout.py:147,
+ * unpack_kcrs_array :156).  dtype is the element type of both sides. */
+int neo_pack_weights(int dtype, const void* src, void* dst, int64_t k, int64_t c, int64_t r,
+                     int64_t s, int x, int y, neo_stream_t stream);
+int neo_unpack_weights(int dtype, const void* src, void* dst, int64_t k, int64_t c, int64_t r,
+                       int64_t s, int x, int y, neo_stream_t stream);
+
+/* Device-private tensor-core weight image used by NEO_MODE_TF32/BF16 convs
+ * (compile time, like pretransform_weights passes.py:258-286).  src is KCRS
+ * float32.  dst layout is slice-major (R, S, ceil(C/x), K, x) - every
+ * (r, s, channel-block) slice is a K x x K-major tile - padded with zero
+ * slices up to `slices_padded` (see neo_conv_umma_slices).  dst_dtype NEO_BF16
+ * rounds RN to bf16; NEO_F32 with NEO_FLAG_ROUND_TF32 rounds RN to tf32. */
+int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_dtype, int64_t k, int64_t c,
+                          int64_t r, int64_t s, int x, int64_t slices_padded, int flags,
+                          neo_stream_t stream);
+/* number of slices the conv kernel expects for (c, r, s, x, mode, tile cfg);
+ * the weight image must be packed with at least that many slices. */
+int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
+                             int slices_per_stage);
+
+/* ---- fused blocked convolution (kernels.py:250-303 conv_blocked, with the
+ * Epilogue kernels.py:74-87 applied in the order scale/shift -> bias ->
+ * residual -> relu, kernels.py:185-197) --------------------------------- */
+typedef struct neo_conv_params {
+  int mode;            /* neo_conv_mode                                       */
+  const void* x;       /* input  (n, cb_total_x, h, w, ic_bn); window below    */
+  const void* w;       /* FP32: KCRS[ic_bn]c[oc_bn]k f32; TF32/BF16: umma image */
+  void* out;           /* output (n, out_cb_total, oh, ow, oc_bn)              */
+  const float* scale;  /* per out-channel, or NULL                             */
+  const float* shift;  /* per out-channel, or NULL (0 when scale given)        */
+  const float* bias;   /* per out-channel, or NULL                             */
+  const void* residual;/* (n, res_cb_total, oh, ow, oc_bn) or NULL             */
+  int relu;
+  int64_t n, c, h, w_in, k, r, s;
+  int stride_h, stride_w, pad_h, pad_w;
+  int ic_bn, oc_bn;
+  int x_cb_offset, x_cb_total;     /* input channel-block window (0,0 = dense) */
+  int out_cb_offset, out_cb_total; /* concat-in-place destination window      */
+  int res_cb_offset, res_cb_total;
+  int out_dtype;       /* NEO_F32 / NEO_BF16 (residual has the same dtype)    */
+  int flags;           /* NEO_FLAG_ROUND_TF32 | NEO_FLAG_PAD_CHANNELS          */
+  /* tile configuration (0 = automatic).  tile_w x tile_h x tile_img output
+   * pixels (<= 128) form the M tile; tile_n output channels (multiple of 16,
+   * <= 256) the N tile; slices_per_stage (r, s, channel-block) slices per
+   * pipeline stage; stages = pipeline depth (<= 8). */
+  int tile_w, tile_h, tile_img, tile_n, slices_per_stage, stages;
+} neo_conv_params;
+
+int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);
+/* fill the automatic tile fields of *p the way neo_conv2d_nchwc_fused would */
+int neo_conv_default_tiles(neo_conv_params* p);
+
+/* ---- memory-bound operators (executor.py:96-203) ------------------------ */
+/* Max (pad -inf) / avg (pad 0, / win^2) pooling over h, w of NCHW[x]c
+ * (x = 1 is NCHW), replaces _pool2d executor.py:103-128. */
+int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb, int64_t h,
+               int64_t w, int x, int win, int stride, int pad, int flags, neo_stream_t stream);
+/* elementwise ops over (n, cb, hw, x) (x = 1 is NCHW); scale/shift indexed by
+ * channel cb*x+lane.  Replaces executor.py:165-190 (ReLU, BatchNorm with
+ * _channel_broadcast :96-100, ElementwiseAdd). */
+int neo_eltwise(int dtype, int op, const void* a, const void* b, void* out, const float* scale,
+                const float* shift, int64_t n, int64_t cb, int64_t hw, int x, int flags,
+                neo_stream_t stream);
+/* strided copy for np.concatenate (executor.py:191-193): src viewed as
+ * (outer, chunk) elements is copied into dst viewed as (outer, dst_row) at
+ * column dst_off.  Concat of k inputs = k calls. */
+int neo_concat_copy(int dtype, const void* src, void* dst, int64_t outer, int64_t chunk,
+                    int64_t dst_row, int64_t dst_off, neo_stream_t stream);
+/* out(n, units) f32 = a(n, in) @ w(units, in)^T (+ bias), executor.py:197-203.
+ * a and w share `dtype`. */
+int neo_dense(int dtype, const void* a, const void* w, const float* bias, float* out, int64_t n,
+              int64_t in_features, int64_t units, neo_stream_t stream);
+/* row softmax with max subtraction, executor.py:167-170 (f32 in/out) */
+int neo_softmax(const float* in, float* out, int64_t rows, int64_t cols, neo_stream_t stream);
+
+/* ---- whole-graph capture (replaces the Python per-op dispatch loop,
+ * executor.py:156-216, with one CUDA graph launch) ------------------------ */
+int neo_capture_begin(neo_stream_t stream);
+int neo_capture_end(neo_stream_t stream, void** graph_exec);
+int neo_graph_launch(void* graph_exec, neo_stream_t stream);
+int neo_graph_destroy(void* graph_exec);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NEOB200_H */

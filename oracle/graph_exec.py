@@ -1,0 +1,127 @@
+"""Whole-graph CPU interpreter -- TEST INFRASTRUCTURE ONLY.
+
+Restates the reference executor (executor.py:131-218) for graphs in the
+reference IR (graph.py:82-126: nodes with ``kind``, ``attrs``, ``inputs``
+edges, ``outputs``).  It is duck-typed: it reads the graph structure but
+imports nothing from the product package.  Conv nodes may carry an
+asymmetric ``pad=(ph, pw)`` / ``stride=(sh, sw)`` (the Inception-v3
+extension the reference cannot express); blocked
+layouts and LayoutTransform nodes are honoured like the reference does.
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+from . import ops
+
+
+def _topo(graph) -> list[int]:
+    """graph.py:129-152: Kahn order, ties broken by ascending id."""
+    indeg = {nid: 0 for nid in graph.nodes}
+    succ = {nid: [] for nid in graph.nodes}
+    for n in graph.nodes.values():
+        seen = set()
+        for i, _ in n.inputs:
+            if i in indeg and i not in seen:
+                seen.add(i)
+                indeg[n.id] += 1
+                succ[i].append(n.id)
+    ready = [nid for nid, d in indeg.items() if d == 0]
+    heapq.heapify(ready)
+    order = []
+    while ready:
+        nid = heapq.heappop(ready)
+        order.append(nid)
+        for s in succ[nid]:
+            indeg[s] -= 1
+            if indeg[s] == 0:
+                heapq.heappush(ready, s)
+    return order
+
+
+def _kind(n) -> str:
+    return getattr(n.kind, "value", n.kind)
+
+
+def _conv(n, vals):
+    data = vals[n.inputs[0][0]]
+    weight = vals[n.inputs[1][0]]
+    epi = dict(n.attrs.get("epilogue") or {})
+    ins = [vals[i] for i, _ in n.inputs]
+    residual = None
+    extra = 0
+    if epi.get("residual"):
+        residual = ins[-1]
+        extra += 1
+    bias = epi.get("bias")
+    if len(n.inputs) - extra >= 3:  # executor.py:63-66 explicit bias input
+        b = ins[2]
+        bias = b if bias is None else bias + b
+    stride, pad = n.attrs["stride"], n.attrs["pad"]
+    blocked = data.ndim == 5
+    if blocked:
+        data = ops.unpack_nchw(data)
+        if weight.ndim == 6:
+            weight = ops.unpack_kcrs(weight)
+        if residual is not None:
+            residual = ops.unpack_nchw(residual)
+    out = ops.conv2d(data, weight, stride, pad, epi.get("scale"), epi.get("shift"),
+                     bias, residual, bool(epi.get("relu", False)))
+    if blocked:
+        sch = n.attrs.get("schedule") or {}
+        y = sch.get("oc_bn") or (vals[n.inputs[1][0]].shape[5]
+                                 if vals[n.inputs[1][0]].ndim == 6 else 1)
+        out = ops.pack_nchw(out, y)
+    return out
+
+
+def execute_reference(graph, inputs: dict) -> list[np.ndarray]:
+    """Run ``graph`` on numpy ``inputs`` (name -> array); outputs in
+    ``graph.outputs`` order."""
+    vals: dict[int, np.ndarray] = {}
+    for nid in _topo(graph):
+        n = graph.nodes[nid]
+        k = _kind(n)
+        src = [vals[i] for i, _ in n.inputs]
+        if k == "Input":
+            name = n.attrs.get("name", f"input{nid}")
+            a = np.ascontiguousarray(inputs[name], dtype=np.float32)
+            if n.attrs.get("layout", "NCHW") == "NHWC":
+                a = ops.nhwc_to_nchw(a)
+            vals[nid] = a
+        elif k == "Constant":
+            vals[nid] = np.asarray(n.attrs["value"], dtype=np.float32)
+        elif k == "Conv2d":
+            vals[nid] = _conv(n, vals)
+        elif k == "ReLU":
+            vals[nid] = ops.relu(src[0])
+        elif k == "Softmax":
+            vals[nid] = ops.softmax(src[0])
+        elif k == "BatchNorm":
+            if len(n.inputs) == 5:
+                # executor.py:176-181 computes in the constants' dtype (f32)
+                g, b, m, v = (np.asarray(t, np.float32) for t in src[1:])
+                scale = g / np.sqrt(v + np.float32(n.attrs.get("eps", 1e-5)))
+                shift = b - m * scale
+            else:
+                scale, shift = n.attrs["scale"], n.attrs["shift"]
+            vals[nid] = ops.batchnorm(src[0], scale, shift)
+        elif k in ("MaxPool", "AvgPool"):
+            vals[nid] = ops.pool2d(src[0], n.attrs["window"], n.attrs["stride"],
+                                   n.attrs.get("pad", 0), "max" if k == "MaxPool" else "avg")
+        elif k == "ElementwiseAdd":
+            vals[nid] = ops.add(src[0], src[1])
+        elif k == "Concat":
+            vals[nid] = ops.concat(src, n.attrs.get("axis", 1))
+        elif k == "Flatten":
+            vals[nid] = ops.flatten(src[0])
+        elif k == "Dense":
+            vals[nid] = ops.dense(src[0], src[1], src[2] if len(src) == 3 else None)
+        elif k == "LayoutTransform":
+            vals[nid] = ops.transform(src[0], n.attrs["src_layout"], n.attrs["dst_layout"])
+        else:
+            raise ValueError(f"oracle cannot execute node kind {k}")
+    return [vals[o] for o in graph.outputs]

@@ -1,0 +1,210 @@
+"""Per-operator CPU restatements (numpy).  TEST INFRASTRUCTURE ONLY -- see
+oracle/__init__.py.  Reference paths are relative to
+/root/reference/pkg/src/neoplan unless noted."""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def rel_err(a, b) -> float:
+    """max|a-b| / max(1, max|b|)  (reference tests/test_kernels.py:31-32)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.size == 0:
+        return 0.0
+    return float(np.abs(a - b).max() / max(1.0, float(np.abs(b).max())))
+
+
+# ---------------------------------------------------------------------------
+# layouts: bit-exact index permutations (layout.py:131-183)
+
+def pack_nchw(a: np.ndarray, x: int) -> np.ndarray:
+    """(n,c,h,w) -> (n,c//x,h,w,c%x)   layout.py:131-137."""
+    n, c, h, w = a.shape
+    if c % x:
+        raise ValueError(f"C={c} not divisible by x={x}")
+    return np.ascontiguousarray(a.reshape(n, c // x, x, h, w).transpose(0, 1, 3, 4, 2))
+
+
+def unpack_nchw(a: np.ndarray) -> np.ndarray:
+    """inverse of pack_nchw   layout.py:140-144."""
+    n, cb, h, w, x = a.shape
+    return np.ascontiguousarray(a.transpose(0, 1, 4, 2, 3).reshape(n, cb * x, h, w))
+
+
+def pack_kcrs(w: np.ndarray, x: int, y: int) -> np.ndarray:
+    """(k,c,r,s) -> (k//y,c//x,r,s,c%x,k%y)   layout.py:147-153."""
+    k, c, r, s = w.shape
+    if c % x or k % y:
+        raise ValueError("indivisible channel")
+    return np.ascontiguousarray(
+        w.reshape(k // y, y, c // x, x, r, s).transpose(0, 2, 4, 5, 3, 1))
+
+
+def unpack_kcrs(w: np.ndarray) -> np.ndarray:
+    """inverse of pack_kcrs   layout.py:156-160."""
+    ko, co, r, s, x, y = w.shape
+    return np.ascontiguousarray(w.transpose(0, 5, 1, 4, 2, 3).reshape(ko * y, co * x, r, s))
+
+
+def retile_nchw(a: np.ndarray, b: int) -> np.ndarray:
+    """NCHW[a]c -> NCHW[b]c == pack(unpack(a), b)   layout.py:163-177."""
+    return pack_nchw(unpack_nchw(a), b)
+
+
+def nhwc_to_nchw(a: np.ndarray) -> np.ndarray:
+    """layout.py:180-183."""
+    return np.ascontiguousarray(a.transpose(0, 3, 1, 2))
+
+
+def transform(a: np.ndarray, src: str, dst: str) -> np.ndarray:
+    """transform_array dispatch (layout.py:219-235) on layout strings such as
+    'NCHW', 'NHWC', 'NCHW16c', 'KCRS', 'KCRS4c8k'."""
+    import re
+    if src == dst:
+        return a
+    ms = re.fullmatch(r"NCHW(\d+)c", src)
+    md = re.fullmatch(r"NCHW(\d+)c", dst)
+    if src == "NHWC" and dst == "NCHW":
+        return nhwc_to_nchw(a)
+    if src == "NCHW" and md:
+        return pack_nchw(a, int(md.group(1)))
+    if ms and dst == "NCHW":
+        return unpack_nchw(a)
+    if ms and md:
+        return retile_nchw(a, int(md.group(1)))
+    mk = re.fullmatch(r"KCRS(\d+)c(\d+)k", dst)
+    if src == "KCRS" and mk:
+        return pack_kcrs(a, int(mk.group(1)), int(mk.group(2)))
+    if re.fullmatch(r"KCRS(\d+)c(\d+)k", src) and dst == "KCRS":
+        return unpack_kcrs(a)
+    raise ValueError(f"no transform from {src} to {dst}")
+
+
+# ---------------------------------------------------------------------------
+# convolution (kernels.py:221-247 conv_reference; oracle form of
+# reference tests/test_kernels.py:11-28 im2col_conv, generalised to (ph, pw)
+# and (sh, sw) for the Inception 1x7 / 7x1 layers the reference cannot express)
+
+def _pair(v):
+    return (v, v) if isinstance(v, (int, np.integer)) else (int(v[0]), int(v[1]))
+
+
+def conv2d(x: np.ndarray, w: np.ndarray, stride=1, pad=0, scale=None,
+           shift=None, bias=None, residual=None, relu=False) -> np.ndarray:
+    """NCHW x KCRS -> NCHW f32; accumulation in float64 (im2col + BLAS), then
+    the epilogue in reference order scale/shift -> bias -> residual -> relu
+    (kernels.py:234-246), each step rounded to f32 like the numpy reference."""
+    sh, sw = _pair(stride)
+    ph, pw = _pair(pad)
+    n, c, h, wd = x.shape
+    k, c2, r, s = w.shape
+    assert c2 == c, (c2, c)
+    oh = (h + 2 * ph - r) // sh + 1
+    ow = (wd + 2 * pw - s) // sw + 1
+    xp = np.pad(x.astype(np.float64), ((0, 0), (0, 0), (ph, ph), (pw, pw)))
+    cols = np.empty((n, oh * ow, c, r, s), dtype=np.float64)
+    for ri in range(r):
+        for si in range(s):
+            patch = xp[:, :, ri:ri + (oh - 1) * sh + 1:sh, si:si + (ow - 1) * sw + 1:sw]
+            cols[:, :, :, ri, si] = patch.reshape(n, c, oh * ow).transpose(0, 2, 1)
+    wm = w.astype(np.float64).reshape(k, c * r * s)
+    out = np.matmul(cols.reshape(n, oh * ow, c * r * s), wm.T)  # (n, ohw, k)
+    out = out.transpose(0, 2, 1).reshape(n, k, oh, ow).astype(np.float32)
+    if scale is not None or shift is not None:
+        sc = np.ones(k, np.float32) if scale is None else np.asarray(scale, np.float32)
+        sf = np.zeros(k, np.float32) if shift is None else np.asarray(shift, np.float32)
+        out = out * sc.reshape(1, k, 1, 1)
+        out = out + sf.reshape(1, k, 1, 1)
+    if bias is not None:
+        out = out + np.asarray(bias, np.float32).reshape(1, k, 1, 1)
+    if residual is not None:
+        out = out + residual.astype(np.float32)
+    if relu:
+        out = np.maximum(out, np.float32(0.0))
+    return np.ascontiguousarray(out, dtype=np.float32)
+
+
+# ---------------------------------------------------------------------------
+# memory-bound ops (executor.py:96-203)
+
+def pool2d(a: np.ndarray, win: int, stride: int, pad: int, mode: str) -> np.ndarray:
+    """_pool2d executor.py:103-128 on NCHW or NCHW[x]c: max pads with -inf,
+    avg pads with 0 and divides by win*win (count_include_pad)."""
+    h, w = a.shape[2], a.shape[3]
+    oh = (h + 2 * pad - win) // stride + 1
+    ow = (w + 2 * pad - win) // stride + 1
+    if pad:
+        shape = list(a.shape)
+        shape[2] += 2 * pad
+        shape[3] += 2 * pad
+        p = np.full(shape, -np.inf if mode == "max" else 0.0, dtype=np.float32)
+        p[:, :, pad:pad + h, pad:pad + w] = a
+        a = p
+    out = None
+    for r in range(win):
+        for s in range(win):
+            sl = a[:, :, r:r + oh * stride:stride, s:s + ow * stride:stride]
+            if out is None:
+                out = sl.astype(np.float32, copy=True)
+            elif mode == "max":
+                out = np.maximum(out, sl)
+            else:
+                out = out + sl
+    if mode == "avg":
+        out = out / np.float32(win * win)
+    return np.ascontiguousarray(out, dtype=np.float32)
+
+
+def channel_broadcast(vec: np.ndarray, a: np.ndarray) -> np.ndarray:
+    """executor.py:96-100."""
+    if a.ndim == 5:
+        x = a.shape[4]
+        return vec.reshape(a.shape[1], x).reshape(1, a.shape[1], 1, 1, x)
+    return vec.reshape(1, -1, 1, 1)
+
+
+def batchnorm(a, scale, shift):
+    """standalone BN as a*scale + shift (executor.py:171-181)."""
+    return (a * channel_broadcast(np.asarray(scale, np.float32), a)
+            + channel_broadcast(np.asarray(shift, np.float32), a)).astype(np.float32)
+
+
+def bn_scale_shift(gamma, beta, mean, var, eps=1e-5):
+    """float64 folding constants (passes.py:92-96 / executor.py:176-178)."""
+    g, b, m, v = (np.asarray(t, np.float64) for t in (gamma, beta, mean, var))
+    scale = g / np.sqrt(v + eps)
+    shift = b - m * scale
+    return scale, shift
+
+
+def relu(a):
+    return np.maximum(a, np.float32(0.0))
+
+
+def add(a, b):
+    return (a + b).astype(np.float32)
+
+
+def concat(arrays, axis=1):
+    return np.concatenate(arrays, axis=axis)
+
+
+def flatten(a):
+    return np.ascontiguousarray(a).reshape(a.shape[0], -1)
+
+
+def dense(a, w, b=None):
+    """a @ w.T (+ b)  executor.py:197-203 (float64 accumulate)."""
+    out = (a.astype(np.float64) @ w.astype(np.float64).T)
+    if b is not None:
+        out = out + np.asarray(b, np.float64)
+    return out.astype(np.float32)
+
+
+def softmax(a):
+    """executor.py:167-170."""
+    a = a.astype(np.float32)
+    e = np.exp(a - a.max(axis=-1, keepdims=True))
+    return (e / e.sum(axis=-1, keepdims=True)).astype(np.float32)

@@ -1,0 +1,610 @@
+// K-CONV: NCHW[x]c convolution as a tcgen05/TMEM implicit GEMM.
+//
+// Replaces conv_blocked (reference kernels.py:250-303, hot loop _blocked_rows
+// :135-198) for NEO_MODE_BF16 / NEO_MODE_TF32.
+//
+// GEMM view:  M = output pixels (n, oh, ow), N = output channels k,
+//             K = (r, s, c) reduction.
+// The K loop walks "slices": one slice = one (r, s, input-channel-block) triple
+// = x channels.  In NCHW[x]c a slice of the input for an M tile is a
+// (BNI images x BH rows x BW cols x x lanes) box that TMA fetches with zero
+// fill for the padding halo (negative / past-the-end coordinates) and with
+// traversal strides for stride-2 convs, so no padded copy is ever made
+// (reference _pad_nchwc :211-218 disappears).  x*sizeof(elem) is exactly the
+// swizzle span (16/32/64/128 B), so each slice lands as a K-major UMMA
+// sub-tile of 128 rows without any reshuffle.  Weights use a device-private
+// slice-major image (R, S, C/x, K, x) so B sub-tiles have the same shape.
+//
+// Warp roles (192 threads, persistent over output tiles):
+//   warp 0     : TMA producer (one lane)     smem ring full/empty mbarriers
+//   warp 1     : TMEM alloc + MMA issuer     double-buffered TMEM accumulator
+//   warps 2..5 : epilogue (TMEM lane quarter = warp % 4): tcgen05.ld, then
+//                scale/shift -> bias -> residual -> relu (kernels.py:185-197)
+//                in registers, stored straight into NCHW[y]c (optionally into
+//                a channel-block window of a concat buffer).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "neo_common.cuh"
+
+namespace {
+
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 192;
+constexpr int kTileM = 128;
+constexpr int kSmemBudget = 227 * 1024;
+
+struct ConvTCParams {
+  CUtensorMap tmA;  // 5-D: (x, W, H, Cb, N)
+  CUtensorMap tmB;  // 3-D: (x, K, slices)
+  int N, OH, OW, K;
+  int BW, BH, BNI, BN;
+  int tiles_w, tiles_h, tiles_k;
+  int num_tiles;
+  int G, kstages, Cb, S, nslices;
+  int stride_h, stride_w, pad_h, pad_w;
+  int rowb;      // x * sizeof(elem)
+  int swz;       // UMMA layout code for rowb
+  int stages;
+  uint32_t a_sub, b_sub, a_stage, b_stage, tx_bytes, tmem_cols;
+  const float* scale;
+  const float* shift;
+  const float* bias;
+  const void* res;
+  void* out;
+  int y, out_cb_off, out_cb_total, res_cb_off, res_cb_total;
+  int relu, out_f32, round_tf32;
+};
+
+__device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n0, int& oh0,
+                                            int& ow0, int& k0) {
+  const int kt = t % p.tiles_k;
+  const int mt = t / p.tiles_k;
+  const int wi = mt % p.tiles_w;
+  const int hi = (mt / p.tiles_w) % p.tiles_h;
+  const int ni = mt / (p.tiles_w * p.tiles_h);
+  n0 = ni * p.BNI;
+  oh0 = hi * p.BH;
+  ow0 = wi * p.BW;
+  k0 = kt * p.BN;
+}
+
+struct EpiAccess {
+  size_t out_base, res_base;  // element offsets of channel block 0 for this pixel
+  size_t plane;               // OH*OW*y elements per channel block
+};
+
+__device__ __forceinline__ float epi_apply(const ConvTCParams& p, float v, int k) {
+  if (p.scale) v = fmaf(v, __ldg(p.scale + k), p.shift ? __ldg(p.shift + k) : 0.f);
+  else if (p.shift) v = v + __ldg(p.shift + k);
+  if (p.bias) v = v + __ldg(p.bias + k);
+  return v;
+}
+
+__device__ __forceinline__ float epi_finish(const ConvTCParams& p, float v) {
+  if (p.relu) v = fmaxf(v, 0.f);
+  if (p.round_tf32) v = neo_round_tf32(v);
+  return v;
+}
+
+// 16 accumulator columns [kbase, kbase+16) of one output pixel
+__device__ __forceinline__ void epi_chunk(const ConvTCParams& p, const uint32_t (&v)[16],
+                                          int kbase, const EpiAccess& ea) {
+  float f[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+
+  if ((p.y & 15) == 0 && kbase + 16 <= p.K) {
+    // whole chunk inside one output channel block: vector path
+    const int kb = kbase / p.y, j0 = kbase % p.y;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = epi_apply(p, f[j], kbase + j);
+    if (p.out_f32) {
+      if (p.res) {
+        const float4* r4 = reinterpret_cast<const float4*>(
+            static_cast<const float*>(p.res) + ea.res_base + (size_t)kb * ea.plane + j0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float4 rv = __ldg(r4 + q);
+          f[4 * q + 0] += rv.x;
+          f[4 * q + 1] += rv.y;
+          f[4 * q + 2] += rv.z;
+          f[4 * q + 3] += rv.w;
+        }
+      }
+      float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(p.out) + ea.out_base +
+                                             (size_t)kb * ea.plane + j0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o4[q] = make_float4(epi_finish(p, f[4 * q]), epi_finish(p, f[4 * q + 1]),
+                            epi_finish(p, f[4 * q + 2]), epi_finish(p, f[4 * q + 3]));
+    } else {
+      if (p.res) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(
+            static_cast<const __nv_bfloat16*>(p.res) + ea.res_base + (size_t)kb * ea.plane + j0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          uint4 rv = __ldg(r4 + q);
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 t = __bfloat1622float2(h2[e]);
+            f[8 * q + 2 * e] += t.x;
+            f[8 * q + 2 * e + 1] += t.y;
+          }
+        }
+      }
+      uint4 packed[2];
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(packed);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        h2[e] = __floats2bfloat162_rn(epi_finish(p, f[2 * e]), epi_finish(p, f[2 * e + 1]));
+      uint4* o4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + ea.out_base +
+                                           (size_t)kb * ea.plane + j0);
+      o4[0] = packed[0];
+      o4[1] = packed[1];
+    }
+    return;
+  }
+  // generic path: any y, partial chunk at the end of K
+#pragma unroll 1
+  for (int j = 0; j < 16; ++j) {
+    const int k = kbase + j;
+    if (k >= p.K) break;
+    const int kb = k / p.y, jj = k % p.y;
+    float val = epi_apply(p, f[j], k);
+    const size_t o = ea.out_base + (size_t)kb * ea.plane + jj;
+    if (p.out_f32) {
+      if (p.res) val += static_cast<const float*>(p.res)[ea.res_base + (size_t)kb * ea.plane + jj];
+      static_cast<float*>(p.out)[o] = epi_finish(p, val);
+    } else {
+      if (p.res)
+        val += __bfloat162float(
+            static_cast<const __nv_bfloat16*>(p.res)[ea.res_base + (size_t)kb * ea.plane + jj]);
+      static_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16_rn(epi_finish(p, val));
+    }
+  }
+}
+
+template <bool TF32>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
+  const uint32_t sA = sraw + pad;
+  const uint32_t sB = sA + p.stages * p.a_stage;
+  const uint32_t sBar = sB + p.stages * p.b_stage;
+  uint8_t* bar_gen = smem_raw + pad + p.stages * (p.a_stage + p.b_stage);
+  auto full_bar = [&](int i) { return sBar + 8u * i; };
+  auto empty_bar = [&](int i) { return sBar + 64u + 8u * i; };
+  auto tfull_bar = [&](int a) { return sBar + 128u + 8u * a; };
+  auto tempty_bar = [&](int a) { return sBar + 144u + 8u * a; };
+  const uint32_t tslot = sBar + 160u;
+  volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 160);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&p.tmA);
+    tma_prefetch_desc(&p.tmB);
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(full_bar(i), 1);
+      mbar_init(empty_bar(i), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tslot, p.tmem_cols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tslot_gen;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int n0, oh0, ow0, k0;
+        decode_tile(p, t, n0, oh0, ow0, k0);
+        const int iw0 = ow0 * p.stride_w - p.pad_w;
+        const int ih0 = oh0 * p.stride_h - p.pad_h;
+        for (int ks = 0; ks < p.kstages; ++ks) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
+          const uint32_t a_dst = sA + stage * p.a_stage;
+          for (int g = 0; g < p.G; ++g) {
+            const int sl = ks * p.G + g;
+            int co = p.Cb, r = 0, s = 0;  // padding slice: fully out of bounds -> zeros
+            if (sl < p.nslices) {
+              co = sl % p.Cb;
+              const int rs = sl / p.Cb;
+              s = rs % p.S;
+              r = rs / p.S;
+            }
+            tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0 + s, ih0 + r, co, n0);
+          }
+          tma_load_3d(sB + stage * p.b_stage, &p.tmB, full_bar(stage), 0, k0, ks * p.G);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, kTileM, p.BN);
+      const int ksteps = p.G * p.rowb / 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * p.BN;
+        for (int ks = 0; ks < p.kstages; ++ks) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t a0 = sA + stage * p.a_stage;
+          const uint32_t b0 = sB + stage * p.b_stage;
+          for (int k = 0; k < ksteps; ++k) {
+            uint64_t ad, bd;
+            if (p.rowb == 16) {
+              // 16-byte rows: no swizzle; one K step spans two slices (LBO)
+              ad = umma_smem_desc(a0 + 2 * k * p.a_sub, p.a_sub, 128, 0);
+              bd = umma_smem_desc(b0 + 2 * k * p.b_sub, p.b_sub, 128, 0);
+            } else {
+              const uint32_t byte = 32u * k;
+              const uint32_t sub = byte / p.rowb, inrow = byte % p.rowb;
+              ad = umma_smem_desc(a0 + sub * p.a_sub + inrow, 16, 8 * p.rowb, p.swz);
+              bd = umma_smem_desc(b0 + sub * p.b_sub + inrow, 16, 8 * p.rowb, p.swz);
+            }
+            umma_ss<TF32>(d_tmem, ad, bd, idesc, (ks | k) != 0);
+          }
+          umma_commit(empty_bar(stage));
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(tfull_bar(acc));
+      }
+    }
+  } else {
+    // ---------------- epilogue warps ----------------
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    const size_t plane = (size_t)p.OH * p.OW * p.y;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      int n0, oh0, ow0, k0;
+      decode_tile(p, t, n0, oh0, ow0, k0);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int wl = m % p.BW, hl = (m / p.BW) % p.BH, nl = m / (p.BW * p.BH);
+      const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
+      const bool valid = (m < p.BW * p.BH * p.BNI) && ow < p.OW && oh < p.OH && n < p.N;
+      EpiAccess ea;
+      ea.plane = plane;
+      const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
+      ea.out_base = (size_t)n * p.out_cb_total * plane + (size_t)p.out_cb_off * plane + pix;
+      ea.res_base = (size_t)n * p.res_cb_total * plane + (size_t)p.res_cb_off * plane + pix;
+
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.BN;
+      const int ncols = min(p.BN, p.K - k0);
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + c0, v);
+        tmem_ld_wait();
+        if (valid) epi_chunk(p, v, k0 + c0, ea);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+int sm_count_of_current_device() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+int swizzle_code_umma(int rowb) {
+  switch (rowb) {
+    case 32: return 6;
+    case 64: return 4;
+    case 128: return 2;
+    default: return 0;
+  }
+}
+CUtensorMapSwizzle swizzle_code_tma(int rowb) {
+  switch (rowb) {
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    default: return CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
+}
+
+int64_t conv_out_dim(int64_t in, int64_t k, int st, int pad) { return (in + 2 * pad - k) / st + 1; }
+
+struct Geometry {
+  int BW, BH, BNI;
+};
+
+// M-tile geometry maximising useful rows of the 128-row MMA tile
+Geometry pick_geometry(int64_t N, int64_t OH, int64_t OW) {
+  Geometry best{1, 1, 1};
+  double best_eff = -1.0;
+  const int bw_max = (int)std::min<int64_t>(OW, kTileM);
+  for (int bw = 1; bw <= bw_max; ++bw) {
+    const int bh_max = (int)std::min<int64_t>(OH, kTileM / bw);
+    for (int bh = 1; bh <= bh_max; ++bh) {
+      const int bni_max = (int)std::min<int64_t>(N, kTileM / (bw * bh));
+      for (int bni = 1; bni <= bni_max; ++bni) {
+        const double tiles =
+            (double)neo_ceil_div(OW, bw) * neo_ceil_div(OH, bh) * neo_ceil_div(N, bni);
+        const double eff = (double)N * OH * OW / (tiles * kTileM);
+        const bool better = eff > best_eff + 1e-9 ||
+                            (eff > best_eff - 1e-9 &&
+                             (bw > best.BW || (bw == best.BW && bw * bh * bni > best.BW * best.BH * best.BNI)));
+        if (better) {
+          best_eff = eff;
+          best = {bw, bh, bni};
+        }
+      }
+    }
+  }
+  return best;
+}
+
+int pick_tile_n(int64_t K) {
+  if (K <= 256) return (int)neo_ceil_div(K, 16) * 16;
+  int best = 256;
+  int64_t best_waste = neo_ceil_div(K, 256) * 256 - K;
+  for (int bn : {192, 128}) {
+    int64_t waste = neo_ceil_div(K, bn) * bn - K;
+    if (waste < best_waste) {
+      best_waste = waste;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+int pick_slices_per_stage(int64_t nslices, int rowb, int bn) {
+  const int gmax = std::max(1, 256 / rowb);
+  int best = (rowb == 16) ? 2 : 1;
+  double best_cost = 1e30;
+  for (int g = 1; g <= gmax; ++g) {
+    if (rowb == 16 && (g & 1)) continue;
+    const int64_t stage_bytes = (int64_t)g * (kTileM + bn) * rowb;
+    if (stage_bytes > 60 * 1024 && g > ((rowb == 16) ? 2 : 1)) continue;
+    const int64_t ks = neo_ceil_div(nslices, g);
+    const double cost = (double)(ks * g) * rowb + (double)ks * 48.0;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = g;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+// exported for layout.cu / the ABI
+int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
+                             int slices_per_stage) {
+  // stage padding past nslices is served by TMA out-of-bounds zero fill, so
+  // the image needs exactly R*S*ceil(C/x) slices whatever slices_per_stage is
+  (void)mode;
+  (void)slices_per_stage;
+  if (x <= 0) return -1;
+  return r * s * neo_ceil_div(c, x);
+}
+
+int neo_conv_default_tiles(neo_conv_params* p) {
+  NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
+  if (p->mode == NEO_MODE_FP32) return NEO_OK;
+  const int es = p->mode == NEO_MODE_BF16 ? 2 : 4;
+  const int rowb = p->ic_bn * es;
+  const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
+  const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
+  NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "conv has empty output");
+  if (p->tile_w <= 0 || p->tile_h <= 0 || p->tile_img <= 0) {
+    Geometry g = pick_geometry(p->n, OH, OW);
+    p->tile_w = g.BW;
+    p->tile_h = g.BH;
+    p->tile_img = g.BNI;
+  }
+  if (p->tile_n <= 0) p->tile_n = pick_tile_n(p->k);
+  const int64_t nslices = p->r * p->s * neo_ceil_div(p->c, p->ic_bn);
+  if (p->slices_per_stage <= 0) p->slices_per_stage = pick_slices_per_stage(nslices, rowb, p->tile_n);
+  if (p->stages <= 0) {
+    const int64_t stage = (int64_t)p->slices_per_stage * (kTileM + p->tile_n) * rowb;
+    p->stages = (int)std::min<int64_t>(kMaxStages, (kSmemBudget - 2048) / stage);
+  }
+  return NEO_OK;
+}
+
+int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
+  neo_conv_params pc = *pin;
+  int st = neo_conv_default_tiles(&pc);
+  if (st != NEO_OK) return st;
+  const neo_conv_params* p = &pc;
+  const bool tf32 = p->mode == NEO_MODE_TF32;
+  const int es = tf32 ? 4 : 2;
+  const int x = p->ic_bn;
+  const int rowb = x * es;
+  NEO_CHECK_ARG(rowb == 16 || rowb == 32 || rowb == 64 || rowb == 128, NEO_ERR_UNSUPPORTED,
+                "tensor-core conv needs ic_bn*sizeof in {16,32,64,128} bytes (ic_bn=%d, %s)", x,
+                tf32 ? "tf32" : "bf16");
+  NEO_CHECK_ARG(p->out_dtype == NEO_F32 || !tf32, NEO_ERR_UNSUPPORTED, "tf32 mode writes f32");
+  const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
+  const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
+  const int BW = p->tile_w, BH = p->tile_h, BNI = p->tile_img, BN = p->tile_n;
+  NEO_CHECK_ARG(BW * BH * BNI <= kTileM && BW >= 1 && BH >= 1 && BNI >= 1, NEO_ERR_SCHEDULE_INVALID,
+                "M tile %dx%dx%d exceeds 128 pixels", BW, BH, BNI);
+  NEO_CHECK_ARG(BN % 16 == 0 && BN >= 16 && BN <= 256, NEO_ERR_SCHEDULE_INVALID,
+                "tile_n=%d must be a multiple of 16 in [16,256]", BN);
+  NEO_CHECK_ARG(BW * p->stride_w <= 256 && BH * p->stride_h <= 256 && p->stride_w <= 8 &&
+                    p->stride_h <= 8,
+                NEO_ERR_UNSUPPORTED, "TMA box too large for stride");
+  const int G = p->slices_per_stage;
+  NEO_CHECK_ARG(G >= 1 && (rowb != 16 || G % 2 == 0), NEO_ERR_SCHEDULE_INVALID,
+                "slices_per_stage=%d invalid for %d-byte rows", G, rowb);
+  NEO_CHECK_ARG(p->stages >= 2 && p->stages <= kMaxStages, NEO_ERR_SCHEDULE_INVALID,
+                "stages=%d outside [2,%d] (stage too large for shared memory?)", p->stages,
+                kMaxStages);
+
+  const int64_t Cb = neo_ceil_div(p->c, x);
+  const int64_t cbt = p->x_cb_total > 0 ? p->x_cb_total : Cb;
+  const int64_t nslices = p->r * p->s * Cb;
+  const int64_t kstages = neo_ceil_div(nslices, G);
+
+  ConvTCParams kp;
+  memset(&kp, 0, sizeof(kp));
+  auto encode = get_encode_fn();
+  NEO_CHECK_ARG(encode != nullptr, NEO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const CUtensorMapDataType dt =
+      tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  {
+    const char* base = static_cast<const char*>(p->x) + (size_t)p->x_cb_offset * p->h * p->w_in * rowb;
+    cuuint64_t dims[5] = {(cuuint64_t)x, (cuuint64_t)p->w_in, (cuuint64_t)p->h, (cuuint64_t)Cb,
+                          (cuuint64_t)p->n};
+    cuuint64_t strides[4] = {(cuuint64_t)rowb, (cuuint64_t)p->w_in * rowb,
+                             (cuuint64_t)p->h * p->w_in * rowb,
+                             (cuuint64_t)cbt * p->h * p->w_in * rowb};
+    cuuint32_t box[5] = {(cuuint32_t)x, (cuuint32_t)(BW * p->stride_w),
+                         (cuuint32_t)(BH * p->stride_h), 1u, (cuuint32_t)BNI};
+    cuuint32_t estr[5] = {1u, (cuuint32_t)p->stride_w, (cuuint32_t)p->stride_h, 1u, 1u};
+    CUresult r = encode(&kp.tmA, dt, 5, const_cast<char*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map A encode failed (%d)", (int)r);
+  }
+  {
+    // slices past nslices (stage padding) are out of bounds -> zero filled
+    cuuint64_t dims[3] = {(cuuint64_t)x, (cuuint64_t)p->k, (cuuint64_t)nslices};
+    cuuint64_t strides[2] = {(cuuint64_t)rowb, (cuuint64_t)p->k * rowb};
+    cuuint32_t box[3] = {(cuuint32_t)x, (cuuint32_t)BN, (cuuint32_t)G};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = encode(&kp.tmB, dt, 3, const_cast<void*>(p->w), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map B encode failed (%d)", (int)r);
+  }
+  kp.N = (int)p->n;
+  kp.OH = (int)OH;
+  kp.OW = (int)OW;
+  kp.K = (int)p->k;
+  kp.BW = BW;
+  kp.BH = BH;
+  kp.BNI = BNI;
+  kp.BN = BN;
+  kp.tiles_w = (int)neo_ceil_div(OW, BW);
+  kp.tiles_h = (int)neo_ceil_div(OH, BH);
+  kp.tiles_k = (int)neo_ceil_div(p->k, BN);
+  const int64_t tiles_n = neo_ceil_div(p->n, BNI);
+  const int64_t num_tiles = (int64_t)kp.tiles_w * kp.tiles_h * tiles_n * kp.tiles_k;
+  NEO_CHECK_ARG(num_tiles < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many tiles");
+  kp.num_tiles = (int)num_tiles;
+  kp.G = G;
+  kp.kstages = (int)kstages;
+  kp.Cb = (int)Cb;
+  kp.S = (int)p->s;
+  kp.nslices = (int)nslices;
+  kp.stride_h = p->stride_h;
+  kp.stride_w = p->stride_w;
+  kp.pad_h = p->pad_h;
+  kp.pad_w = p->pad_w;
+  kp.rowb = rowb;
+  kp.swz = swizzle_code_umma(rowb);
+  kp.stages = p->stages;
+  kp.a_sub = (uint32_t)(kTileM * rowb);
+  kp.b_sub = (uint32_t)(BN * rowb);
+  kp.a_stage = kp.a_sub * G;
+  kp.b_stage = kp.b_sub * G;
+  kp.tx_bytes = (uint32_t)(G * (BW * BH * BNI * rowb + BN * rowb));
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * BN)) cols <<= 1;
+  kp.tmem_cols = cols;
+  kp.scale = p->scale;
+  kp.shift = p->shift;
+  kp.bias = p->bias;
+  kp.res = p->residual;
+  kp.out = p->out;
+  kp.y = p->oc_bn;
+  const int64_t kbt = neo_ceil_div(p->k, p->oc_bn);
+  kp.out_cb_off = p->out_cb_offset;
+  kp.out_cb_total = p->out_cb_total > 0 ? p->out_cb_total : (int)kbt;
+  kp.res_cb_off = p->res_cb_offset;
+  kp.res_cb_total = p->res_cb_total > 0 ? p->res_cb_total : (int)kbt;
+  kp.relu = p->relu;
+  kp.out_f32 = p->out_dtype == NEO_F32;
+  kp.round_tf32 = (p->flags & NEO_FLAG_ROUND_TF32) ? 1 : 0;
+
+  const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) + 256;
+  NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
+                "conv tile needs %zu bytes of shared memory", smem);
+  const int grid = (int)std::min<int64_t>(num_tiles, sm_count_of_current_device());
+  if (tf32) {
+    NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    conv_tc_kernel<true><<<grid, kThreads, smem, stream>>>(kp);
+  } else {
+    NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    conv_tc_kernel<false><<<grid, kThreads, smem, stream>>>(kp);
+  }
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}

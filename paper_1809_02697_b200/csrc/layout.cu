@@ -1,0 +1,307 @@
+// K-LAYOUT / K-WPACK: bit-exact layout transforms between NCHW, NHWC and
+// NCHW[x]c feature maps and between KCRS and KCRS[x]c[y]k weights
+// (reference layout.py:131-235), plus the device-private slice-major weight
+// image consumed by the tensor-core conv.
+//
+// Pack / unpack / NHWC ingest are batched 2-D transposes staged through a
+// 32x33 shared-memory tile so both the read and the write side are coalesced;
+// retile and the weight permutations are gathers (compile time / rare).
+#include "neo_common.cuh"
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld_as_f(const T* p, int64_t i) {
+  return Elem<T>::to_f(p[i]);
+}
+
+// bit-preserving element move with optional dtype conversion / tf32 rounding
+template <typename Ts, typename Td>
+struct Conv {
+  static __device__ __forceinline__ Td cvt(Ts v, bool) { return Elem<Td>::from_f(Elem<Ts>::to_f(v)); }
+};
+template <>
+struct Conv<float, float> {
+  static __device__ __forceinline__ float cvt(float v, bool round) {
+    return round ? neo_round_tf32(v) : v;
+  }
+};
+template <>
+struct Conv<__nv_bfloat16, __nv_bfloat16> {
+  static __device__ __forceinline__ __nv_bfloat16 cvt(__nv_bfloat16 v, bool) { return v; }
+};
+
+// Batched transpose: for each batch b, src viewed (R rows x C cols) is written
+// to dst viewed (C rows x R cols).  Index maps are supplied by Map.
+struct PackMap {  // NCHW -> NCHW[x]c; b = (n, cb); rows = lanes j, cols = pixels
+  int64_t Call, HW, Cb;
+  int x;
+  __device__ bool src(int64_t b, int64_t r, int64_t c, int64_t& off) const {
+    const int64_t n = b / Cb, cb = b % Cb, ch = cb * x + r;
+    off = (n * Call + ch) * HW + c;
+    return ch < Call;
+  }
+  __device__ bool dst(int64_t b, int64_t c, int64_t r, int64_t& off) const {
+    off = (b * HW + c) * x + r;
+    return true;
+  }
+};
+struct UnpackMap {  // NCHW[x]c -> NCHW; b = (n, cb); rows = pixels, cols = lanes
+  int64_t Call, HW, Cb;
+  int x;
+  __device__ bool src(int64_t b, int64_t r, int64_t c, int64_t& off) const {
+    off = (b * HW + r) * x + c;
+    return true;
+  }
+  __device__ bool dst(int64_t b, int64_t c, int64_t r, int64_t& off) const {
+    const int64_t n = b / Cb, cb = b % Cb, ch = cb * x + c;
+    off = (n * Call + ch) * HW + r;
+    return ch < Call;
+  }
+};
+struct NhwcMap {  // NHWC -> NCHW; b = n; rows = pixels, cols = channels
+  int64_t Call, HW;
+  __device__ bool src(int64_t b, int64_t r, int64_t c, int64_t& off) const {
+    off = (b * HW + r) * Call + c;
+    return true;
+  }
+  __device__ bool dst(int64_t b, int64_t c, int64_t r, int64_t& off) const {
+    off = (b * Call + c) * HW + r;
+    return true;
+  }
+};
+
+template <typename Ts, typename Td, class Map>
+__global__ void transpose_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, Map m,
+                                 int64_t B, int64_t R, int64_t C, bool round) {
+  __shared__ Ts tile[32][33];
+  __shared__ bool ok[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int64_t b = blockIdx.z; b < B; b += gridDim.z) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t r = r0 + ty + 8 * i, c = c0 + tx;
+      int64_t off = 0;
+      bool v = r < R && c < C && m.src(b, r, c, off);
+      tile[ty + 8 * i][tx] = v ? src[off] : Elem<Ts>::from_f(0.f);
+      ok[ty + 8 * i][tx] = r < R && c < C;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t c = c0 + ty + 8 * i, r = r0 + tx;
+      int64_t off = 0;
+      if (ok[tx][ty + 8 * i] && m.dst(b, c, r, off))
+        dst[off] = Conv<Ts, Td>::cvt(tile[tx][ty + 8 * i], round);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename Ts, typename Td, class Map>
+void launch_transpose(const void* src, void* dst, Map m, int64_t B, int64_t R, int64_t C,
+                      bool round, cudaStream_t st) {
+  dim3 block(32, 8);
+  dim3 grid((unsigned)neo_ceil_div(C, 32), (unsigned)neo_ceil_div(R, 32),
+            (unsigned)std::min<int64_t>(B, 65535));
+  transpose_kernel<Ts, Td, Map><<<grid, block, 0, st>>>(static_cast<const Ts*>(src),
+                                                        static_cast<Td*>(dst), m, B, R, C, round);
+}
+
+// NCHW[a]c -> NCHW[b]c (retile_nchw_array layout.py:163-177), also same-layout
+// copies/conversions (a == b, or NCHW as a = 1)
+template <typename Ts, typename Td>
+__global__ void retile_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, int64_t N,
+                              int64_t Call, int64_t HW, int a, int b, bool round) {
+  const int64_t cbd = (Call + b - 1) / b, cbs = (Call + a - 1) / a;
+  const int64_t total = N * cbd * HW * b;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int j = (int)(t % b);
+    t /= b;
+    const int64_t p = t % HW;
+    t /= HW;
+    const int64_t cb = t % cbd;
+    const int64_t n = t / cbd;
+    const int64_t ch = cb * b + j;
+    if (ch < Call) {
+      const int64_t so = ((n * cbs + ch / a) * HW + p) * a + ch % a;
+      dst[i] = Conv<Ts, Td>::cvt(src[so], round);
+    } else {
+      dst[i] = Elem<Td>::from_f(0.f);
+    }
+  }
+}
+
+template <typename Ts, typename Td>
+int dispatch_layout(const void* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                    int src_tag, int src_x, int dst_tag, int dst_x, bool round, cudaStream_t st) {
+  const int64_t HW = h * w;
+  if (src_tag == NEO_NCHW && dst_tag == NEO_NCHWC) {
+    const int64_t cb = neo_ceil_div(c, dst_x);
+    launch_transpose<Ts, Td>(src, dst, PackMap{c, HW, cb, dst_x}, n * cb, dst_x, HW, round, st);
+  } else if (src_tag == NEO_NCHWC && dst_tag == NEO_NCHW) {
+    const int64_t cb = neo_ceil_div(c, src_x);
+    launch_transpose<Ts, Td>(src, dst, UnpackMap{c, HW, cb, src_x}, n * cb, HW, src_x, round, st);
+  } else if (src_tag == NEO_NHWC && dst_tag == NEO_NCHW) {
+    launch_transpose<Ts, Td>(src, dst, NhwcMap{c, HW}, n, HW, c, round, st);
+  } else {
+    // NCHW[a]c -> NCHW[b]c, NCHW -> NCHW (a = b = 1)
+    const int a = src_tag == NEO_NCHW ? 1 : src_x;
+    const int b = dst_tag == NEO_NCHW ? 1 : dst_x;
+    const int64_t total = n * neo_ceil_div(c, b) * HW * b;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
+    retile_kernel<Ts, Td><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const Ts*>(src),
+                                                            static_cast<Td*>(dst), n, c, HW, a, b,
+                                                            round);
+  }
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+// KCRS -> KCRS[x]c[y]k and back (pack_kcrs_array :147, unpack_kcrs_array :156);
+// 32-bit / 16-bit payloads moved as raw bits
+template <typename T>
+__global__ void weights_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t K, int64_t C,
+                               int64_t RS, int x, int y, bool pack) {
+  const int64_t total = K * C * RS;
+  const int64_t Cb = C / x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // i enumerates the packed layout (ko, co, rs, ci, kj)
+    int64_t t = i;
+    const int kj = (int)(t % y);
+    t /= y;
+    const int ci = (int)(t % x);
+    t /= x;
+    const int64_t rs = t % RS;
+    t /= RS;
+    const int64_t co = t % Cb;
+    const int64_t ko = t / Cb;
+    const int64_t plain = ((ko * y + kj) * C + co * x + ci) * RS + rs;
+    if (pack) dst[i] = src[plain];
+    else dst[plain] = src[i];
+  }
+}
+
+template <typename Td>
+__global__ void weights_umma_kernel(const float* __restrict__ src, Td* __restrict__ dst, int64_t K,
+                                    int64_t C, int64_t R, int64_t S, int x, int64_t slices,
+                                    int64_t nslices, bool round) {
+  const int64_t Cb = (C + x - 1) / x;
+  const int64_t total = slices * K * x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int j = (int)(t % x);
+    t /= x;
+    const int64_t k = t % K;
+    const int64_t sl = t / K;
+    float v = 0.f;
+    if (sl < nslices) {
+      const int64_t cb = sl % Cb, rs = sl / Cb;
+      const int64_t s = rs % S, r = rs / S;
+      const int64_t ch = cb * x + j;
+      if (ch < C) v = src[((k * C + ch) * R + r) * S + s];
+    }
+    if constexpr (sizeof(Td) == 4) dst[i] = round ? neo_round_tf32(v) : v;
+    else dst[i] = Elem<Td>::from_f(v);
+  }
+}
+
+int64_t grid_for(int64_t total) {
+  return std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
+}
+
+}  // namespace
+
+extern "C" int neo_layout_transform(int src_dtype, int dst_dtype, const void* src, void* dst,
+                                    int64_t n, int64_t c, int64_t h, int64_t w, int src_tag,
+                                    int src_x, int dst_tag, int dst_x, int flags,
+                                    neo_stream_t stream) {
+  NEO_CHECK_ARG(src && dst, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(n >= 1 && c >= 1 && h >= 1 && w >= 1, NEO_ERR_SHAPE_MISMATCH,
+                "non-positive dim in (%lld,%lld,%lld,%lld)", (long long)n, (long long)c,
+                (long long)h, (long long)w);
+  NEO_CHECK_ARG((src_dtype == NEO_F32 || src_dtype == NEO_BF16) &&
+                    (dst_dtype == NEO_F32 || dst_dtype == NEO_BF16),
+                NEO_ERR_INVALID_ARG, "bad dtype");
+  NEO_CHECK_ARG(src_tag >= 0 && src_tag <= 2 && dst_tag >= 0 && dst_tag <= 2, NEO_ERR_WRONG_LAYOUT,
+                "unknown layout tag");
+  NEO_CHECK_ARG(dst_tag != NEO_NHWC, NEO_ERR_WRONG_LAYOUT, "no transform to NHWC");
+  NEO_CHECK_ARG(src_tag != NEO_NHWC || dst_tag == NEO_NCHW, NEO_ERR_WRONG_LAYOUT,
+                "NHWC is only ingested into NCHW");
+  const bool padc = (flags & NEO_FLAG_PAD_CHANNELS) != 0;
+  if (src_tag == NEO_NCHWC) {
+    NEO_CHECK_ARG(src_x >= 1, NEO_ERR_WRONG_LAYOUT, "NCHW[x]c needs x >= 1");
+    NEO_CHECK_ARG(padc || c % src_x == 0, NEO_ERR_INDIVISIBLE_CHANNEL,
+                  "C=%lld not divisible by x=%d", (long long)c, src_x);
+  }
+  if (dst_tag == NEO_NCHWC) {
+    NEO_CHECK_ARG(dst_x >= 1, NEO_ERR_WRONG_LAYOUT, "NCHW[x]c needs x >= 1");
+    NEO_CHECK_ARG(padc || c % dst_x == 0, NEO_ERR_INDIVISIBLE_CHANNEL,
+                  "C=%lld not divisible by x=%d", (long long)c, dst_x);
+  }
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (src_dtype == NEO_F32 && dst_dtype == NEO_F32)
+    return dispatch_layout<float, float>(src, dst, n, c, h, w, src_tag, src_x, dst_tag, dst_x, round, st);
+  if (src_dtype == NEO_F32 && dst_dtype == NEO_BF16)
+    return dispatch_layout<float, __nv_bfloat16>(src, dst, n, c, h, w, src_tag, src_x, dst_tag, dst_x, round, st);
+  if (src_dtype == NEO_BF16 && dst_dtype == NEO_F32)
+    return dispatch_layout<__nv_bfloat16, float>(src, dst, n, c, h, w, src_tag, src_x, dst_tag, dst_x, round, st);
+  return dispatch_layout<__nv_bfloat16, __nv_bfloat16>(src, dst, n, c, h, w, src_tag, src_x, dst_tag, dst_x, round, st);
+}
+
+static int weights_common(int dtype, const void* src, void* dst, int64_t k, int64_t c, int64_t r,
+                          int64_t s, int x, int y, bool pack, cudaStream_t st) {
+  NEO_CHECK_ARG(src && dst, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(k >= 1 && c >= 1 && r >= 1 && s >= 1, NEO_ERR_SHAPE_MISMATCH, "non-positive dim");
+  NEO_CHECK_ARG(x >= 1 && y >= 1, NEO_ERR_WRONG_LAYOUT, "KCRS[x]c[y]k needs x >= 1 and y >= 1");
+  NEO_CHECK_ARG(c % x == 0 && k % y == 0, NEO_ERR_INDIVISIBLE_CHANNEL,
+                "(K=%lld, C=%lld) not divisible by (y=%d, x=%d)", (long long)k, (long long)c, y, x);
+  const int64_t total = k * c * r * s;
+  if (dtype == NEO_BF16)
+    weights_kernel<uint16_t><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), k, c, r * s, x, y, pack);
+  else
+    weights_kernel<uint32_t><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), k, c, r * s, x, y, pack);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_pack_weights(int dtype, const void* src, void* dst, int64_t k, int64_t c,
+                                int64_t r, int64_t s, int x, int y, neo_stream_t stream) {
+  return weights_common(dtype, src, dst, k, c, r, s, x, y, true, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int neo_unpack_weights(int dtype, const void* src, void* dst, int64_t k, int64_t c,
+                                  int64_t r, int64_t s, int x, int y, neo_stream_t stream) {
+  return weights_common(dtype, src, dst, k, c, r, s, x, y, false, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_dtype, int64_t k,
+                                     int64_t c, int64_t r, int64_t s, int x,
+                                     int64_t slices_padded, int flags, neo_stream_t stream) {
+  NEO_CHECK_ARG(src_kcrs && dst, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(k >= 1 && c >= 1 && r >= 1 && s >= 1 && x >= 1, NEO_ERR_SHAPE_MISMATCH,
+                "non-positive dim");
+  const int64_t nslices = r * s * neo_ceil_div(c, x);
+  NEO_CHECK_ARG((flags & NEO_FLAG_PAD_CHANNELS) || c % x == 0, NEO_ERR_INDIVISIBLE_CHANNEL,
+                "C=%lld not divisible by x=%d", (long long)c, x);
+  if (slices_padded < nslices) slices_padded = nslices;
+  const int64_t total = slices_padded * k * x;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  if (dst_dtype == NEO_BF16)
+    weights_umma_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        src_kcrs, static_cast<__nv_bfloat16*>(dst), k, c, r, s, x, slices_padded, nslices, round);
+  else
+    weights_umma_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        src_kcrs, static_cast<float*>(dst), k, c, r, s, x, slices_padded, nslices, round);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}

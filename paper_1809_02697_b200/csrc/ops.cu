@@ -1,0 +1,282 @@
+// Memory-bound operators on the blocked layout (reference executor.py:96-203):
+// K-POOL, K-ELTWISE, K-CONCAT, K-DENSE (SIMT, HBM-bound weight stream) and
+// K-SOFTMAX.  Channel-blocked tensors are (n, cb, hw, x) with x innermost, so
+// consecutive threads take consecutive lanes / pixels and every access is
+// coalesced; fp32 arithmetic follows the reference's numpy op order.
+#include <cfloat>
+
+#include "neo_common.cuh"
+
+namespace {
+
+int64_t grid_for(int64_t total, int threads = 256) {
+  return std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, threads), 148 * 32));
+}
+
+// _pool2d (executor.py:103-128): max pads with -inf, avg pads with 0 and
+// divides by win*win; window taps visited r-major like the reference
+template <typename T>
+__global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t N, int64_t Cb,
+                            int H, int W, int OH, int OW, int x, int win, int stride, int pad,
+                            bool is_max, bool round) {
+  const int64_t total = N * Cb * OH * OW * x;
+  const float inv = (float)(win * win);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int j = (int)(t % x);
+    t /= x;
+    const int ow = (int)(t % OW);
+    t /= OW;
+    const int oh = (int)(t % OH);
+    const int64_t plane = t / OH;  // n*Cb + cb
+    const T* src = in + plane * H * W * x + j;
+    float acc = is_max ? -INFINITY : 0.f;
+    bool first = true;
+    for (int r = 0; r < win; ++r) {
+      const int ih = oh * stride + r - pad;
+      for (int s = 0; s < win; ++s) {
+        const int iw = ow * stride + s - pad;
+        const bool inb = ih >= 0 && ih < H && iw >= 0 && iw < W;
+        const float v = inb ? Elem<T>::to_f(src[((int64_t)ih * W + iw) * x]) : (is_max ? -INFINITY : 0.f);
+        if (first) {
+          acc = v;
+          first = false;
+        } else if (is_max) {
+          acc = fmaxf(acc, v);
+        } else {
+          acc = __fadd_rn(acc, v);
+        }
+      }
+    }
+    if (!is_max) acc = __fdiv_rn(acc, inv);
+    if (round) acc = neo_round_tf32(acc);
+    out[i] = Elem<T>::from_f(acc);
+  }
+}
+
+template <typename T>
+__global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                               const float* __restrict__ scale, const float* __restrict__ shift,
+                               int64_t total, int64_t Cb, int64_t HW, int x, int op, bool round) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = Elem<T>::to_f(a[i]);
+    switch (op) {
+      case NEO_ELT_RELU: v = fmaxf(v, 0.f); break;
+      case NEO_ELT_ADD: v = __fadd_rn(v, Elem<T>::to_f(b[i])); break;
+      case NEO_ELT_ADD_RELU: v = fmaxf(__fadd_rn(v, Elem<T>::to_f(b[i])), 0.f); break;
+      default: {
+        const int64_t j = i % x;
+        const int64_t cb = (i / ((int64_t)x * HW)) % Cb;
+        const int64_t ch = cb * x + j;
+        // executor.py:180-181: a * scale + shift as two rounded numpy ops
+        v = __fadd_rn(__fmul_rn(v, scale[ch]), shift[ch]);
+        if (op == NEO_ELT_SCALE_SHIFT_RELU) v = fmaxf(v, 0.f);
+      }
+    }
+    if (round) v = neo_round_tf32(v);
+    out[i] = Elem<T>::from_f(v);
+  }
+}
+
+template <typename T>
+__global__ void concat_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t outer,
+                              int64_t chunk, int64_t dst_row, int64_t dst_off) {
+  const int64_t total = outer * chunk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / chunk, c = i % chunk;
+    dst[o * dst_row + dst_off + c] = src[i];
+  }
+}
+
+// 16-byte vector variant when every row boundary is 16-byte aligned
+__global__ void concat_kernel_v4(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                 int64_t outer, int64_t chunk, int64_t dst_row, int64_t dst_off) {
+  const int64_t total = outer * chunk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / chunk, c = i % chunk;
+    dst[o * dst_row + dst_off + c] = src[i];
+  }
+}
+
+// Dense: one warp per output unit, all (<= 8 per pass) batch rows at once so
+// each weight row streams from HBM exactly once per pass.
+template <typename T, int NB>
+__global__ void dense_kernel(const T* __restrict__ a, const T* __restrict__ w,
+                             const float* __restrict__ bias, float* __restrict__ out, int64_t n,
+                             int64_t in_f, int64_t units) {
+  const int warps = blockDim.x / 32;
+  const int64_t u = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (u >= units) return;
+  const T* wr = w + u * in_f;
+  for (int64_t n0 = blockIdx.y * NB; n0 < n; n0 += (int64_t)gridDim.y * NB) {
+    float acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+    for (int64_t i = lane; i < in_f; i += 32) {
+      const float wv = Elem<T>::to_f(wr[i]);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (n0 + b < n) acc[b] = fmaf(Elem<T>::to_f(a[(n0 + b) * in_f + i]), wv, acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float v = acc[b];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && n0 + b < n) out[(n0 + b) * units + u] = bias ? v + bias[u] : v;
+    }
+  }
+}
+
+// softmax over the last axis: e = exp(a - max); e / sum(e)   (executor.py:167-170)
+__global__ void softmax_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t rows,
+                               int64_t cols) {
+  __shared__ float red[32];
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const float* a = in + row * cols;
+    float* o = out + row * cols;
+    float mx = -INFINITY;
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) mx = fmaxf(mx, a[i]);
+    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
+      for (int s = 16; s > 0; s >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, s));
+      if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float sum = 0.f;
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) {
+      const float e = expf(a[i] - mx);
+      o[i] = e;
+      sum += e;
+    }
+    for (int s = 16; s > 0; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = sum;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+      for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+      if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = red[0];
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) o[i] = o[i] / inv;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+extern "C" int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb,
+                          int64_t h, int64_t w, int x, int win, int stride, int pad, int flags,
+                          neo_stream_t stream) {
+  NEO_CHECK_ARG(in && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(win >= 1 && stride >= 1 && pad >= 0 && x >= 1, NEO_ERR_INVALID_ARG,
+                "bad pool window/stride/pad");
+  const int64_t OH = (h + 2 * pad - win) / stride + 1, OW = (w + 2 * pad - win) / stride + 1;
+  NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "pool has empty output");
+  const int64_t total = n * cb * OH * OW * x;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  if (dtype == NEO_BF16)
+    pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
+        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+  else
+    pool_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
+        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_eltwise(int dtype, int op, const void* a, const void* b, void* out,
+                           const float* scale, const float* shift, int64_t n, int64_t cb,
+                           int64_t hw, int x, int flags, neo_stream_t stream) {
+  NEO_CHECK_ARG(a && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(op >= 0 && op <= 4, NEO_ERR_INVALID_ARG, "bad eltwise op %d", op);
+  NEO_CHECK_ARG(!(op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) || b, NEO_ERR_INVALID_ARG,
+                "add needs two inputs");
+  NEO_CHECK_ARG(op < NEO_ELT_SCALE_SHIFT || (scale && shift), NEO_ERR_INVALID_ARG,
+                "scale/shift needs both vectors");
+  const int64_t total = n * cb * hw * x;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  if (dtype == NEO_BF16)
+    eltwise_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
+        static_cast<__nv_bfloat16*>(out), scale, shift, total, cb, hw, x, op, round);
+  else
+    eltwise_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out), scale,
+        shift, total, cb, hw, x, op, round);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_concat_copy(int dtype, const void* src, void* dst, int64_t outer, int64_t chunk,
+                               int64_t dst_row, int64_t dst_off, neo_stream_t stream) {
+  NEO_CHECK_ARG(src && dst, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(outer >= 0 && chunk >= 0 && dst_off + chunk <= dst_row, NEO_ERR_SHAPE_MISMATCH,
+                "concat slice out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t es = neo_dtype_size(dtype);
+  const int64_t per = 16 / es;
+  if (outer * chunk == 0) return NEO_OK;
+  if (chunk % per == 0 && dst_row % per == 0 && dst_off % per == 0 &&
+      ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0) {
+    const int64_t total = outer * (chunk / per);
+    concat_kernel_v4<<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), outer, chunk / per,
+        dst_row / per, dst_off / per);
+  } else if (es == 2) {
+    concat_kernel<uint16_t><<<(unsigned)grid_for(outer * chunk), 256, 0, st>>>(
+        static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), outer, chunk, dst_row,
+        dst_off);
+  } else {
+    concat_kernel<uint32_t><<<(unsigned)grid_for(outer * chunk), 256, 0, st>>>(
+        static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), outer, chunk, dst_row,
+        dst_off);
+  }
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_dense(int dtype, const void* a, const void* w, const float* bias, float* out,
+                         int64_t n, int64_t in_features, int64_t units, neo_stream_t stream) {
+  NEO_CHECK_ARG(a && w && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(n >= 1 && in_features >= 1 && units >= 1, NEO_ERR_SHAPE_MISMATCH, "bad dense dims");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  constexpr int NB = 8;
+  const int threads = 256;
+  dim3 grid((unsigned)neo_ceil_div(units, threads / 32),
+            (unsigned)std::min<int64_t>(neo_ceil_div(n, NB), 65535));
+  if (dtype == NEO_BF16)
+    dense_kernel<__nv_bfloat16, NB><<<grid, threads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(w), bias, out, n,
+        in_features, units);
+  else
+    dense_kernel<float, NB><<<grid, threads, 0, st>>>(static_cast<const float*>(a),
+                                                      static_cast<const float*>(w), bias, out, n,
+                                                      in_features, units);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_softmax(const float* in, float* out, int64_t rows, int64_t cols,
+                           neo_stream_t stream) {
+  NEO_CHECK_ARG(in && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(rows >= 1 && cols >= 1, NEO_ERR_SHAPE_MISMATCH, "bad softmax dims");
+  softmax_kernel<<<(unsigned)std::min<int64_t>(rows, 148 * 8), 256, 0,
+                   static_cast<cudaStream_t>(stream)>>>(in, out, rows, cols);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}

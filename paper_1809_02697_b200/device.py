@@ -1,0 +1,185 @@
+"""Device-side operator calls: thin typed wrappers that pass torch CUDA
+tensors (allocation only) to libneob200 through ctypes.  Every function is
+stream-ordered on the current torch stream and raises the reference
+exception types on failure.  No function here has a CPU path."""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib as L
+from . import errors as E
+
+_DT = {torch.float32: L.F32, torch.bfloat16: L.BF16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise E.InputMismatch(f"unsupported dtype {t.dtype}") from None
+
+
+def torch_dtype(code: int) -> torch.dtype:
+    return torch.bfloat16 if code == L.BF16 else torch.float32
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise E.InputMismatch("device operators take CUDA tensors")
+    if not t.is_contiguous():
+        raise E.InputMismatch("device operators take contiguous tensors")
+    return t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _tag(layout) -> tuple[int, int]:
+    """(tag, x) of a Layout or layout string."""
+    s = str(layout)
+    if s == "NCHW":
+        return L.NCHW_TAG, 1
+    if s == "NHWC":
+        return L.NHWC_TAG, 1
+    if s.startswith("NCHW") and s.endswith("c"):
+        return L.NCHWC_TAG, int(s[4:-1])
+    raise E.WrongLayout(f"not a feature-map layout: {s}")
+
+
+def layout_transform(src: torch.Tensor, dst: torch.Tensor, n: int, c: int, h: int, w: int,
+                     src_layout, dst_layout, flags: int = 0, stream=None) -> None:
+    st, sx = _tag(src_layout)
+    dt, dx = _tag(dst_layout)
+    L.call("neo_layout_transform", dtype_code(src), dtype_code(dst), _ptr(src), _ptr(dst),
+           n, c, h, w, st, sx, dt, dx, flags, stream_handle(stream))
+
+
+def pack_weights(src: torch.Tensor, dst: torch.Tensor, x: int, y: int, stream=None) -> None:
+    k, c, r, s = src.shape
+    L.call("neo_pack_weights", dtype_code(src), _ptr(src), _ptr(dst), k, c, r, s, x, y,
+           stream_handle(stream))
+
+
+def unpack_weights(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
+    ko, co, r, s, x, y = src.shape
+    L.call("neo_unpack_weights", dtype_code(src), _ptr(src), _ptr(dst), ko * y, co * x, r, s,
+           x, y, stream_handle(stream))
+
+
+def umma_slices(mode: int, c: int, r: int, s: int, x: int) -> int:
+    return int(L.load().neo_conv_umma_slices(mode, c, r, s, x, 1))
+
+
+def pack_weights_umma(w_kcrs: torch.Tensor, x: int, mode: int, pad_channels: bool = False,
+                      stream=None) -> torch.Tensor:
+    """Device-private slice-major weight image for the tensor-core conv."""
+    if w_kcrs.dtype != torch.float32:
+        raise E.InputMismatch("umma weight packing takes f32 KCRS")
+    k, c, r, s = w_kcrs.shape
+    slices = umma_slices(mode, c, r, s, x)
+    dt = L.BF16 if mode == L.MODE_BF16 else L.F32
+    out = torch.empty(slices * k * x, dtype=torch_dtype(dt), device=w_kcrs.device)
+    flags = (L.FLAG_ROUND_TF32 if mode == L.MODE_TF32 else 0) | \
+        (L.FLAG_PAD_CHANNELS if pad_channels else 0)
+    L.call("neo_pack_weights_umma", _ptr(w_kcrs), _ptr(out), dt, k, c, r, s, x, slices, flags,
+           stream_handle(stream))
+    return out
+
+
+def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 0), ic_bn=1,
+                oc_bn=1, scale=None, shift=None, bias=None, residual=None, relu=False,
+                x_cb=(0, 0), out_cb=(0, 0), res_cb=(0, 0), flags=0, tile=None) -> L.ConvParams:
+    p = L.ConvParams()
+    p.mode = mode
+    p.x, p.w, p.out = _ptr(x), _ptr(w), _ptr(out)
+    p.scale, p.shift, p.bias, p.residual = _ptr(scale), _ptr(shift), _ptr(bias), _ptr(residual)
+    p.relu = int(bool(relu))
+    p.n, p.c, p.h, p.w_in, p.k, p.r, p.s = n, c, h, w_in, k, r, s
+    p.stride_h, p.stride_w = stride
+    p.pad_h, p.pad_w = pad
+    p.ic_bn, p.oc_bn = ic_bn, oc_bn
+    p.x_cb_offset, p.x_cb_total = x_cb
+    p.out_cb_offset, p.out_cb_total = out_cb
+    p.res_cb_offset, p.res_cb_total = res_cb
+    p.out_dtype = dtype_code(out)
+    p.flags = flags
+    if tile:
+        for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages"):
+            setattr(p, key, int(tile.get(key, 0) or 0))
+    return p
+
+
+def conv2d(p: L.ConvParams, stream=None) -> None:
+    L.call("neo_conv2d_nchwc_fused", ctypes.byref(p), stream_handle(stream))
+
+
+def default_tiles(p: L.ConvParams) -> dict:
+    q = L.ConvParams.from_buffer_copy(p)
+    L.check(L.load().neo_conv_default_tiles(ctypes.byref(q)), "neo_conv_default_tiles")
+    return {k: getattr(q, k) for k in ("tile_w", "tile_h", "tile_img", "tile_n",
+                                        "slices_per_stage", "stages")}
+
+
+def pool2d(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, flags=0, stream=None):
+    L.call("neo_pool2d", dtype_code(inp), L.POOL_MAX if mode == "max" else L.POOL_AVG,
+           _ptr(inp), _ptr(out), n, cb, h, w, x, win, stride, pad, flags, stream_handle(stream))
+
+
+def eltwise(op: int, a, b, out, n, cb, hw, x, scale=None, shift=None, flags=0, stream=None):
+    L.call("neo_eltwise", dtype_code(a), op, _ptr(a), _ptr(b), _ptr(out), _ptr(scale),
+           _ptr(shift), n, cb, hw, x, flags, stream_handle(stream))
+
+
+def concat_copy(src, dst, outer, chunk, dst_row, dst_off, stream=None):
+    L.call("neo_concat_copy", dtype_code(src), _ptr(src), _ptr(dst), outer, chunk, dst_row,
+           dst_off, stream_handle(stream))
+
+
+def dense(a, w, bias, out, n, in_f, units, stream=None):
+    L.call("neo_dense", dtype_code(a), _ptr(a), _ptr(w), _ptr(bias), _ptr(out), n, in_f, units,
+           stream_handle(stream))
+
+
+def softmax(inp, out, rows, cols, stream=None):
+    L.call("neo_softmax", _ptr(inp), _ptr(out), rows, cols, stream_handle(stream))
+
+
+class CapturedGraph:
+    """A whole-forward CUDA graph captured from libneob200 launches."""
+
+    def __init__(self, handle: int):
+        self.handle = handle
+
+    def launch(self, stream=None) -> None:
+        L.call("neo_graph_launch", self.handle, stream_handle(stream))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.load().neo_graph_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def capture(fn, stream=None) -> CapturedGraph:
+    """Run ``fn`` under stream capture and return the instantiated graph."""
+    s = stream or torch.cuda.current_stream()
+    L.call("neo_capture_begin", stream_handle(s))
+    try:
+        fn()
+    except BaseException:
+        h = ctypes.c_void_p()
+        L.load().neo_capture_end(stream_handle(s), ctypes.byref(h))
+        if h.value:
+            L.load().neo_graph_destroy(h)
+        raise
+    h = ctypes.c_void_p()
+    L.call("neo_capture_end", stream_handle(s), ctypes.byref(h))
+    return CapturedGraph(h.value)

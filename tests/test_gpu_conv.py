@@ -1,0 +1,226 @@
+"""Parity of the device conv (tcgen05 bf16 / tf32 and SIMT fp32) against the
+CPU oracle, through the C-ABI.  Reference tests mirrored:
+tests/test_kernels.py:71-125 (workload/schedule edge cases), :167-186
+(epilogue order and residual)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.ops import pack_nchw, unpack_nchw, pack_kcrs
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_round(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
+
+
+def tf32_round(a):
+    """RN (ties away) to tf32, like cvt.rna.tf32.f32."""
+    b = np.ascontiguousarray(a, np.float32).view(np.uint32).copy()
+    finite = np.isfinite(a)
+    b[finite] = (b[finite] + np.uint32(0x1000)) & np.uint32(0xFFFFE000)
+    return b.view(np.float32)
+
+
+def run_conv(mode, x_nchw, w_kcrs, stride, pad, ic_bn, oc_bn, scale=None, shift=None,
+             bias=None, residual=None, relu=False, out_f32=True, tile=None, pad_channels=False,
+             out_cb=None):
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    dev = torch.device("cuda:0")
+    n, c, h, w = x_nchw.shape
+    k, _, r, s = w_kcrs.shape
+    sh, sw = stride
+    ph, pw = pad
+    oh = (h + 2 * ph - r) // sh + 1
+    ow = (w + 2 * pw - s) // sw + 1
+    if mode == L.MODE_BF16:
+        act = torch.bfloat16
+    else:
+        act = torch.float32
+    cb = -(-c // ic_bn)
+    xpad = np.zeros((n, cb * ic_bn, h, w), np.float32)
+    xpad[:, :c] = x_nchw
+    xb = torch.from_numpy(pack_nchw(xpad, ic_bn)).to(dev).to(act)
+    if mode == L.MODE_FP32:
+        wdev = torch.from_numpy(pack_kcrs(w_kcrs, ic_bn, oc_bn)).to(dev)
+    else:
+        wdev = D.pack_weights_umma(torch.from_numpy(w_kcrs).to(dev), ic_bn, mode,
+                                   pad_channels=pad_channels)
+    out_dt = torch.float32 if (out_f32 or mode != L.MODE_BF16) else torch.bfloat16
+    kb = k // oc_bn
+    total_cb, off = (kb, 0) if out_cb is None else out_cb
+    out = torch.full((n, total_cb, oh, ow, oc_bn), float("nan"), dtype=out_dt, device=dev)
+    t = lambda v: None if v is None else torch.from_numpy(np.asarray(v, np.float32)).to(dev)
+    res = None
+    if residual is not None:
+        res = torch.from_numpy(pack_nchw(residual, oc_bn)).to(dev).to(out_dt)
+    p = D.conv_params(mode, xb, wdev, out, n, c, h, w, k, r, s, (sh, sw), (ph, pw), ic_bn,
+                      oc_bn, t(scale), t(shift), t(bias), res, relu,
+                      out_cb=(off, total_cb) if out_cb else (0, 0),
+                      flags=(L.FLAG_PAD_CHANNELS if pad_channels else 0), tile=tile)
+    D.conv2d(p)
+    torch.cuda.synchronize()
+    o = out.float().cpu().numpy()
+    if out_cb is not None:
+        return o
+    return unpack_nchw(o)
+
+
+CASES = [
+    # (n, c, h, w, k, r, s, stride, pad)
+    (1, 64, 56, 56, 64, 3, 3, (1, 1), (1, 1)),      # BASELINE C0
+    (2, 64, 14, 14, 128, 1, 1, (1, 1), (0, 0)),     # 1x1
+    (2, 64, 28, 28, 128, 1, 1, (2, 2), (0, 0)),     # 1x1 stride 2 (downsample)
+    (1, 64, 29, 29, 64, 3, 3, (2, 2), (1, 1)),      # 3x3 stride 2, odd size
+    (3, 128, 7, 7, 256, 3, 3, (1, 1), (1, 1)),      # 7x7 maps, several images per tile
+    (1, 64, 17, 17, 96, 1, 7, (1, 1), (0, 3)),      # Inception 1x7 asymmetric pad
+    (1, 64, 17, 17, 80, 7, 1, (1, 1), (3, 0)),      # Inception 7x1, K=80
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+def test_tc_conv_accumulate(cuda, case, mode_name):
+    """Operands pre-rounded to the tensor-core type, f32 output: any error is
+    accumulation order only."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, r, s, st, pd = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    wt = (rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x, wt = rnd(x), rnd(wt)
+    ref = oracle.conv2d(x, wt, st, pd)
+    x_bn = 64 if mode_name == "bf16" else 32
+    x_bn = min(x_bn, c)
+    got = run_conv(mode, x, wt, st, pd, x_bn, 16 if k % 16 == 0 else 8)
+    assert got.shape == ref.shape
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("x_bn", [8, 16, 32, 64])
+def test_tc_conv_block_sizes(cuda, x_bn):
+    """Every GPU-legal input block size (16..128-byte rows) in bf16."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(x_bn)
+    x = bf16_round(rng.standard_normal((2, 64, 12, 12)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((48, 64, 3, 3)) * 0.06).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 1, 1)
+    for y in (16, 48):
+        got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), x_bn, y)
+        assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_tc_conv_epilogue_order(cuda):
+    """scale/shift -> bias -> residual -> relu (kernels.py:185-197)."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(7)
+    x = tf32_round(rng.standard_normal((1, 32, 10, 10)).astype(np.float32))
+    wt = tf32_round((rng.standard_normal((32, 32, 3, 3)) * 0.08).astype(np.float32))
+    scale = rng.uniform(0.5, 1.5, 32).astype(np.float32)
+    shift = rng.uniform(-1, 1, 32).astype(np.float32)
+    bias = rng.uniform(-1, 1, 32).astype(np.float32)
+    res = rng.standard_normal((1, 32, 10, 10)).astype(np.float32)
+    ref = oracle.conv2d(x, wt, 1, 1, scale, shift, bias, res, True)
+    got = run_conv(L.MODE_TF32, x, wt, (1, 1), (1, 1), 16, 16, scale, shift, bias, res, True)
+    assert oracle.rel_err(got, ref) < 1e-4
+    assert (got >= 0).all()
+
+
+def test_tc_conv_stem_padded_channels(cuda):
+    """ResNet stem: C=3 padded to one 8-lane block, 7x7 stride 2 pad 3."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(3)
+    x = bf16_round(rng.standard_normal((2, 3, 64, 64)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((64, 3, 7, 7)) * 0.1).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 2, 3)
+    got = run_conv(L.MODE_BF16, x, wt, (2, 2), (3, 3), 8, 64, pad_channels=True)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_tc_conv_odd_out_channels(cuda):
+    """SSD class head: K = 84 = 4 anchors x 21 classes, y = 84 (scalar epilogue)."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(5)
+    x = bf16_round(rng.standard_normal((2, 64, 10, 10)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((84, 64, 3, 3)) * 0.05).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 1, 1)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 84)
+    assert oracle.rel_err(got, ref) < 1e-4
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 12)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_tc_conv_concat_window(cuda):
+    """Output written into a channel-block window of a wider buffer (concat in place)."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(11)
+    x = bf16_round(rng.standard_normal((1, 32, 8, 8)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((32, 32, 3, 3)) * 0.1).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 1, 1)
+    o = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 32, 16, out_cb=(5, 2))
+    got = unpack_nchw(o[:, 2:4])
+    assert oracle.rel_err(got, ref) < 1e-4
+    assert np.isnan(o[:, :2]).all() and np.isnan(o[:, 4:]).all()
+
+
+@pytest.mark.parametrize("tile", [
+    dict(tile_w=8, tile_h=8, tile_img=1, tile_n=32, slices_per_stage=1, stages=2),
+    dict(tile_w=14, tile_h=9, tile_img=1, tile_n=64, slices_per_stage=3, stages=2),
+    dict(tile_w=7, tile_h=7, tile_img=2, tile_n=128, slices_per_stage=2, stages=3),
+    dict(tile_w=28, tile_h=4, tile_img=1, tile_n=256, slices_per_stage=1, stages=4),
+])
+def test_tc_conv_tile_configs(cuda, tile):
+    """Explicit tile / pipeline configurations (the tuner's search space)."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(13)
+    x = bf16_round(rng.standard_normal((2, 128, 14, 14)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((256, 128, 3, 3)) * 0.03).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 1, 1)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, tile=tile)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_bf16_end_to_end_c0(cuda):
+    """BASELINE config 0 in bf16 storage: within the north_star 2e-2."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((1, 64, 56, 56)).astype(np.float32)
+    wt = (rng.standard_normal((64, 64, 3, 3)) * np.sqrt(2 / 576)).astype(np.float32)
+    scale = rng.uniform(0.5, 1.5, 64).astype(np.float32)
+    shift = rng.normal(0, 0.1, 64).astype(np.float32)
+    ref = oracle.conv2d(x, wt, 1, 1, scale, shift, relu=True)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, scale, shift, relu=True,
+                   out_f32=False)
+    assert oracle.rel_err(got, ref) < 2e-2
+
+
+@pytest.mark.parametrize("case", CASES[:4])
+def test_fp32_direct_matches_oracle(cuda, case):
+    """SIMT fp32 path (NEO_MODE_FP32) within the reference's 1e-5 (Acceptance 1)."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, r, s, st, pd = case
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    wt = rng.standard_normal((k, c, r, s)).astype(np.float32)
+    ref = oracle.conv2d(x, wt, st, pd)
+    got = run_conv(L.MODE_FP32, x, wt, st, pd, 16, 16)
+    assert oracle.rel_err(got, ref) < 1e-5
+    got1 = run_conv(L.MODE_FP32, x, wt, st, pd, 1, 1)
+    assert oracle.rel_err(got1, ref) < 1e-5
+
+
+def test_tc_conv_deterministic(cuda):
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2, 64, 20, 20)).astype(np.float32)
+    wt = (rng.standard_normal((64, 64, 3, 3)) * 0.05).astype(np.float32)
+    a = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
+    b = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
+    assert np.array_equal(a, b)
