@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NCHW[x]c inference path (driver contract).
+
+Default workload: ResNet-50 v1 inference, batch 64 per GPU, 224x224, bf16
+tensor-core mode (BASELINE.json config 2; its headline metric is images/s at
+1/2/4/8 GPUs).  One process per GPU; under torchrun every rank compiles the
+same planned graph for its own batch shard (weak scaling, no collective on
+the hot path; NCCL/torch.distributed only for the barrier and the max-over-
+ranks of the timings).
+
+Prints ONE JSON line on rank 0.  ``value`` is device-resident throughput
+(input already in HBM, per-step CUDA events on the executor stream, L2
+flushed between steps); ``e2e`` is the same metric through the public
+DeviceProgram API with pinned host input copied in and the output read back
+every step.  ``roofline`` describes the dominant kernel (the tcgen05 conv,
+all conv launches of a step) from an instrumented pass with CUDA events
+around every conv launch.  ``cpu_baseline`` times the unmodified reference
+(neoplan, numba, all host cores) on a bounded sample.
+
+``--impl reference`` runs only the reference CPU implementation (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/s (1/2/4/8 GPU) and per-conv TFLOP/s as fraction of tensor-core peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
+    ap.add_argument("--mode", default="bf16", choices=["bf16", "tf32", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        loaded = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks() -> tuple[dict, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+# ---------------------------------------------------------------------------
+# reference CPU implementation (baseline / --impl reference)
+
+def reference_cpu(model: str, per_step: int, steps: int, warmup: int, seconds: float):
+    """images/s of the unmodified reference optimized executor on the host
+    cores, on ``per_step`` images per step; falls back to the oracle port."""
+    from paper_1809_02697_b200 import build_model, model_input
+    g = build_model(model, batch=per_step)
+    feeds = model_input(g)
+    try:
+        from oracle.refbridge import import_reference, reference_optimized, to_reference_graph
+        neo = import_reference()
+        ng = reference_optimized(to_reference_graph(g, neo), neo)
+        cores = neo.physical_cores()
+        pool = neo.ThreadPool(cores)
+        run = lambda: neo.execute(ng, feeds, pool)
+        kind = "reference"
+    except Exception as exc:   # reference not installed: numpy restatement
+        import oracle
+        cores = os.cpu_count() or 1
+        run = lambda: oracle.execute_reference(g, feeds)
+        kind = f"port ({type(exc).__name__})"
+    for _ in range(max(1, warmup)):
+        run()
+    times = []
+    t_end = time.perf_counter() + seconds
+    for i in range(max(1, steps)):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end and i + 1 >= 2:
+            break
+    total = float(np.sum(times))
+    return {"value": per_step * len(times) / total, "unit": "images/s", "cores": int(cores),
+            "kind": "reference" if kind == "reference" else "port",
+            "sample": f"{model} batch {per_step} x {len(times)} steps "
+                      f"({kind}, optimized graph, ThreadPool over physical cores)",
+            "seconds": total}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = 2
+    res = reference_cpu(args.model, per_step, args.steps, args.warmup, 1e9)
+    ms = 1000.0 * res["seconds"] / max(1, args.steps)
+    line = {"metric": METRIC, "value": res["value"], "unit": "images/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1), random init)",
+            "config": {"workload": f"{args.model} inference, {per_step} images/step sample of the "
+                                   f"batch-{args.batch} workload, 224x224, reference CPU path",
+                       "model": args.model},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "images/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind: str):
+    """Instrumented pass: CUDA events around every conv launch on the
+    executor stream; returns (roofline dict, conv share of the step)."""
+    import torch
+    conv_idx = [i for i, n in enumerate(prog.launch_names) if n.startswith("conv")]
+    totals = []
+    step_times = []
+    for _ in range(steps):
+        evs = []
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(prog.stream)
+        for i, fn in enumerate(prog.launches):
+            if i in conv_idx:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(prog.stream)
+                fn()
+                b.record(prog.stream)
+                evs.append((a, b))
+            else:
+                fn()
+        s1.record(prog.stream)
+        s1.synchronize()
+        totals.append(sum(a.elapsed_time(b) for a, b in evs) * 1e-3)
+        step_times.append(s0.elapsed_time(s1) * 1e-3)
+    conv_s = float(np.median(totals))
+    achieved = flops_per_step / conv_s / 1e12
+    pk = float(peak.get("bf16_tflops_sustained", peak.get("bf16_tflops", 1400.0)))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_step")
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+            "frac": achieved / pk, "traffic": traffic,
+            "kernel": "conv_tc_kernel (all %d conv launches of one step)" % len(conv_idx),
+            "conv_ms_per_step": conv_s * 1e3, "peak_source": f"{peak_kind} bf16 sustained"}
+    return roof, conv_s / float(np.median(step_times))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, build_model, compile_graph,
+                                       model_input)
+    from paper_1809_02697_b200.models import conv_flops
+
+    g = build_model(args.model, batch=args.batch)
+    flops_step = float(conv_flops(g))
+    planned = compile_graph(g, mode=args.mode)
+    prog = DeviceProgram(ExecutablePlan.compile(planned), local, args.mode)
+    feeds = model_input(g, seed=1 + rank)
+    name = prog.input_names()[0]
+    pinned = torch.from_numpy(feeds[name]).pin_memory()
+    out_t = prog.output_tensors()[0]
+    out_host = torch.empty(out_t.shape, dtype=out_t.dtype).pin_memory()
+    stream = prog.stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=local)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident throughput ------------------------------------
+    prog.set_inputs(feeds)
+    for _ in range(max(3, args.warmup)):
+        prog.launch()
+    stream.synchronize()
+    barrier()
+    evs = []
+    with ClockSampler(local) as clocks:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)          # L2 flush between steps, outside the events
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            prog.launch()
+            b.record(stream)
+            evs.append((a, b))
+        stream.synchronize()
+        wall = time.perf_counter() - wall0
+    barrier()
+    dev_s = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
+    # ---- end to end through the public API (pinned host in, result out) --
+    e2e_evs = []
+    for i in range(args.steps + args.warmup):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        prog.set_inputs({name: pinned})
+        prog.launch()
+        with torch.cuda.stream(stream):
+            out_host.copy_(out_t, non_blocking=True)
+        b.record(stream)
+        if i >= args.warmup:
+            e2e_evs.append((a, b))
+    stream.synchronize()
+    barrier()
+    e2e_s = sum(a.elapsed_time(b) for a, b in e2e_evs) * 1e-3
+    # ---- dominant-kernel roofline (instrumented, un-graphed pass) -------
+    pk, pk_kind = peaks()
+    roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind)
+    barrier()
+
+    times = torch.tensor([dev_s, e2e_s, wall], dtype=torch.float64, device=local)
+    if world > 1:
+        torch.distributed.all_reduce(times, op=torch.distributed.ReduceOp.MAX)
+    dev_s, e2e_s, wall = times.tolist()
+    images = args.batch * world * args.steps
+    value = images / dev_s
+    e2e_value = images / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = reference_cpu(args.model, 2, 50, 1, args.cpu_seconds)
+            cpu.pop("seconds", None)
+        except Exception as exc:
+            cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * dev_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.mode,
+            "data": "synthetic (seeded N(0,1) input, random-init weights)",
+            "config": {"workload": f"{args.model} v1 inference, batch {args.batch} per GPU, "
+                                   f"224x224, {args.mode} tensor-core NCHW[x]c path",
+                       "model": args.model, "global_batch": args.batch * world,
+                       "per_gpu_batch": args.batch, "image": 224,
+                       "parallelism": f"dp{world} batch sharding (no collective)",
+                       "l2": "flushed between timed steps (256 MiB write outside the events)",
+                       "conv_gflop_per_image": flops_step / args.batch / 1e9,
+                       "wall_s_timed_region": wall},
+            "e2e": {"value": e2e_value, "unit": "images/s",
+                    "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
+                    "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size())},
+            "gpu_launches": prog.kernel_launches * args.steps,
+            "launches_per_step": prog.kernel_launches,
+            "roofline": roof,
+            "conv_share_of_step": conv_share,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -596,15 +596,25 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
   const int grid = (int)std::min<int64_t>(num_tiles, sm_count_of_current_device());
-  if (tf32) {
-    NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-    conv_tc_kernel<true><<<grid, kThreads, smem, stream>>>(kp);
-  } else {
-    NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-    conv_tc_kernel<false><<<grid, kThreads, smem, stream>>>(kp);
+  // opt in to the large dynamic shared memory once per (device, kernel); the
+  // attribute call is kept out of later launches so they can be graph-captured
+  static bool attr_set[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  bool& done = attr_set[dev & 63][tf32 ? 1 : 0];
+  if (!done) {
+    if (tf32)
+      NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    else
+      NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    done = true;
   }
+  if (tf32)
+    conv_tc_kernel<true><<<grid, kThreads, smem, stream>>>(kp);
+  else
+    conv_tc_kernel<false><<<grid, kThreads, smem, stream>>>(kp);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

@@ -183,3 +183,14 @@ def capture(fn, stream=None) -> CapturedGraph:
     h = ctypes.c_void_p()
     L.call("neo_capture_end", stream_handle(s), ctypes.byref(h))
     return CapturedGraph(h.value)
+
+
+def round_tf32(t: torch.Tensor) -> torch.Tensor:
+    """RN (ties away) rounding of an f32 device tensor to tf32 precision,
+    as a same-layout transform with the rounding flag."""
+    if t.dtype != torch.float32:
+        raise E.InputMismatch("round_tf32 takes f32")
+    out = torch.empty_like(t)
+    L.call("neo_layout_transform", L.F32, L.F32, _ptr(t), _ptr(out), 1, t.numel(), 1, 1,
+           L.NCHW_TAG, 1, L.NCHW_TAG, 1, L.FLAG_ROUND_TF32, stream_handle())
+    return out

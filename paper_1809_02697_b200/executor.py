@@ -1,0 +1,693 @@
+"""Graph executor: lowers a (planned or unplanned) graph onto libneob200.
+
+Reference surface kept (executor.py): ``ExecutablePlan.compile`` (:25-45),
+``execute(plan|graph, inputs, pool=None)`` (:131-218), ``benchmark`` (:221-236)
+and ``scalability_report`` (:239-247).  The reference interprets the graph in
+Python and allocates every intermediate in NumPy; here ``DeviceProgram``
+compiles it once per (device, mode):
+
+* every operator becomes one pre-bound libneob200 launch (conv with fused
+  epilogue, pool, eltwise, concat copy, dense, softmax, layout transform);
+* standalone BatchNorm followed by its only consumer ReLU runs as one fused
+  scale-shift-relu launch (DenseNet's pre-activations);
+* all intermediates live in one static arena with liveness-based reuse
+  (reference executor.py:211-216 only frees buffers; SPEC.md asks for a
+  planned arena);
+* the whole forward is captured once as a CUDA graph and replayed;
+* dtype rule: NCHW[x]c feature maps are stored in the mode's activation type
+  (bf16 in "bf16", tf32-rounded f32 in "tf32", f32 in "fp32"); everything
+  else (NCHW maps, matrices, logits, graph outputs) is f32;
+* a 3-channel (or otherwise tensor-core-illegal) packed graph input that
+  only feeds convs is physically packed with zero-padded lanes to the
+  smallest legal block (8 bf16 / 4 tf32 lanes), so the stem runs on the
+  tensor cores too.
+
+There is no CPU path: without libneob200 or a CUDA device every entry point
+raises.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import InputMismatch, ShapeMismatch
+from .graph import Graph, OpKind, hw_pair, infer_shapes, topo_sort, validate
+from .kernels import bytes_per_elem, tc_legal_block
+from .layout import Layout, host_unpack_kcrs
+from .runtime import DevicePool, resolve_pool
+
+
+@dataclass
+class ExecutablePlan:
+    """Validated graph + deterministic order + use counts (executor.py:25-45)."""
+
+    graph: Graph
+    order: list
+    refcounts: dict
+    input_ids: list
+    programs: dict = field(default_factory=dict, repr=False)
+
+    @classmethod
+    def compile(cls, g: Graph) -> "ExecutablePlan":
+        problems = validate(g)
+        if problems:
+            raise InputMismatch("invalid graph: " + "; ".join(problems))
+        order = topo_sort(g)
+        uses = {nid: 0 for nid in g.nodes}
+        for node in g.nodes.values():
+            for src, _ in node.inputs:
+                uses[src] += 1
+        for o in g.outputs:
+            uses[o] += 1
+        inputs = [nid for nid in order if g.nodes[nid].kind == OpKind.Input]
+        return cls(g, order, uses, inputs)
+
+
+# ---------------------------------------------------------------------------
+# device values and the arena
+
+@dataclass
+class _Val:
+    nid: int
+    shape: tuple          # physical storage shape
+    dtype: object         # torch dtype
+    layout: Layout        # logical layout
+    px: int = 0           # physical block size of an NCHW[x]c value
+    alias: int | None = None  # value whose storage this one views (Flatten)
+    first: int = 0
+    last: int = 0
+    offset: int = -1
+    tensor: object = None
+
+    @property
+    def nbytes(self) -> int:
+        import torch
+        return int(np.prod(self.shape)) * torch.empty((), dtype=self.dtype).element_size()
+
+
+def _plan_arena(vals: list[_Val], align: int = 256) -> int:
+    """Greedy first-fit offsets for non-overlapping lifetimes; returns size."""
+    placed: list[_Val] = []
+    for v in sorted(vals, key=lambda v: (-v.nbytes, v.first)):
+        size = -(-v.nbytes // align) * align
+        busy = sorted((p.offset, p.offset + (-(-p.nbytes // align) * align)) for p in placed
+                      if not (p.last < v.first or v.last < p.first))
+        off = 0
+        for lo, hi in busy:
+            if off + size <= lo:
+                break
+            off = max(off, hi)
+        v.offset = off
+        placed.append(v)
+    return max((p.offset + p.nbytes for p in placed), default=0)
+
+
+class DeviceProgram:
+    """One compiled forward of ``plan`` on ``device`` in ``mode``."""
+
+    def __init__(self, plan: ExecutablePlan, device: int = 0, mode: str = "bf16",
+                 keep=(), use_graph: bool = True):
+        import torch
+        from . import _lib as L
+        L.load()
+        if not torch.cuda.is_available():
+            raise InputMismatch("DeviceProgram needs a CUDA device")
+        self.plan = plan
+        self.g = plan.graph
+        self.mode = mode
+        self.device = torch.device("cuda", device)
+        self.keep = list(keep)
+        self.act_dtype = torch.bfloat16 if mode == "bf16" else torch.float32
+        self.round_flag = L.FLAG_ROUND_TF32 if mode == "tf32" else 0
+        self.launches: list = []        # zero-arg callables, in order
+        self.launch_names: list[str] = []
+        self.vals: dict[int, _Val] = {}
+        self.weights: list = []         # device tensors kept alive
+        self.graph_exec = None
+        self.use_graph = use_graph
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.Stream(self.device)
+            self._lower()
+            self._allocate()
+            self._bind()
+            torch.cuda.synchronize(self.device)   # weight images built on the side stream
+
+    # -- analysis ------------------------------------------------------------
+    def _lower(self):
+        import torch
+        g = self.g
+        self.specs = infer_shapes(g)
+        self.users = g.consumers()
+        order = self.plan.order
+        self.step = {nid: i for i, nid in enumerate(order)}
+        self.fused_bn_relu: dict[int, int] = {}   # relu id -> bn id
+        self.skip: set[int] = set()
+        for nid in order:
+            node = g.nodes[nid]
+            if node.kind == OpKind.BatchNorm and len(node.inputs) == 1:
+                us = self.users[nid]
+                if (len(us) == 1 and g.nodes[us[0]].kind == OpKind.ReLU
+                        and nid not in g.outputs and nid not in self.keep):
+                    self.fused_bn_relu[us[0]] = nid
+                    self.skip.add(nid)
+        # physical block size for tensor-core-illegal packed inputs
+        self.phys_x: dict[int, int] = {}
+        if self.mode in ("bf16", "tf32"):
+            min_lanes = 16 // bytes_per_elem(self.mode)
+            for nid in order:
+                node = g.nodes[nid]
+                if node.kind != OpKind.LayoutTransform:
+                    continue
+                dst = Layout.parse(node.attrs["dst_layout"])
+                if dst.tag != "NCHWc" or tc_legal_block(dst.x, self.mode):
+                    continue
+                src_layout = Layout.parse(node.attrs["src_layout"])
+                us = self.users[nid]
+                if (src_layout.tag == "NCHW" and us and nid not in g.outputs
+                        and all(g.nodes[u].kind == OpKind.Conv2d and g.nodes[u].inputs[0][0] == nid
+                                for u in us)):
+                    px = min_lanes
+                    while px < dst.x:
+                        px *= 2
+                    if tc_legal_block(px, self.mode):
+                        self.phys_x[nid] = px
+        for nid in order:
+            if nid in self.skip:
+                continue
+            node = g.nodes[nid]
+            if node.kind == OpKind.Constant:
+                continue
+            self.vals[nid] = self._make_val(nid)
+        # lifetimes
+        last_step = len(order)
+        for nid, v in self.vals.items():
+            v.first = self.step[nid]
+            v.last = self.step[nid]
+        for nid in order:
+            node = self.g.nodes[nid]
+            for src, _ in node.inputs:
+                tgt = self._storage(src)
+                if tgt is not None:
+                    tgt.last = max(tgt.last, self.step[nid])
+            if nid in self.fused_bn_relu.keys():
+                bn = self.fused_bn_relu[nid]
+                tgt = self._storage(self.g.nodes[bn].inputs[0][0])
+                tgt.last = max(tgt.last, self.step[nid])
+        for o in list(self.g.outputs) + self.keep:
+            tgt = self._storage(o)
+            if tgt is not None:
+                tgt.last = last_step
+        for nid in self.plan.input_ids:
+            self.vals[nid].first = -1
+
+    def _storage(self, nid) -> _Val | None:
+        v = self.vals.get(nid)
+        while v is not None and v.alias is not None:
+            v = self.vals[v.alias]
+        return v
+
+    def _make_val(self, nid) -> _Val:
+        import torch
+        spec = self.specs[nid]
+        node = self.g.nodes[nid]
+        layout = spec.layout
+        if node.kind == OpKind.Input and layout.tag == "NHWC":
+            layout = Layout("NCHW")
+            n, h, w, c = spec.shape
+            return _Val(nid, (n, c, h, w), torch.float32, layout)
+        if node.kind == OpKind.Flatten:
+            return _Val(nid, spec.shape, self.vals[node.inputs[0][0]].dtype, layout,
+                        alias=node.inputs[0][0])
+        if layout.tag == "NCHWc":
+            px = self.phys_x.get(nid, layout.x)
+            n, c, h, w = spec.logical_nchw
+            if nid in self.phys_x:
+                shape = (n, -(-c // px), h, w, px)
+            else:
+                shape = spec.shape
+            return _Val(nid, tuple(shape), self.act_dtype, layout, px=px)
+        return _Val(nid, tuple(spec.shape), torch.float32, layout)
+
+    # -- memory ----------------------------------------------------------------
+    def _allocate(self):
+        import torch
+        owners = [v for v in self.vals.values() if v.alias is None]
+        inputs = [v for v in owners if v.first < 0]
+        arena_vals = [v for v in owners if v.first >= 0]
+        size = _plan_arena(arena_vals)
+        self.arena = torch.empty(max(size, 256), dtype=torch.uint8, device=self.device)
+        self.arena_bytes = size
+        for v in arena_vals:
+            nb = v.nbytes
+            v.tensor = self.arena[v.offset:v.offset + nb].view(v.dtype).view(v.shape)
+        for v in inputs:
+            v.tensor = torch.empty(v.shape, dtype=v.dtype, device=self.device)
+        for v in self.vals.values():
+            if v.alias is not None:
+                base = self._storage(v.nid)
+                v.tensor = base.tensor.reshape(v.shape)
+
+    # -- launches --------------------------------------------------------------
+    def _emit(self, name, fn):
+        self.launches.append(fn)
+        self.launch_names.append(name)
+
+    def _upload(self, arr, dtype=None):
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(self.device)
+        if dtype is not None and dtype != torch.float32:
+            t = t.to(dtype)
+        self.weights.append(t)
+        return t
+
+    def _bind(self):
+        from . import device as D
+        g = self.g
+        for nid in self.plan.order:
+            node = g.nodes[nid]
+            kind = node.kind
+            if nid in self.skip or kind in (OpKind.Input, OpKind.Constant, OpKind.Flatten):
+                continue
+            out = self.vals[nid]
+            ins = [self.vals.get(src) for src, _ in node.inputs]
+            if kind == OpKind.Conv2d:
+                self._bind_conv(node, out)
+            elif kind == OpKind.LayoutTransform:
+                self._bind_transform(node, ins[0], out)
+            elif kind in (OpKind.MaxPool, OpKind.AvgPool):
+                self._bind_pool(node, ins[0], out)
+            elif kind == OpKind.ReLU:
+                if nid in self.fused_bn_relu:
+                    bn = g.nodes[self.fused_bn_relu[nid]]
+                    self._bind_scale_shift(bn, self.vals[bn.inputs[0][0]], out, relu=True)
+                else:
+                    self._bind_eltwise(D_ELT_RELU, ins[0], None, out)
+            elif kind == OpKind.BatchNorm:
+                self._bind_scale_shift(node, ins[0], out, relu=False)
+            elif kind == OpKind.ElementwiseAdd:
+                if ins[0].shape != ins[1].shape:
+                    raise ShapeMismatch(f"add {nid}: {ins[0].shape} vs {ins[1].shape}",
+                                        node_id=nid)
+                self._bind_eltwise(D_ELT_ADD, ins[0], ins[1], out)
+            elif kind == OpKind.Concat:
+                self._bind_concat(node, ins, out)
+            elif kind == OpKind.Dense:
+                self._bind_dense(node, ins[0], out)
+            elif kind == OpKind.Softmax:
+                self._bind_softmax(ins[0], out)
+            else:
+                raise InputMismatch(f"cannot execute node kind {kind}")
+        # graph outputs / kept values that ended up in bf16 get an f32 copy
+        self.out_vals = []
+        for o in list(g.outputs) + self.keep:
+            v = self.vals[o]
+            self.out_vals.append(v)
+        del D
+
+    # conv ---------------------------------------------------------------------
+    def _bind_conv(self, node, out: _Val):
+        import torch
+        from . import _lib as L
+        from . import device as D
+        g = self.g
+        data = self.vals[node.inputs[0][0]]
+        wv = g.nodes[node.inputs[1][0]].attrs["value"]
+        epi = dict(node.attrs.get("epilogue") or {})
+        extra = 1 if epi.get("residual") else 0
+        res = self.vals[node.inputs[-1][0]] if extra else None
+        bias = epi.get("bias")
+        if len(node.inputs) - extra >= 3:   # executor.py:63-66: explicit bias input
+            b = g.nodes[node.inputs[2][0]].attrs["value"]
+            bias = b if bias is None else bias + b
+        sh, sw = hw_pair(node.attrs["stride"])
+        ph, pw = hw_pair(node.attrs["pad"])
+        dspec = self.specs[node.inputs[0][0]]
+        n, c, h, w = dspec.logical_nchw
+        if wv.ndim == 6:
+            kcrs = host_unpack_kcrs(wv)
+        else:
+            kcrs = np.asarray(wv, np.float32)
+        k, wc, r, s = kcrs.shape
+        if data.layout.tag == "NCHWc":
+            ic_bn = data.px
+            oc_bn = out.layout.x
+        else:   # NCHW data: the naive path, NCHW == NCHW[1]c
+            ic_bn, oc_bn = 1, 1
+        c = min(c, wc)              # channel-padded input: only wc real channels
+        pad_c = c % ic_bn != 0
+        use_tc = data.layout.tag == "NCHWc" and tc_legal_block(ic_bn, self.mode)
+        scale, shift = epi.get("scale"), epi.get("shift")
+        if scale is None and shift is not None:
+            scale = np.ones(k, np.float32)
+        if scale is not None and shift is None:
+            shift = np.zeros(k, np.float32)
+        vec = lambda v: None if v is None else self._upload(np.asarray(v, np.float32))
+        t_scale, t_shift, t_bias = vec(scale), vec(shift), vec(bias)
+        sched = node.attrs.get("schedule") or {}
+        tile = {f: sched.get(f, 0) for f in ("tile_w", "tile_h", "tile_img", "tile_n",
+                                             "slices_per_stage", "stages")}
+        if use_tc:
+            mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
+            wk = self._upload(kcrs)
+            wd = D.pack_weights_umma(wk, ic_bn, mode, pad_channels=pad_c)
+            self.weights.append(wd)
+            x_t, o_t = data.tensor, out.tensor
+            r_t = None
+            if res is not None:
+                r_t = res.tensor if res.tensor.dtype == o_t.dtype else self._as_f32(res)
+            flags = self.round_flag | (L.FLAG_PAD_CHANNELS if pad_c else 0)
+            p = D.conv_params(mode, x_t, wd, o_t, n, c, h, w, k, r, s, (sh, sw), (ph, pw),
+                              ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t,
+                              bool(epi.get("relu")), flags=flags,
+                              tile=tile if any(tile.values()) else None)
+            self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream))
+            return
+        # SIMT fp32 path (fp32 mode, NCHW data, or tensor-core-illegal blocks)
+        if ic_bn > 1 or oc_bn > 1:
+            wpk = wv if wv.ndim == 6 else None
+            if wpk is None or wpk.shape[4] != ic_bn or wpk.shape[5] != oc_bn:
+                from .layout import host_pack_kcrs
+                wpk = host_pack_kcrs(kcrs, ic_bn, oc_bn)
+        else:
+            wpk = kcrs
+        wdev = self._upload(wpk)
+        x_t = self._as_f32(data)
+        r_t = self._as_f32(res) if res is not None else None
+        o_t = out.tensor if out.tensor.dtype == torch.float32 else torch.empty(
+            out.shape, dtype=torch.float32, device=self.device)
+        if o_t is not out.tensor:
+            self.weights.append(o_t)
+        p = D.conv_params(L.MODE_FP32, x_t, wdev, o_t, n, c, h, w, k, r, s, (sh, sw), (ph, pw),
+                          ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t, bool(epi.get("relu")),
+                          flags=self.round_flag)
+        self._emit(f"conv{node.id}_simt", lambda p=p: D.conv2d(p, self.stream))
+        if o_t is not out.tensor:
+            self._emit_convert(o_t, out.tensor)
+
+    def _as_f32(self, v: _Val):
+        import torch
+        if v.tensor.dtype == torch.float32:
+            return v.tensor
+        t = torch.empty(v.shape, dtype=torch.float32, device=self.device)
+        self.weights.append(t)
+        self._emit_convert(v.tensor, t)
+        return t
+
+    def _emit_convert(self, src, dst):
+        from . import _lib as L
+        from . import device as D
+        numel = src.numel()
+        self._emit("convert", lambda: L.call(
+            "neo_layout_transform", D.dtype_code(src), D.dtype_code(dst), src.data_ptr(),
+            dst.data_ptr(), 1, numel, 1, 1, L.NCHW_TAG, 1, L.NCHW_TAG, 1, 0,
+            D.stream_handle(self.stream)))
+
+    # other operators ---------------------------------------------------------
+    def _bind_transform(self, node, src: _Val, out: _Val):
+        from . import _lib as L
+        from . import device as D
+        n, c, h, w = self.specs[node.inputs[0][0]].logical_nchw
+        src_layout = src.layout
+        dst_layout = Layout.parse(node.attrs["dst_layout"])
+        s_tag = src_layout if src_layout.tag != "NCHWc" else Layout("NCHWc", x=src.px)
+        d_tag = dst_layout if dst_layout.tag != "NCHWc" else Layout("NCHWc", x=out.px)
+        flags = 0
+        if node.attrs.get("pad_channels") or out.nid in self.phys_x:
+            flags |= L.FLAG_PAD_CHANNELS
+        if out.tensor.dtype.is_floating_point and out.layout.tag == "NCHWc":
+            flags |= self.round_flag
+        s_t, d_t = src.tensor, out.tensor
+        self._emit(f"transform{node.id}", lambda: D.layout_transform(
+            s_t, d_t, n, c, h, w, s_tag, d_tag, flags, self.stream))
+
+    def _geom(self, v: _Val):
+        """(n, channel blocks, h, w, lanes) of a feature-map value."""
+        if v.layout.tag == "NCHWc":
+            n, cb, h, w, x = v.shape
+            return n, cb, h, w, x
+        if len(v.shape) == 4:
+            n, c, h, w = v.shape
+            return n, c, h, w, 1
+        # matrices / vectors: channel-free elementwise over all elements
+        return 1, 1, 1, int(np.prod(v.shape)), 1
+
+    def _bind_pool(self, node, src: _Val, out: _Val):
+        from . import device as D
+        n, cb, h, w, x = self._geom(src)
+        mode = "max" if node.kind == OpKind.MaxPool else "avg"
+        win, st, pad = node.attrs["window"], node.attrs["stride"], node.attrs.get("pad", 0)
+        flags = self.round_flag if src.layout.tag == "NCHWc" else 0
+        s_t, d_t = src.tensor, out.tensor
+        self._emit(f"{mode}pool{node.id}", lambda: D.pool2d(
+            s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream))
+
+    def _bind_eltwise(self, op, a: _Val, b: _Val | None, out: _Val):
+        from . import device as D
+        n, cb, h, w, x = self._geom(a)
+        flags = self.round_flag if a.layout.tag == "NCHWc" else 0
+        a_t, b_t, o_t = a.tensor, (b.tensor if b is not None else None), out.tensor
+        self._emit(f"eltwise{out.nid}", lambda: D.eltwise(
+            op, a_t, b_t, o_t, n, cb, h * w, x, None, None, flags, self.stream))
+
+    def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
+        from . import device as D
+        from . import _lib as L
+        if len(node.inputs) == 5:   # unfolded BN (executor.py:174-178, f32 arithmetic)
+            gamma, beta, mean, var = (np.asarray(self.g.nodes[s].attrs["value"], np.float32)
+                                      for s, _ in node.inputs[1:])
+            scale = gamma / np.sqrt(var + np.float32(node.attrs.get("eps", 1e-5)))
+            shift = beta - mean * scale
+        else:
+            scale, shift = node.attrs["scale"], node.attrs["shift"]
+        t_scale, t_shift = self._upload(scale), self._upload(shift)
+        n, cb, h, w, x = self._geom(src)
+        op = L.ELT_SCALE_SHIFT_RELU if relu else L.ELT_SCALE_SHIFT
+        flags = self.round_flag if src.layout.tag == "NCHWc" else 0
+        a_t, o_t = src.tensor, out.tensor
+        self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise(
+            op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream))
+
+    def _bind_concat(self, node, ins, out: _Val):
+        from . import device as D
+        axis = node.attrs.get("axis", 1)
+        outer = int(np.prod(out.shape[:axis]))
+        row = int(np.prod(out.shape[axis:]))
+        off = 0
+        for v in ins:
+            if v.tensor.dtype != out.tensor.dtype:
+                raise InputMismatch(f"concat {node.id}: mixed storage types")
+            chunk = int(np.prod(v.shape[axis:]))
+            s_t, d_t = v.tensor, out.tensor
+            self._emit(f"concat{node.id}", lambda s_t=s_t, d_t=d_t, chunk=chunk, off=off:
+                       D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream))
+            off += chunk
+
+    def _bind_dense(self, node, src: _Val, out: _Val):
+        from . import device as D
+        w = np.asarray(self.g.nodes[node.inputs[1][0]].attrs["value"], np.float32)
+        units, width = w.shape
+        a_t = src.tensor
+        w_t = self._upload(w, a_t.dtype)
+        b_t = None
+        if len(node.inputs) == 3:
+            b_t = self._upload(self.g.nodes[node.inputs[2][0]].attrs["value"])
+        n = src.shape[0]
+        o_t = out.tensor
+        self._emit(f"dense{node.id}", lambda: D.dense(a_t, w_t, b_t, o_t, n, width, units,
+                                                      self.stream))
+
+    def _bind_softmax(self, src: _Val, out: _Val):
+        from . import device as D
+        cols = src.shape[-1]
+        rows = int(np.prod(src.shape[:-1]))
+        a_t = self._as_f32(src)
+        o_t = out.tensor
+        self._emit(f"softmax{out.nid}", lambda: D.softmax(a_t, o_t, rows, cols, self.stream))
+
+    # -- running -----------------------------------------------------------------
+    def input_names(self) -> list[str]:
+        return [self.g.nodes[nid].attrs.get("name", f"input{nid}") for nid in self.plan.input_ids]
+
+    def input_tensor(self, name: str):
+        for nid in self.plan.input_ids:
+            if self.g.nodes[nid].attrs.get("name", f"input{nid}") == name:
+                return self.vals[nid].tensor
+        raise InputMismatch(f"missing input {name!r}")
+
+    def output_tensors(self) -> list:
+        return [v.tensor for v in self.out_vals]
+
+    def _launch_all(self):
+        for fn in self.launches:
+            fn()
+
+    def launch(self):
+        """Run the forward on ``self.stream`` (inputs already in place)."""
+        import torch
+        from . import device as D
+        if self.use_graph and self.graph_exec is None:
+            with torch.cuda.device(self.device):
+                self._launch_all()                 # warm-up: sets kernel attributes
+                self.stream.synchronize()
+                with torch.cuda.stream(self.stream):
+                    self.graph_exec = D.capture(self._launch_all, self.stream)
+        if self.graph_exec is not None:
+            self.graph_exec.launch(self.stream)
+        else:
+            with torch.cuda.device(self.device):
+                self._launch_all()
+
+    @property
+    def kernel_launches(self) -> int:
+        return len(self.launches)
+
+    def set_inputs(self, inputs: dict):
+        import torch
+        for nid in self.plan.input_ids:
+            node = self.g.nodes[nid]
+            name = node.attrs.get("name", f"input{nid}")
+            if name not in inputs:
+                raise InputMismatch(f"missing input {name!r}")
+            a = inputs[name]
+            declared = tuple(node.attrs["shape"])
+            if tuple(a.shape) != declared:
+                raise InputMismatch(f"input {name!r}: shape {tuple(a.shape)} vs {declared}")
+            dst = self.vals[nid].tensor
+            if node.attrs.get("layout", "NCHW") == "NHWC":
+                self._ingest_nhwc(a, dst)
+                continue
+            src = a if isinstance(a, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(a, dtype=np.float32))
+            with torch.cuda.stream(self.stream):
+                dst.copy_(src, non_blocking=True)
+
+    def _ingest_nhwc(self, a, dst):
+        import torch
+        from . import device as D
+        src = a if isinstance(a, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(a, dtype=np.float32))
+        staging = torch.empty(tuple(src.shape), dtype=torch.float32, device=self.device)
+        with torch.cuda.stream(self.stream):
+            staging.copy_(src, non_blocking=True)
+        n, h, w, c = src.shape
+        D.layout_transform(staging, dst, n, c, h, w, "NHWC", "NCHW", 0, self.stream)
+        self.weights.append(staging)
+
+    def run(self, inputs: dict) -> list[np.ndarray]:
+        """Host in, host out: inputs -> device, forward, outputs -> host f32."""
+        self.set_inputs(inputs)
+        self.launch()
+        self.stream.synchronize()
+        return [t.float().cpu().numpy() for t in self.output_tensors()]
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible entry points
+
+D_ELT_RELU, D_ELT_ADD = 0, 1
+
+
+def _program(plan: ExecutablePlan, device: int, mode: str, keep=()) -> DeviceProgram:
+    key = (device, mode, tuple(keep))
+    prog = plan.programs.get(key)
+    if prog is None:
+        prog = DeviceProgram(plan, device, mode, keep)
+        plan.programs[key] = prog
+    return prog
+
+
+def with_batch(g: Graph, batch: int) -> Graph:
+    """Copy of ``g`` whose Input nodes have leading dimension ``batch``."""
+    h = g.copy()
+    for node in h.nodes.values():
+        if node.kind == OpKind.Input:
+            shape = list(node.attrs["shape"])
+            shape[0] = batch
+            node.attrs["shape"] = tuple(shape)
+    return h
+
+
+def execute(plan, inputs: dict, pool=None, keep=()) -> list[np.ndarray]:
+    """Run the graph; outputs in ``graph.outputs`` order (then ``keep``), in
+    the default layout as host f32 arrays (executor.py:131-218).
+
+    ``pool``: a DevicePool (devices + mode), a mode string or None.  With
+    several devices the batch is split contiguously across them and each
+    shard runs the same compiled graph independently (no collective)."""
+    if isinstance(plan, Graph):
+        plan = ExecutablePlan.compile(plan)
+    dp = resolve_pool(pool)
+    if dp.size == 1:
+        return _program(plan, dp.device, dp.mode, keep).run(inputs)
+    batch = plan.graph.nodes[plan.input_ids[0]].attrs["shape"][0]
+    shards = dp.shards(batch)
+    progs = []
+    for dev, (lo, hi) in shards:
+        sub = plan.programs.get(("shard", dev, lo, hi, dp.mode, tuple(keep)))
+        if sub is None:
+            sub = DeviceProgram(ExecutablePlan.compile(with_batch(plan.graph, hi - lo)), dev,
+                                dp.mode, keep)
+            plan.programs[("shard", dev, lo, hi, dp.mode, tuple(keep))] = sub
+        sub.set_inputs({k: v[lo:hi] for k, v in inputs.items()})
+        sub.launch()
+        progs.append(sub)
+    parts = []
+    for sub in progs:
+        sub.stream.synchronize()
+        parts.append([t.float().cpu().numpy() for t in sub.output_tensors()])
+    return [np.concatenate([p[i] for p in parts], axis=0) for i in range(len(parts[0]))]
+
+
+def benchmark(plan, pool, inputs: dict, samples: int = 1000,
+              warmups: int = 3) -> tuple[float, float]:
+    """(mean_ns, stderr_ns) of end-to-end forwards (executor.py:221-236):
+    each sample = inputs to device + forward + outputs to host, timed with
+    CUDA events on the program's stream."""
+    import torch
+    if isinstance(plan, Graph):
+        plan = ExecutablePlan.compile(plan)
+    dp = resolve_pool(pool)
+    prog = _program(plan, dp.device, dp.mode)
+    for _ in range(max(1, warmups)):
+        prog.run(inputs)
+    times = np.empty(samples, dtype=np.float64)
+    for i in range(samples):
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(prog.stream)
+        prog.set_inputs(inputs)
+        prog.launch()
+        outs = [t.float().cpu() for t in prog.output_tensors()]
+        end.record(prog.stream)
+        end.synchronize()
+        times[i] = start.elapsed_time(end) * 1e6
+        del outs
+    mean = float(times.mean())
+    stderr = float(times.std(ddof=1) / math.sqrt(samples)) if samples > 1 else 0.0
+    return mean, stderr
+
+
+def scalability_report(g: Graph, inputs: dict, samples: int, device_counts,
+                       mode: str = "bf16") -> list[str]:
+    """CSV lines ``gpus,samples,mean_ns,stderr_ns`` (executor.py:239-247 with
+    device counts in place of thread counts); the batch is sharded."""
+    import torch
+    lines = []
+    plan = ExecutablePlan.compile(g)
+    for count in device_counts:
+        count = min(count, max(1, torch.cuda.device_count()))
+        pool = DevicePool(list(range(count)), mode)
+        execute(plan, inputs, pool)
+        times = []
+        for _ in range(samples):
+            t0 = time.perf_counter_ns()
+            execute(plan, inputs, pool)
+            times.append(time.perf_counter_ns() - t0)
+        arr = np.asarray(times, np.float64)
+        se = float(arr.std(ddof=1) / math.sqrt(len(arr))) if len(arr) > 1 else 0.0
+        lines.append(f"{count},{samples},{arr.mean():.0f},{se:.0f}")
+    return lines
