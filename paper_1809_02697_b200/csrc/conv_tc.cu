@@ -32,13 +32,16 @@
 namespace {
 
 constexpr int kMaxStages = 8;
-constexpr int kThreads = 192;
+constexpr int kThreads = 576;   // warp 0 TMA, warp 1 MMA, warps 2-17 epilogue (2 groups of 8)
+constexpr int kEpiGroupThreads = 256;
 constexpr int kTileM = 128;
 constexpr int kSmemBudget = 227 * 1024;
 
 struct ConvTCParams {
   CUtensorMap tmA;  // 5-D: (x, W, H, Cb, N)
   CUtensorMap tmB;  // 3-D: (x, K, slices)
+  CUtensorMap tmO;  // 5-D output store map: (y, OW, OH, Kb_total, N)   (tma_epi)
+  CUtensorMap tmR;  // 5-D residual load map, same geometry              (tma_epi)
   int N, OH, OW, K;
   int BW, BH, BNI, BN;
   int tiles_w, tiles_h, tiles_k;
@@ -56,6 +59,11 @@ struct ConvTCParams {
   void* out;
   int y, out_cb_off, out_cb_total, res_cb_off, res_cb_total;
   int relu, out_f32, round_tf32;
+  int tma_epi;        // stage output blocks in smem and store them with TMA
+  int rowb_out;       // y * sizeof(out elem) for the TMA epilogue
+  uint32_t stage_out; // bytes of one staging buffer (128 rows * rowb_out)
+  uint32_t out_box_bytes;
+  int nslot;          // staging slots per epilogue group (tma_epi)
 };
 
 __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n0, int& oh0,
@@ -168,6 +176,97 @@ __device__ __forceinline__ void epi_chunk(const ConvTCParams& p, const uint32_t 
   }
 }
 
+// Epilogue of one output channel block (y columns) staged through shared
+// memory: TMEM -> registers -> (+ residual from the smem tile the TMA load
+// brought in) -> swizzled smem row -> TMA store of the whole block.
+// Per-column epilogue vectors of a 16-column chunk, loaded as broadcast
+// float4s (every thread of the warp reads the same addresses); absent vectors
+// become the identity so the per-element math is branch-free:
+//   v = fma(v, scale, shift) ; v += bias ; v += residual ; v = max(v, floor)
+// (floor = 0 for relu, -inf otherwise) -- the reference order of
+// kernels.py:185-197 with one rounding per reference operation.
+struct EpiVecs {
+  float sc[16], sh[16], bi[16];
+};
+
+__device__ __forceinline__ void load_vec16(const float* base, int k, float fill, float (&dst)[16]) {
+  if (base) {
+    const float4* v4 = reinterpret_cast<const float4*>(base + k);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 t = __ldg(v4 + q);
+      dst[4 * q] = t.x;
+      dst[4 * q + 1] = t.y;
+      dst[4 * q + 2] = t.z;
+      dst[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dst[j] = fill;
+  }
+}
+
+// One output channel block (y columns) of one pixel row: TMEM -> registers ->
+// epilogue -> swizzled smem row (which already holds the residual block when
+// HAS_RES).  OUT_F32 selects f32 vs bf16 storage.
+template <bool OUT_F32, bool HAS_RES>
+__device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int kbase,
+                                              int m, uint8_t* sbuf_gen, float relu_floor,
+                                              bool round) {
+  const int nchunk = p.y / 16;  // 16-column TMEM loads
+  constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
+#pragma unroll 1
+  for (int c = 0; c < nchunk; ++c) {
+    uint32_t v[16];
+    tmem_ld16(tcol + c * 16, v);
+    EpiVecs e;
+    const int k = kbase + c * 16;
+    load_vec16(p.scale, k, 1.f, e.sc);
+    load_vec16(p.shift, k, 0.f, e.sh);
+    load_vec16(p.bias, k, 0.f, e.bi);
+    tmem_ld_wait();
+    float f[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      f[j] = fmaf(__uint_as_float(v[j]), e.sc[j], e.sh[j]) + e.bi[j];
+#pragma unroll
+    for (int q = 0; q < kChunks16; ++q) {
+      const uint32_t off = swz_offset(m, c * kChunks16 + q, p.rowb_out);
+      uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
+      if constexpr (OUT_F32) {
+        float o[4];
+        float4 rv = HAS_RES ? *reinterpret_cast<float4*>(slot) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float r4[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float t = f[4 * q + j];
+          if constexpr (HAS_RES) t += r4[j];
+          t = fmaxf(t, relu_floor);
+          o[j] = round ? neo_round_tf32(t) : t;
+        }
+        *reinterpret_cast<float4*>(slot) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+        uint4 packed;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&packed);
+        uint4 rv;
+        if constexpr (HAS_RES) rv = *slot;
+        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float a = f[8 * q + 2 * j], b = f[8 * q + 2 * j + 1];
+          if constexpr (HAS_RES) {
+            const float2 t = __bfloat1622float2(r2[j]);
+            a += t.x;
+            b += t.y;
+          }
+          h2[j] = __floats2bfloat162_rn(fmaxf(a, relu_floor), fmaxf(b, relu_floor));
+        }
+        *slot = packed;
+      }
+    }
+  }
+}
+
 template <bool TF32>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -175,14 +274,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   const uint32_t sA = sraw + pad;
   const uint32_t sB = sA + p.stages * p.a_stage;
-  const uint32_t sBar = sB + p.stages * p.b_stage;
-  uint8_t* bar_gen = smem_raw + pad + p.stages * (p.a_stage + p.b_stage);
+  const uint32_t sO = sB + p.stages * p.b_stage;                // 2 groups x nslot staging slots
+  const uint32_t sBar = sO + 2 * p.nslot * p.stage_out;
+  uint8_t* gen_base = smem_raw + pad;
+  uint8_t* bar_gen = gen_base + (sBar - sA);
   auto full_bar = [&](int i) { return sBar + 8u * i; };
   auto empty_bar = [&](int i) { return sBar + 64u + 8u * i; };
   auto tfull_bar = [&](int a) { return sBar + 128u + 8u * a; };
   auto tempty_bar = [&](int a) { return sBar + 144u + 8u * a; };
-  const uint32_t tslot = sBar + 160u;
-  volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 160);
+  auto res_bar = [&](int g, int b) { return sBar + 160u + 16u * g + 8u * b; };
+  const uint32_t tslot = sBar + 192u;
+  volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 192);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,13 +292,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmA);
     tma_prefetch_desc(&p.tmB);
+    if (p.tma_epi) {
+      tma_prefetch_desc(&p.tmO);
+      if (p.res) tma_prefetch_desc(&p.tmR);
+    }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(full_bar(i), 1);
       mbar_init(empty_bar(i), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4);
+      mbar_init(tempty_bar(a), 8);
+      mbar_init(res_bar(a, 0), 1);
+      mbar_init(res_bar(a, 1), 1);
     }
     fence_mbar_init();
   }
@@ -285,39 +393,110 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
     }
   } else {
-    // ---------------- epilogue warps ----------------
-    const int q = warp & 3;
-    const int m = q * 32 + lane;
+    // ---------------- epilogue: two groups of 4 warps, group g takes the
+    // tiles whose accumulator lives in TMEM stage g (alternate tiles), so
+    // both groups drain in parallel with the MMA of the next tile.
+    const int grp = (warp - 2) >> 3;
+    const int half = ((warp - 2) >> 2) & 1;  // which channel blocks of a tile
+    const int q = warp & 3;                 // TMEM lane quarter of this warp
+    const int m = q * 32 + lane;            // accumulator row = tile pixel
+    const bool leader = (warp == 2 + 8 * grp) && lane == 0;
+    const uint32_t bar_id = 1 + grp;
     const size_t plane = (size_t)p.OH * p.OW * p.y;
-    int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    uint32_t res_phase = 0u;                // phase of this group's residual barrier
+    int it = grp;
+    for (int t = blockIdx.x + grp * gridDim.x; t < p.num_tiles; t += 2 * gridDim.x, it += 2) {
       int n0, oh0, ow0, k0;
       decode_tile(p, t, n0, oh0, ow0, k0);
-      const int acc = it & 1;
+      const int acc = grp;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int wl = m % p.BW, hl = (m / p.BW) % p.BH, nl = m / (p.BW * p.BH);
-      const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
-      const bool valid = (m < p.BW * p.BH * p.BNI) && ow < p.OW && oh < p.OH && n < p.N;
-      EpiAccess ea;
-      ea.plane = plane;
-      const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
-      ea.out_base = (size_t)n * p.out_cb_total * plane + (size_t)p.out_cb_off * plane + pix;
-      ea.res_base = (size_t)n * p.res_cb_total * plane + (size_t)p.res_cb_off * plane + pix;
-
-      mbar_wait(tfull_bar(acc), acc_phase);
-      tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.BN;
       const int ncols = min(p.BN, p.K - k0);
-      for (int c0 = 0; c0 < ncols; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(trow + c0, v);
-        tmem_ld_wait();
-        if (valid) epi_chunk(p, v, k0 + c0, ea);
+      if (p.tma_epi) {
+        // staged epilogue: the tile's output channel blocks go through up to
+        // p.nslot swizzled smem slots; residual blocks are fetched by TMA
+        // into the same slots before the accumulator is waited for, then
+        // results overwrite them and leave with TMA bulk stores.
+        const bool has_res = p.res != nullptr;
+        const int nblk = ncols / p.y;
+        const uint32_t sgrp = sO + grp * p.nslot * p.stage_out;
+        uint8_t* sgrp_gen = gen_base + (sgrp - sA);
+        auto issue_res = [&](int b0, int cnt) {
+          if (!leader) return;
+          bulk_wait_read<0>();              // previous stores left the slots
+          if (has_res) {
+            mbar_arrive_expect_tx(res_bar(grp, 0), cnt * p.out_box_bytes);
+            for (int i = 0; i < cnt; ++i)
+              tma_load_5d(sgrp + i * p.stage_out, &p.tmR, res_bar(grp, 0), 0, ow0, oh0,
+                          p.res_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
+          }
+        };
+        issue_res(0, min(nblk, p.nslot));
+        named_bar_sync(bar_id, kEpiGroupThreads);
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+        for (int b0 = 0; b0 < nblk; b0 += p.nslot) {
+          const int cnt = min(p.nslot, nblk - b0);
+          if (b0 > 0) {
+            issue_res(b0, cnt);
+            named_bar_sync(bar_id, kEpiGroupThreads);
+          }
+          if (has_res) {
+            mbar_wait(res_bar(grp, 0), res_phase & 1u);
+            res_phase ^= 1u;
+          }
+          const float floor_v = p.relu ? 0.f : -INFINITY;
+          const bool rnd = p.round_tf32 != 0;
+          for (int i = half; i < cnt; i += 2) {
+            const uint32_t tcol = trow + (b0 + i) * p.y;
+            const int kb0 = k0 + (b0 + i) * p.y;
+            uint8_t* sg = sgrp_gen + i * p.stage_out;
+            if (p.out_f32) {
+              if (has_res) epi_block_tma<true, true>(p, tcol, kb0, m, sg, floor_v, rnd);
+              else epi_block_tma<true, false>(p, tcol, kb0, m, sg, floor_v, rnd);
+            } else {
+              if (has_res) epi_block_tma<false, true>(p, tcol, kb0, m, sg, floor_v, rnd);
+              else epi_block_tma<false, false>(p, tcol, kb0, m, sg, floor_v, rnd);
+            }
+          }
+          if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(acc));
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(bar_id, kEpiGroupThreads);
+          if (leader) {
+            for (int i = 0; i < cnt; ++i)
+              tma_store_5d(&p.tmO, sgrp + i * p.stage_out, 0, ow0, oh0,
+                           p.out_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
+            bulk_commit();
+          }
+        }
+        continue;
+      } else {
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+        const int wl = m % p.BW, hl = (m / p.BW) % p.BH, nl = m / (p.BW * p.BH);
+        const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
+        const bool valid = (m < p.BW * p.BH * p.BNI) && ow < p.OW && oh < p.OH && n < p.N;
+        EpiAccess ea;
+        ea.plane = plane;
+        const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
+        ea.out_base = (size_t)n * p.out_cb_total * plane + (size_t)p.out_cb_off * plane + pix;
+        ea.res_base = (size_t)n * p.res_cb_total * plane + (size_t)p.res_cb_off * plane + pix;
+        for (int c0 = 16 * half; c0 < ncols; c0 += 32) {
+          uint32_t v[16];
+          tmem_ld16(trow + c0, v);
+          tmem_ld_wait();
+          if (valid) epi_chunk(p, v, k0 + c0, ea);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty_bar(acc));
     }
+    if (leader) bulk_wait_all();
   }
 
   __syncthreads();
@@ -451,6 +630,18 @@ int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
   return r * s * neo_ceil_div(c, x);
 }
 
+// Row bytes of one output channel block for the TMA-store epilogue, or 0 when
+// the direct-store path must run: the block must be a 32/64/128-byte row of
+// whole 16-column chunks and every N tile must hold whole channel blocks.
+static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
+  const int out_es = p->out_dtype == NEO_F32 ? 4 : 2;
+  const int y = p->oc_bn;
+  const int rowb_out = y * out_es;
+  const bool ok = y % 16 == 0 && (rowb_out == 32 || rowb_out == 64 || rowb_out == 128) &&
+                  tile_n % y == 0 && !getenv("NEOB200_DIRECT_EPILOGUE");
+  return ok ? rowb_out : 0;
+}
+
 int neo_conv_default_tiles(neo_conv_params* p) {
   NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
   if (p->mode == NEO_MODE_FP32) return NEO_OK;
@@ -469,8 +660,14 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   const int64_t nslices = p->r * p->s * neo_ceil_div(p->c, p->ic_bn);
   if (p->slices_per_stage <= 0) p->slices_per_stage = pick_slices_per_stage(nslices, rowb, p->tile_n);
   if (p->stages <= 0) {
+    // deep enough to hide load latency, leaving at least one staging slot per
+    // epilogue group; single-stage reductions (1x1, C <= x) only need 2
     const int64_t stage = (int64_t)p->slices_per_stage * (kTileM + p->tile_n) * rowb;
-    p->stages = (int)std::min<int64_t>(kMaxStages, (kSmemBudget - 2048) / stage);
+    const int64_t kst = neo_ceil_div(nslices, p->slices_per_stage);
+    const int rb = epi_rowb_out(p, p->tile_n);
+    const int64_t want = kst <= 1 ? 2 : std::min<int64_t>(6, kst + 1);
+    const int64_t room = kSmemBudget - 2048 - (rb ? 2ll * kTileM * rb : 0);
+    p->stages = (int)std::max<int64_t>(std::min<int64_t>(want, room / stage), 2);
   }
   return NEO_OK;
 }
@@ -592,7 +789,48 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.out_f32 = p->out_dtype == NEO_F32;
   kp.round_tf32 = (p->flags & NEO_FLAG_ROUND_TF32) ? 1 : 0;
 
-  const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) + 256;
+  // TMA-store epilogue: output / residual tensor maps over (y, OW, OH, Kb_total, N)
+  const int rb_out = epi_rowb_out(p, BN);
+  {
+    const int64_t left = (int64_t)kSmemBudget - 2048 - (int64_t)p->stages * (kp.a_stage + kp.b_stage);
+    const int64_t slots = rb_out ? left / (2ll * kTileM * rb_out) : 0;
+    kp.nslot = (int)std::min<int64_t>(slots, BN / std::max(1, p->oc_bn));
+  }
+  kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
+  if (kp.tma_epi) {
+    const int y = p->oc_bn;
+    kp.rowb_out = rb_out;
+    kp.stage_out = (uint32_t)(kTileM * kp.rowb_out);
+    kp.out_box_bytes = (uint32_t)(BW * BH * BNI * kp.rowb_out);
+    const CUtensorMapDataType odt =
+        kp.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    cuuint32_t box[5] = {(cuuint32_t)y, (cuuint32_t)BW, (cuuint32_t)BH, 1u, (cuuint32_t)BNI};
+    cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    auto encode_fm = [&](CUtensorMap* map, const void* base, int64_t cb_total) {
+      cuuint64_t dims[5] = {(cuuint64_t)y, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)cb_total,
+                            (cuuint64_t)p->n};
+      cuuint64_t strides[4] = {(cuuint64_t)kp.rowb_out, (cuuint64_t)OW * kp.rowb_out,
+                               (cuuint64_t)OH * OW * kp.rowb_out,
+                               (cuuint64_t)cb_total * OH * OW * kp.rowb_out};
+      return encode(map, odt, 5, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(kp.rowb_out),
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode_fm(&kp.tmO, p->out, kp.out_cb_total);
+    NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map O encode failed (%d)", (int)r);
+    if (p->residual) {
+      r = encode_fm(&kp.tmR, p->residual, kp.res_cb_total);
+      NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map R encode failed (%d)", (int)r);
+    }
+  } else {
+    kp.nslot = 0;
+    kp.rowb_out = 0;
+    kp.stage_out = 0;
+    kp.out_box_bytes = 0;
+  }
+
+  const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) +
+                     2 * (size_t)kp.nslot * kp.stage_out + 256;
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
   const int grid = (int)std::min<int64_t>(num_tiles, sm_count_of_current_device());

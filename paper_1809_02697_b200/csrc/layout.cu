@@ -135,11 +135,62 @@ __global__ void retile_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, 
   }
 }
 
+// NCHW -> NCHW[x]c for small x (x*sizeof(dst) <= 64 B, e.g. the 3-channel
+// image into 8 padded bf16 lanes): one thread per (n, cb, pixel) gathers its
+// x channels (coalesced across threads) and writes them as one contiguous row.
+template <typename Ts, typename Td, int X>
+__global__ void pack_small_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, int64_t N,
+                                  int64_t Call, int64_t HW, bool round) {
+  const int64_t Cb = (Call + X - 1) / X;
+  const int64_t total = N * Cb * HW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % HW;
+    const int64_t b = i / HW;
+    const int64_t n = b / Cb, cb = b % Cb;
+    Td row[X];
+#pragma unroll
+    for (int j = 0; j < X; ++j) {
+      const int64_t ch = cb * X + j;
+      row[j] = ch < Call ? Conv<Ts, Td>::cvt(src[(n * Call + ch) * HW + p], round)
+                         : Elem<Td>::from_f(0.f);
+    }
+    constexpr int kVec = (int)(X * sizeof(Td) / 16);
+    if constexpr (kVec >= 1) {
+      const uint4* r4 = reinterpret_cast<const uint4*>(row);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + i * X);
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) d4[v] = r4[v];
+    } else {
+#pragma unroll
+      for (int j = 0; j < X; ++j) dst[i * X + j] = row[j];
+    }
+  }
+}
+
+template <typename Ts, typename Td>
+bool try_pack_small(const void* src, void* dst, int64_t n, int64_t c, int64_t hw, int x,
+                    bool round, cudaStream_t st) {
+  const int64_t total = n * ((c + x - 1) / x) * hw;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32));
+  auto s = static_cast<const Ts*>(src);
+  auto d = static_cast<Td*>(dst);
+  switch (x) {
+    case 4: pack_small_kernel<Ts, Td, 4><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
+    case 8: pack_small_kernel<Ts, Td, 8><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
+    case 16: pack_small_kernel<Ts, Td, 16><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
+    default: return false;
+  }
+}
+
 template <typename Ts, typename Td>
 int dispatch_layout(const void* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
                     int src_tag, int src_x, int dst_tag, int dst_x, bool round, cudaStream_t st) {
   const int64_t HW = h * w;
-  if (src_tag == NEO_NCHW && dst_tag == NEO_NCHWC) {
+  if (src_tag == NEO_NCHW && dst_tag == NEO_NCHWC && dst_x <= 16 &&
+      try_pack_small<Ts, Td>(src, dst, n, c, HW, dst_x, round, st)) {
+    // small block: per-pixel gather kernel
+  } else if (src_tag == NEO_NCHW && dst_tag == NEO_NCHWC) {
     const int64_t cb = neo_ceil_div(c, dst_x);
     launch_transpose<Ts, Td>(src, dst, PackMap{c, HW, cb, dst_x}, n * cb, dst_x, HW, round, st);
   } else if (src_tag == NEO_NCHWC && dst_tag == NEO_NCHW) {

@@ -55,6 +55,59 @@ __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64
   }
 }
 
+// vector variant: V consecutive lanes of x per thread (16-byte loads/stores)
+template <typename T, int V>
+__global__ void pool_kernel_vec(const T* __restrict__ in, T* __restrict__ out, int64_t N,
+                                int64_t Cb, int H, int W, int OH, int OW, int x, int win,
+                                int stride, int pad, bool is_max, bool round) {
+  const int groups = x / V;
+  const int64_t total = N * Cb * OH * OW * groups;
+  const float inv = (float)(win * win);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int gq = (int)(t % groups);
+    t /= groups;
+    const int ow = (int)(t % OW);
+    t /= OW;
+    const int oh = (int)(t % OH);
+    const int64_t plane = t / OH;
+    const T* src = in + plane * H * W * x + gq * V;
+    float acc[V];
+    bool first = true;
+    for (int r = 0; r < win; ++r) {
+      const int ih = oh * stride + r - pad;
+      for (int s = 0; s < win; ++s) {
+        const int iw = ow * stride + s - pad;
+        const bool inb = ih >= 0 && ih < H && iw >= 0 && iw < W;
+        float v[V];
+        if (inb) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(src + ((int64_t)ih * W + iw) * x);
+          const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int j = 0; j < V; ++j) v[j] = Elem<T>::to_f(e[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; ++j) v[j] = is_max ? -INFINITY : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[j] = first ? v[j] : (is_max ? fmaxf(acc[j], v[j]) : __fadd_rn(acc[j], v[j]));
+        first = false;
+      }
+    }
+    uint4 packed;
+    T* o = reinterpret_cast<T*>(&packed);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float a = is_max ? acc[j] : __fdiv_rn(acc[j], inv);
+      if (round) a = neo_round_tf32(a);
+      o[j] = Elem<T>::from_f(a);
+    }
+    *reinterpret_cast<uint4*>(out + (((plane * OH + oh) * OW + ow) * x) + gq * V) = packed;
+  }
+}
+
 template <typename T>
 __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
                                const float* __restrict__ scale, const float* __restrict__ shift,
@@ -186,7 +239,17 @@ extern "C" int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_
   const int64_t total = n * cb * OH * OW * x;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
-  if (dtype == NEO_BF16)
+  if (dtype == NEO_BF16 && x % 8 == 0) {
+    const int64_t tv = total / 8;
+    pool_kernel_vec<__nv_bfloat16, 8><<<(unsigned)grid_for(tv), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
+        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+  } else if (dtype == NEO_F32 && x % 4 == 0) {
+    const int64_t tv = total / 4;
+    pool_kernel_vec<float, 4><<<(unsigned)grid_for(tv), 256, 0, st>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
+        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+  } else if (dtype == NEO_BF16)
     pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
         (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);

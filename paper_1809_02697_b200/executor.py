@@ -154,6 +154,24 @@ class DeviceProgram:
                         and nid not in g.outputs and nid not in self.keep):
                     self.fused_bn_relu[us[0]] = nid
                     self.skip.add(nid)
+        # Dense layers run as 1x1 tensor-core convs over their row-major input
+        # ((N, F) == NCHW[x]c with H = W = 1); a Dense whose only consumer is a
+        # ReLU writes the ReLU's value with the relu fused into the epilogue.
+        self.tc_dense: set[int] = set()
+        self.fused_dense_relu: dict[int, int] = {}   # relu id -> dense id
+        if self.mode in ("bf16", "tf32"):
+            for nid in order:
+                node = g.nodes[nid]
+                if node.kind != OpKind.Dense:
+                    continue
+                width = g.nodes[node.inputs[1][0]].attrs["value"].shape[1]
+                if self._dense_block(width):
+                    self.tc_dense.add(nid)
+                us = self.users[nid]
+                if (len(us) == 1 and g.nodes[us[0]].kind == OpKind.ReLU
+                        and nid not in g.outputs and nid not in self.keep):
+                    self.fused_dense_relu[us[0]] = nid
+                    self.skip.add(nid)
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -182,6 +200,17 @@ class DeviceProgram:
             if node.kind == OpKind.Constant:
                 continue
             self.vals[nid] = self._make_val(nid)
+        # NCHW[x]c -> NCHW of an H = W = 1 map is the identity on memory: alias
+        for nid in order:
+            node = g.nodes[nid]
+            if node.kind != OpKind.LayoutTransform or nid not in self.vals:
+                continue
+            src = self.vals.get(node.inputs[0][0])
+            out = self.vals[nid]
+            if (src is not None and src.layout.tag == "NCHWc" and out.layout.tag == "NCHW"
+                    and src.shape[2] == 1 and src.shape[3] == 1 and src.dtype == out.dtype
+                    and src.px == src.layout.x and not node.attrs.get("pad_channels")):
+                out.alias = node.inputs[0][0]
         # lifetimes
         last_step = len(order)
         for nid, v in self.vals.items():
@@ -193,10 +222,12 @@ class DeviceProgram:
                 tgt = self._storage(src)
                 if tgt is not None:
                     tgt.last = max(tgt.last, self.step[nid])
-            if nid in self.fused_bn_relu.keys():
-                bn = self.fused_bn_relu[nid]
-                tgt = self._storage(self.g.nodes[bn].inputs[0][0])
-                tgt.last = max(tgt.last, self.step[nid])
+            fused_src = self.fused_bn_relu.get(nid, self.fused_dense_relu.get(nid))
+            if fused_src is not None:
+                for src, _ in self.g.nodes[fused_src].inputs:
+                    tgt = self._storage(src)
+                    if tgt is not None:
+                        tgt.last = max(tgt.last, self.step[nid])
         for o in list(self.g.outputs) + self.keep:
             tgt = self._storage(o)
             if tgt is not None:
@@ -230,7 +261,39 @@ class DeviceProgram:
             else:
                 shape = spec.shape
             return _Val(nid, tuple(shape), self.act_dtype, layout, px=px)
-        return _Val(nid, tuple(spec.shape), torch.float32, layout)
+        dtype = self.act_dtype if self._feeds_tc_dense(nid) else torch.float32
+        return _Val(nid, tuple(spec.shape), dtype, layout)
+
+    def _dense_block(self, width: int) -> int:
+        """Legal tensor-core block dividing a dense input width (0 if none)."""
+        for x in (64, 32, 16, 8, 4):
+            if width % x == 0 and tc_legal_block(x, self.mode):
+                return x
+        return 0
+
+    def _feeds_tc_dense(self, nid: int) -> bool:
+        """A non-blocked value is kept in the activation type when every use
+        is the data input of a tensor-core Dense (directly or via Flatten)."""
+        g = self.g
+        if nid in g.outputs or nid in self.keep:
+            return False
+        us = self.users[nid]
+        if not us:
+            return False
+        for u in us:
+            node = g.nodes[u]
+            if node.kind == OpKind.Dense:
+                if u not in self.tc_dense or node.inputs[0][0] != nid:
+                    return False
+            elif node.kind == OpKind.Flatten:
+                if not self._feeds_tc_dense(u):
+                    return False
+            elif node.kind == OpKind.ReLU and nid in self.fused_dense_relu.values():
+                if not self._feeds_tc_dense(u):
+                    return False
+            else:
+                return False
+        return True
 
     # -- memory ----------------------------------------------------------------
     def _allocate(self):
@@ -277,9 +340,13 @@ class DeviceProgram:
             if kind == OpKind.Conv2d:
                 self._bind_conv(node, out)
             elif kind == OpKind.LayoutTransform:
-                self._bind_transform(node, ins[0], out)
+                if out.alias is None:
+                    self._bind_transform(node, ins[0], out)
             elif kind in (OpKind.MaxPool, OpKind.AvgPool):
                 self._bind_pool(node, ins[0], out)
+            elif kind == OpKind.ReLU and nid in self.fused_dense_relu:
+                dn = g.nodes[self.fused_dense_relu[nid]]
+                self._bind_dense(dn, self.vals[dn.inputs[0][0]], out, relu=True)
             elif kind == OpKind.ReLU:
                 if nid in self.fused_bn_relu:
                     bn = g.nodes[self.fused_bn_relu[nid]]
@@ -486,19 +553,48 @@ class DeviceProgram:
                        D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream))
             off += chunk
 
-    def _bind_dense(self, node, src: _Val, out: _Val):
+    def _bind_dense(self, node, src: _Val, out: _Val, relu: bool = False):
+        import torch
+        from . import _lib as L
         from . import device as D
         w = np.asarray(self.g.nodes[node.inputs[1][0]].attrs["value"], np.float32)
         units, width = w.shape
-        a_t = src.tensor
-        w_t = self._upload(w, a_t.dtype)
         b_t = None
         if len(node.inputs) == 3:
             b_t = self._upload(self.g.nodes[node.inputs[2][0]].attrs["value"])
         n = src.shape[0]
-        o_t = out.tensor
+        if node.id in self.tc_dense and src.tensor.dtype == self.act_dtype:
+            # tensor cores: (n, width) row-major == NCHW[x]c with H = W = 1, so
+            # the dense is a 1x1 conv; the output (n, units) is NCHW[y]c with
+            # H = W = 1 for any y dividing units.
+            x = self._dense_block(width)
+            mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
+            wd = D.pack_weights_umma(self._upload(w.reshape(units, width, 1, 1)), x, mode)
+            self.weights.append(wd)
+            o_t = out.tensor
+            y = next(d for d in (32, 16, 8, 4, 2, 1) if units % d == 0)
+            tile = {"tile_w": 1, "tile_h": 1, "tile_img": min(n, 128),
+                    "tile_n": max(16, min(256, -(-units // 148 // 16) * 16))}
+            p = D.conv_params(mode, src.tensor.reshape(-1), wd, o_t.reshape(-1), n, width, 1, 1,
+                              units, 1, 1, (1, 1), (0, 0), x, y, bias=b_t, relu=relu,
+                              flags=self.round_flag if o_t.dtype == torch.float32 and
+                              self._feeds_tc_dense(out.nid) else 0, tile=tile)
+            self._emit(f"dense{node.id}_tc", lambda p=p: D.conv2d(p, self.stream))
+            return
+        a_t = self._as_f32(src) if self.mode != "bf16" or src.tensor.dtype != torch.bfloat16 \
+            else src.tensor
+        w_t = self._upload(w, a_t.dtype)
+        o_t = out.tensor if out.tensor.dtype == torch.float32 else torch.empty(
+            out.shape, dtype=torch.float32, device=self.device)
         self._emit(f"dense{node.id}", lambda: D.dense(a_t, w_t, b_t, o_t, n, width, units,
                                                       self.stream))
+        if relu:
+            from . import _lib as L2
+            self._emit(f"relu{out.nid}", lambda: D.eltwise(
+                L2.ELT_RELU, o_t, None, o_t, 1, 1, 1, o_t.numel(), 1, 0, self.stream))
+        if o_t is not out.tensor:
+            self.weights.append(o_t)
+            self._emit_convert(o_t, out.tensor)
 
     def _bind_softmax(self, src: _Val, out: _Val):
         from . import device as D

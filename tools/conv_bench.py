@@ -1,0 +1,89 @@
+#!/usr/bin/env python
+"""Time one tensor-core conv configuration (CUDA events), optionally sweeping
+tile configurations.  Used for ncu captures and tile exploration.
+
+  python tools/conv_bench.py --n 64 --c 64 --k 256 --hw 56 --r 1 [--res] [--sweep]
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--c", type=int, default=64)
+    ap.add_argument("--k", type=int, default=256)
+    ap.add_argument("--hw", type=int, default=56)
+    ap.add_argument("--r", type=int, default=1)
+    ap.add_argument("--stride", type=int, default=1)
+    ap.add_argument("--x", type=int, default=64)
+    ap.add_argument("--y", type=int, default=64)
+    ap.add_argument("--mode", default="bf16")
+    ap.add_argument("--res", action="store_true")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--tile", default="", help="json dict of tile fields")
+    args = ap.parse_args()
+
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+
+    dev = torch.device("cuda:0")
+    act = torch.bfloat16 if args.mode == "bf16" else torch.float32
+    lmode = L.MODE_BF16 if args.mode == "bf16" else L.MODE_TF32
+    n, c, k, hw, r, st = args.n, args.c, args.k, args.hw, args.r, args.stride
+    pad = r // 2
+    oh = (hw + 2 * pad - r) // st + 1
+    x = torch.randn((n, c // args.x, hw, hw, args.x), device=dev).to(act)
+    w = torch.randn((k, c, r, r), device=dev) * 0.05
+    wd = D.pack_weights_umma(w, args.x, lmode)
+    out = torch.empty((n, k // args.y, oh, oh, args.y), dtype=act, device=dev)
+    res = torch.randn_like(out) if args.res else None
+    bias = torch.randn(k, device=dev)
+    flops = 2 * n * k * c * r * r * oh * oh
+    byts = (x.numel() + out.numel() * (2 if args.res else 1)) * x.element_size()
+
+    def run(tile):
+        p = D.conv_params(lmode, x, wd, out, n, c, hw, hw, k, r, r, (st, st), (pad, pad), args.x,
+                          args.y, bias=bias, residual=res, relu=True, tile=tile)
+        cfg = D.default_tiles(p)
+        for _ in range(3):
+            D.conv2d(p)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.iters):
+            D.conv2d(p)
+        b.record()
+        b.synchronize()
+        us = a.elapsed_time(b) * 1e3 / args.iters
+        return us, cfg
+
+    tiles = [json.loads(args.tile) if args.tile else None]
+    if args.sweep:
+        tiles = [None]
+        for tn, g, stg in itertools.product((64, 128, 256), (1, 2), (2, 3, 4, 6)):
+            if tn > -(-k // 16) * 16:
+                continue
+            tiles.append({"tile_n": tn, "slices_per_stage": g, "stages": stg})
+    for tile in tiles:
+        try:
+            us, cfg = run(tile)
+        except Exception as exc:
+            print(f"{tile}: {type(exc).__name__}: {exc}")
+            continue
+        print(f"{json.dumps(cfg)} {us:8.1f} us  {flops / us / 1e6:7.1f} TF/s  "
+              f"{byts / us / 1e3:7.0f} GB/s")
+
+
+if __name__ == "__main__":
+    main()
