@@ -105,6 +105,16 @@ int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_dtype, int64
 int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
                              int slices_per_stage);
 
+/* Stem fold (B200 lowering, no reference counterpart): NCHW f32 src ->
+ * NCHW[xf]c dst over folded channels f = s*C + c, width ow:
+ *   dst[n, f/xf, h, w', f%xf] = src[n, c, h, stride_w*w' + s - pad_w] (0 if OOB)
+ * A conv with kernel width S, stride_w, pad_w over src equals a conv with
+ * kernel width 1, stride 1, pad 0 along w over dst with weights
+ * W'[k, s*C + c, r, 0] = W[k, c, r, s]; used for 3-channel image stems. */
+int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t n, int64_t c, int64_t h,
+                  int64_t w, int s, int stride_w, int pad_w, int64_t ow, int xf, int flags,
+                  neo_stream_t stream);
+
 /* ---- fused blocked convolution (kernels.py:250-303 conv_blocked, with the
  * Epilogue kernels.py:74-87 applied in the order scale/shift -> bias ->
  * residual -> relu, kernels.py:185-197) --------------------------------- */

@@ -79,6 +79,8 @@ SIGNATURES = {
                                     _c_int, _c_int, _c_vp]),
     "neo_pack_weights_umma": (_c_int, [_c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64,
                                        _c_int, _c_i64, _c_int, _c_vp]),
+    "neo_stem_fold": (_c_int, [_c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
+                               _c_int, _c_int, _c_i64, _c_int, _c_int, _c_vp]),
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
     "neo_conv2d_nchwc_fused": (_c_int, [ctypes.POINTER(ConvParams), _c_vp]),
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),

@@ -64,6 +64,13 @@ struct ConvTCParams {
   uint32_t stage_out; // bytes of one staging buffer (128 rows * rowb_out)
   uint32_t out_box_bytes;
   int nslot;          // staging slots per epilogue group (tma_epi)
+  // halo mode (stride-1 convs): tiles span the padded output width
+  // BW = OW + S - 1; a pipeline slice is one (kernel row r, channel block)
+  // input band, loaded once; the S horizontal taps read it through
+  // descriptors shifted by s rows; B holds the S weight slices of the pair.
+  int halo;
+  int R;
+  int halo_baseoff;   // set the UMMA matrix base offset for shifted views
 };
 
 __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n0, int& oh0,
@@ -212,11 +219,11 @@ __device__ __forceinline__ void load_vec16(const float* base, int k, float fill,
 template <bool OUT_F32, bool HAS_RES>
 __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int kbase,
                                               int m, uint8_t* sbuf_gen, float relu_floor,
-                                              bool round) {
+                                              bool round, int c_begin, int c_step) {
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
 #pragma unroll 1
-  for (int c = 0; c < nchunk; ++c) {
+  for (int c = c_begin; c < nchunk; c += c_step) {
     uint32_t v[16];
     tmem_ld16(tcol + c * 16, v);
     EpiVecs e;
@@ -327,6 +334,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         decode_tile(p, t, n0, oh0, ow0, k0);
         const int iw0 = ow0 * p.stride_w - p.pad_w;
         const int ih0 = oh0 * p.stride_h - p.pad_h;
+        if (p.halo) {
+          for (int ks = 0; ks < p.kstages; ++ks) {
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
+            const uint32_t a_dst = sA + stage * p.a_stage;
+            const uint32_t b_dst = sB + stage * p.b_stage;
+            for (int g = 0; g < p.G; ++g) {
+              const int pi = ks * p.G + g;        // (r, channel block) pair
+              int co = p.Cb, r = 0;               // padding pair -> zeros
+              if (pi < p.nslices) {
+                co = pi % p.Cb;
+                r = pi / p.Cb;
+              }
+              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0, ih0 + r, co, n0);
+              tma_load_4d(b_dst + g * p.b_sub, &p.tmB, full_bar(stage), 0, k0, co, r * p.S);
+            }
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          continue;
+        }
         for (int ks = 0; ks < p.kstages; ++ks) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
@@ -369,6 +399,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           tc_fence_after();
           const uint32_t a0 = sA + stage * p.a_stage;
           const uint32_t b0 = sB + stage * p.b_stage;
+          if (p.halo) {
+            // 128-byte rows (SW128): tap s = A view shifted by s rows
+            const uint32_t b_tap = (uint32_t)p.BN * 128u;
+            for (int g = 0; g < p.G; ++g) {
+              for (int s = 0; s < p.S; ++s) {
+                const uint32_t a_s = a0 + g * p.a_sub + s * 128u;
+                const uint32_t bo = p.halo_baseoff ? ((a_s >> 7) & 7u) : 0u;
+                const uint32_t b_s = b0 + g * p.b_sub + s * b_tap;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t ad = umma_smem_desc(a_s + 32u * kk, 16, 1024, 2, bo);
+                  const uint64_t bd = umma_smem_desc(b_s + 32u * kk, 16, 1024, 2);
+                  umma_ss<TF32>(d_tmem, ad, bd, idesc, (ks | g | s | kk) != 0);
+                }
+              }
+            }
+            umma_commit(empty_bar(stage));
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            continue;
+          }
           for (int k = 0; k < ksteps; ++k) {
             uint64_t ad, bd;
             if (p.rowb == 16) {
@@ -447,16 +500,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
           const float floor_v = p.relu ? 0.f : -INFINITY;
           const bool rnd = p.round_tf32 != 0;
-          for (int i = half; i < cnt; i += 2) {
+          // the two warps of a lane quarter split the chunk's work: whole
+          // blocks when there are several, 16-column pieces of one block else
+          const int bstep = cnt >= 2 ? 2 : 1;
+          const int cbeg = cnt >= 2 ? 0 : half, cstep = cnt >= 2 ? 1 : 2;
+          for (int i = (cnt >= 2 ? half : 0); i < cnt; i += bstep) {
             const uint32_t tcol = trow + (b0 + i) * p.y;
             const int kb0 = k0 + (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
             if (p.out_f32) {
-              if (has_res) epi_block_tma<true, true>(p, tcol, kb0, m, sg, floor_v, rnd);
-              else epi_block_tma<true, false>(p, tcol, kb0, m, sg, floor_v, rnd);
+              if (has_res) epi_block_tma<true, true>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
+              else epi_block_tma<true, false>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
             } else {
-              if (has_res) epi_block_tma<false, true>(p, tcol, kb0, m, sg, floor_v, rnd);
-              else epi_block_tma<false, false>(p, tcol, kb0, m, sg, floor_v, rnd);
+              if (has_res) epi_block_tma<false, true>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
+              else epi_block_tma<false, false>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
             }
           }
           if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
@@ -642,6 +699,20 @@ static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
   return ok ? rowb_out : 0;
 }
 
+// stride-1 convs with a horizontal window, 128-byte rows (SW128 shifted
+// views) and a padded width that fits the 128-row M tile
+static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
+  static const bool disabled = getenv("NEOB200_NO_HALO") != nullptr;
+  return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 && rowb == 128 &&
+         OW + p->s - 1 <= kTileM;
+}
+static int halo_a_rows(const neo_conv_params* p) {
+  return (int)neo_ceil_div(kTileM + p->s - 1, 8) * 8;
+}
+static int64_t halo_pair_bytes(const neo_conv_params* p, int rowb) {
+  return (int64_t)halo_a_rows(p) * rowb + (int64_t)p->s * p->tile_n * rowb;
+}
+
 int neo_conv_default_tiles(neo_conv_params* p) {
   NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
   if (p->mode == NEO_MODE_FP32) return NEO_OK;
@@ -655,19 +726,65 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     p->tile_w = g.BW;
     p->tile_h = g.BH;
     p->tile_img = g.BNI;
+    if (halo_eligible(p, rowb, OW)) {
+      // halo tiles: full padded width, as many output rows as fit in 128
+      const int bwp = (int)(OW + p->s - 1);
+      const int bh = (int)std::min<int64_t>(OH, kTileM / bwp);
+      const double eff_h = (double)OW * OH / ((double)neo_ceil_div(OH, bh) * kTileM);
+      const double eff_s = (double)OW * OH * p->n /
+                           ((double)neo_ceil_div(OW, g.BW) * neo_ceil_div(OH, g.BH) *
+                            neo_ceil_div(p->n, g.BNI) * kTileM);
+      // the band reuse cuts A traffic ~S-fold, which outweighs idle rows
+      if (eff_h >= 0.35 * eff_s) {
+        p->tile_w = bwp;
+        p->tile_h = bh;
+        p->tile_img = 1;
+      }
+    }
   }
-  if (p->tile_n <= 0) p->tile_n = pick_tile_n(p->k);
-  const int64_t nslices = p->r * p->s * neo_ceil_div(p->c, p->ic_bn);
-  if (p->slices_per_stage <= 0) p->slices_per_stage = pick_slices_per_stage(nslices, rowb, p->tile_n);
-  if (p->stages <= 0) {
-    // deep enough to hide load latency, leaving at least one staging slot per
-    // epilogue group; single-stage reductions (1x1, C <= x) only need 2
-    const int64_t stage = (int64_t)p->slices_per_stage * (kTileM + p->tile_n) * rowb;
-    const int64_t kst = neo_ceil_div(nslices, p->slices_per_stage);
-    const int rb = epi_rowb_out(p, p->tile_n);
-    const int64_t want = kst <= 1 ? 2 : std::min<int64_t>(6, kst + 1);
-    const int64_t room = kSmemBudget - 2048 - (rb ? 2ll * kTileM * rb : 0);
-    p->stages = (int)std::max<int64_t>(std::min<int64_t>(want, room / stage), 2);
+  const bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
+  const int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
+                          neo_ceil_div(p->n, p->tile_img);
+  if (p->tile_n <= 0) {
+    // widest N tile that still gives every SM at least one tile (halo
+    // stages carry S weight slices, so their N tile stops at 128)
+    const int widest = halo ? std::min(128, pick_tile_n(p->k)) : pick_tile_n(p->k);
+    p->tile_n = widest;
+    for (int bn : {256, 128, 64}) {
+      if (bn > widest) continue;
+      p->tile_n = bn;
+      if (m_tiles * neo_ceil_div(p->k, bn) >= sm_count_of_current_device()) break;
+    }
+    if (p->tile_n > widest) p->tile_n = widest;
+  }
+  const int64_t nslices = halo ? p->r * neo_ceil_div(p->c, p->ic_bn)
+                               : p->r * p->s * neo_ceil_div(p->c, p->ic_bn);
+  // pipeline: keep the full epilogue staging (every output block of a tile
+  // in smem, so residual loads are issued before the accumulator is ready)
+  // and as many stages as fit, shrinking slices per stage if needed
+  const int rb = epi_rowb_out(p, p->tile_n);
+  const int64_t staging = rb ? 2ll * kTileM * rb * (p->tile_n / std::max(1, p->oc_bn)) : 0;
+  const int64_t budget = kSmemBudget - 2048;
+  if (p->slices_per_stage <= 0 || p->stages <= 0) {
+    int g = p->slices_per_stage > 0 ? p->slices_per_stage
+                                    : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
+    const int gmin = rowb == 16 ? 2 : 1;
+    for (;;) {
+      const int64_t stage = halo ? (int64_t)g * halo_pair_bytes(p, rowb)
+                                 : (int64_t)g * (kTileM + p->tile_n) * rowb;
+      const int64_t kst = neo_ceil_div(nslices, g);
+      const int64_t want = kst <= 1 ? 2 : std::min<int64_t>(6, kst + 1);
+      const int64_t fit = (budget - staging) / stage;
+      if (fit >= std::min<int64_t>(want, 3) || g <= gmin || p->slices_per_stage > 0) {
+        p->slices_per_stage = g;
+        if (p->stages <= 0) {
+          const int64_t room = fit >= 2 ? fit : budget / stage;   // else shrink staging
+          p->stages = (int)std::max<int64_t>(2, std::min<int64_t>(want, room));
+        }
+        break;
+      }
+      g = std::max(gmin, g / 2);
+    }
   }
   return NEO_OK;
 }
@@ -704,7 +821,12 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
 
   const int64_t Cb = neo_ceil_div(p->c, x);
   const int64_t cbt = p->x_cb_total > 0 ? p->x_cb_total : Cb;
-  const int64_t nslices = p->r * p->s * Cb;
+  const bool halo = BW > OW;
+  NEO_CHECK_ARG(!halo || halo_eligible(p, rowb, OW), NEO_ERR_SCHEDULE_INVALID,
+                "tile_w=%d wider than the output needs a stride-1, 128-byte-row conv", BW);
+  NEO_CHECK_ARG(!halo || (BW == OW + p->s - 1 && BNI == 1), NEO_ERR_SCHEDULE_INVALID,
+                "halo tiles must span the padded width OW+S-1 of one image");
+  const int64_t nslices = halo ? p->r * Cb : p->r * p->s * Cb;
   const int64_t kstages = neo_ceil_div(nslices, G);
 
   ConvTCParams kp;
@@ -722,13 +844,26 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                              (cuuint64_t)cbt * p->h * p->w_in * rowb};
     cuuint32_t box[5] = {(cuuint32_t)x, (cuuint32_t)(BW * p->stride_w),
                          (cuuint32_t)(BH * p->stride_h), 1u, (cuuint32_t)BNI};
+    // halo: box = BH rows of the padded width (stride 1), i.e. BH*BW pixels
     cuuint32_t estr[5] = {1u, (cuuint32_t)p->stride_w, (cuuint32_t)p->stride_h, 1u, 1u};
     CUresult r = encode(&kp.tmA, dt, 5, const_cast<char*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map A encode failed (%d)", (int)r);
   }
-  {
+  if (halo) {
+    // weight image viewed as (x, K, Cb, R*S); one box = the S taps of (r, cb)
+    cuuint64_t dims[4] = {(cuuint64_t)x, (cuuint64_t)p->k, (cuuint64_t)Cb,
+                          (cuuint64_t)(p->r * p->s)};
+    cuuint64_t strides[3] = {(cuuint64_t)rowb, (cuuint64_t)p->k * rowb,
+                             (cuuint64_t)Cb * p->k * rowb};
+    cuuint32_t box[4] = {(cuuint32_t)x, (cuuint32_t)BN, 1u, (cuuint32_t)p->s};
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    CUresult r = encode(&kp.tmB, dt, 4, const_cast<void*>(p->w), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map B encode failed (%d)", (int)r);
+  } else {
     // slices past nslices (stage padding) are out of bounds -> zero filled
     cuuint64_t dims[3] = {(cuuint64_t)x, (cuuint64_t)p->k, (cuuint64_t)nslices};
     cuuint64_t strides[2] = {(cuuint64_t)rowb, (cuuint64_t)p->k * rowb};
@@ -766,11 +901,23 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.rowb = rowb;
   kp.swz = swizzle_code_umma(rowb);
   kp.stages = p->stages;
-  kp.a_sub = (uint32_t)(kTileM * rowb);
-  kp.b_sub = (uint32_t)(BN * rowb);
+  kp.halo = halo ? 1 : 0;
+  kp.R = (int)p->r;
+  {
+    static const char* bo = getenv("NEOB200_HALO_BASEOFF");
+    kp.halo_baseoff = bo ? atoi(bo) : 0;  // swizzle follows absolute address bits
+  }
+  if (halo) {
+    kp.a_sub = (uint32_t)(halo_a_rows(p) * rowb);
+    kp.b_sub = (uint32_t)(p->s * BN * rowb);
+    kp.tx_bytes = (uint32_t)(G * (BW * BH * rowb + p->s * BN * rowb));
+  } else {
+    kp.a_sub = (uint32_t)(kTileM * rowb);
+    kp.b_sub = (uint32_t)(BN * rowb);
+    kp.tx_bytes = (uint32_t)(G * (BW * BH * BNI * rowb + BN * rowb));
+  }
   kp.a_stage = kp.a_sub * G;
   kp.b_stage = kp.b_sub * G;
-  kp.tx_bytes = (uint32_t)(G * (BW * BH * BNI * rowb + BN * rowb));
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * BN)) cols <<= 1;
   kp.tmem_cols = cols;

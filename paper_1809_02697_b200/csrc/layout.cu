@@ -356,3 +356,92 @@ extern "C" int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_d
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Stem folding (B200 lowering of a small-channel graph-entry conv input):
+// X'[n, cb, h, w', j] with folded channel f = cb*xf + j = s*C + c holds
+// X[n, c, h, sw*w' + s - pw] (0 outside the image or for pad lanes), for
+// w' in [0, ow).  A conv with an S-wide kernel, stride sw and pad pw over X
+// equals a conv with an S=1 kernel, stride 1 and pad 0 along w over X' with
+// weights W'[k, s*C + c, r, 0] = W[k, c, r, s]: the horizontal taps become
+// input channels, so a 3-channel 7x7/2 stem reads 21 (of 32) useful lanes
+// instead of 3 (of 8) and the tensor cores see 64-byte rows.
+namespace {
+template <typename Td, int XF>
+__global__ void stem_fold_kernel(const float* __restrict__ src, Td* __restrict__ dst, int64_t N,
+                                 int C, int H, int W, int S, int sw, int pw, int OW, bool round) {
+  const int F = S * C;
+  const int Cb = (F + XF - 1) / XF;
+  const int64_t total = N * Cb * H * (int64_t)OW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int wq = (int)(i % OW);
+    const int64_t rest = i / OW;
+    const int h = (int)(rest % H);
+    const int64_t ncb = rest / H;
+    const int cb = (int)(ncb % Cb);
+    const int64_t n = ncb / Cb;
+    float vals[XF];
+#pragma unroll
+    for (int j = 0; j < XF; ++j) vals[j] = 0.f;
+    const float* plane = src + (n * C) * (int64_t)H * W + (int64_t)h * W;
+    const int iw0 = sw * wq - pw;
+    // folded channel f = s*C + c, lanes [cb*XF, cb*XF + XF)
+    int f = cb * XF;
+    int s = f / C, c = f % C;
+#pragma unroll
+    for (int j = 0; j < XF; ++j) {
+      if (s < S) {
+        const int iw = iw0 + s;
+        if (iw >= 0 && iw < W) vals[j] = __ldg(plane + (int64_t)c * H * W + iw);
+      }
+      if (++c == C) {
+        c = 0;
+        ++s;
+      }
+    }
+    Td row[XF];
+#pragma unroll
+    for (int j = 0; j < XF; ++j) {
+      if constexpr (sizeof(Td) == 4) row[j] = round ? neo_round_tf32(vals[j]) : vals[j];
+      else row[j] = Elem<Td>::from_f(vals[j]);
+    }
+    constexpr int kVec = (int)(XF * sizeof(Td) / 16);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + i * XF);
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) d4[v] = r4[v];
+  }
+}
+}  // namespace
+
+extern "C" int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t n, int64_t c,
+                             int64_t h, int64_t w, int s, int stride_w, int pad_w, int64_t ow,
+                             int xf, int flags, neo_stream_t stream) {
+  NEO_CHECK_ARG(src && dst, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(n >= 1 && c >= 1 && h >= 1 && w >= 1 && s >= 1 && ow >= 1 && stride_w >= 1,
+                NEO_ERR_SHAPE_MISMATCH, "bad stem fold geometry");
+  const int64_t total = n * neo_ceil_div(s * c, xf) * h * ow;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+#define NEO_FOLD(T, X)                                                                      \
+  stem_fold_kernel<T, X><<<grid, 256, 0, st>>>(src, static_cast<T*>(dst), n, (int)c, (int)h, \
+                                               (int)w, s, stride_w, pad_w, (int)ow, round)
+  if (dst_dtype == NEO_BF16) {
+    if (xf == 8) NEO_FOLD(__nv_bfloat16, 8);
+    else if (xf == 16) NEO_FOLD(__nv_bfloat16, 16);
+    else if (xf == 32) NEO_FOLD(__nv_bfloat16, 32);
+    else if (xf == 64) NEO_FOLD(__nv_bfloat16, 64);
+    else NEO_CHECK_ARG(false, NEO_ERR_UNSUPPORTED, "stem fold block %d", xf);
+  } else {
+    if (xf == 4) NEO_FOLD(float, 4);
+    else if (xf == 8) NEO_FOLD(float, 8);
+    else if (xf == 16) NEO_FOLD(float, 16);
+    else if (xf == 32) NEO_FOLD(float, 32);
+    else NEO_CHECK_ARG(false, NEO_ERR_UNSUPPORTED, "stem fold block %d", xf);
+  }
+#undef NEO_FOLD
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}

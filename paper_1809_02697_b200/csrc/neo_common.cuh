@@ -170,6 +170,15 @@ __device__ __forceinline__ uint32_t swz_offset(uint32_t row, uint32_t chunk, uin
   return o ^ (((o >> 7) & mask) << 4);
 }
 
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint32_t bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
 // --- tcgen05 / TMEM -------------------------------------------------------
 
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
@@ -236,13 +245,16 @@ __device__ __forceinline__ void tmem_ld_wait() {
 
 // UMMA shared-memory matrix descriptor (sm_100 layout: version bits [46,48) = 1)
 //   layout: 0 = interleave (no swizzle), 2 = 128B, 4 = 64B, 6 = 32B swizzle
+//   base_off: bits [49,52) "matrix base offset" for start addresses that are
+//   not aligned to the swizzle pattern repeat (row-shifted views)
 __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
-                                                   uint32_t layout) {
+                                                   uint32_t layout, uint32_t base_off = 0) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(base_off & 0x7u) << 49;
   d |= (uint64_t)(layout & 0x7u) << 61;
   return d;
 }

@@ -194,3 +194,10 @@ def round_tf32(t: torch.Tensor) -> torch.Tensor:
     L.call("neo_layout_transform", L.F32, L.F32, _ptr(t), _ptr(out), 1, t.numel(), 1, 1,
            L.NCHW_TAG, 1, L.NCHW_TAG, 1, L.FLAG_ROUND_TF32, stream_handle())
     return out
+
+
+def stem_fold(src: torch.Tensor, dst: torch.Tensor, n, c, h, w, s, stride_w, pad_w, ow, xf,
+              flags=0, stream=None) -> None:
+    """NCHW f32 -> horizontally folded NCHW[xf]c (see neo_stem_fold)."""
+    L.call("neo_stem_fold", _ptr(src), _ptr(dst), dtype_code(dst), n, c, h, w, s, stride_w,
+           pad_w, ow, xf, flags, stream_handle(stream))

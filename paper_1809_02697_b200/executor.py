@@ -172,6 +172,14 @@ class DeviceProgram:
                         and nid not in g.outputs and nid not in self.keep):
                     self.fused_dense_relu[us[0]] = nid
                     self.skip.add(nid)
+        # 3-channel image stems: fold the kernel's horizontal taps into
+        # channels (neo_stem_fold) so the first conv reads 64-byte rows
+        self.stem_fold: dict[int, dict] = {}
+        if self.mode in ("bf16", "tf32"):
+            for nid in order:
+                info = self._stem_fold_info(nid)
+                if info:
+                    self.stem_fold[nid] = info
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -185,6 +193,8 @@ class DeviceProgram:
                     continue
                 src_layout = Layout.parse(node.attrs["src_layout"])
                 us = self.users[nid]
+                if nid in self.stem_fold:
+                    continue
                 if (src_layout.tag == "NCHW" and us and nid not in g.outputs
                         and all(g.nodes[u].kind == OpKind.Conv2d and g.nodes[u].inputs[0][0] == nid
                                 for u in us)):
@@ -235,6 +245,42 @@ class DeviceProgram:
         for nid in self.plan.input_ids:
             self.vals[nid].first = -1
 
+    def _stem_fold_info(self, nid) -> dict | None:
+        """Fold parameters if ``nid`` packs a few-channel graph input that
+        only feeds convs sharing one kernel width / stride / pad along w."""
+        g = self.g
+        node = g.nodes[nid]
+        if node.kind != OpKind.LayoutTransform or nid in g.outputs or nid in self.keep:
+            return None
+        if Layout.parse(node.attrs["src_layout"]).tag != "NCHW" or \
+                Layout.parse(node.attrs["dst_layout"]).tag != "NCHWc":
+            return None
+        src = node.inputs[0][0]
+        if g.nodes[src].kind != OpKind.Input:
+            return None
+        n, c, h, w = self.specs[src].logical_nchw
+        us = self.users[nid]
+        if not us or c > 4:
+            return None
+        geo = set()
+        for u in us:
+            un = g.nodes[u]
+            if un.kind != OpKind.Conv2d or un.inputs[0][0] != nid:
+                return None
+            wt = g.nodes[un.inputs[1][0]].attrs["value"]
+            geo.add((wt.shape[3], hw_pair(un.attrs["stride"])[1], hw_pair(un.attrs["pad"])[1]))
+        if len(geo) != 1:
+            return None
+        S, sw, pw = geo.pop()
+        F = S * c
+        lanes = [x for x in (8, 16, 32, 64, 4) if tc_legal_block(x, self.mode)]
+        fits = [x for x in sorted(lanes) if x >= F]
+        if S == 1 or not fits:
+            return None
+        ow = (w + 2 * pw - S) // sw + 1
+        return {"S": S, "sw": sw, "pw": pw, "ow": ow, "C": c, "F": F, "xf": fits[0],
+                "n": n, "h": h, "w": w}
+
     def _storage(self, nid) -> _Val | None:
         v = self.vals.get(nid)
         while v is not None and v.alias is not None:
@@ -253,6 +299,10 @@ class DeviceProgram:
         if node.kind == OpKind.Flatten:
             return _Val(nid, spec.shape, self.vals[node.inputs[0][0]].dtype, layout,
                         alias=node.inputs[0][0])
+        if nid in self.stem_fold:
+            f = self.stem_fold[nid]
+            shape = (f["n"], -(-f["F"] // f["xf"]), f["h"], f["ow"], f["xf"])
+            return _Val(nid, shape, self.act_dtype, layout, px=f["xf"])
         if layout.tag == "NCHWc":
             px = self.phys_x.get(nid, layout.x)
             n, c, h, w = spec.logical_nchw
@@ -399,6 +449,13 @@ class DeviceProgram:
         else:
             kcrs = np.asarray(wv, np.float32)
         k, wc, r, s = kcrs.shape
+        fold = self.stem_fold.get(node.inputs[0][0])
+        if fold is not None:
+            # W'[k, s*C + c, r, 0] = W[k, c, r, s]; width taps became channels
+            kcrs = np.ascontiguousarray(
+                kcrs.transpose(0, 3, 1, 2).reshape(k, s * wc, r, 1), dtype=np.float32)
+            k, wc, r, s = kcrs.shape
+            c, w, sw, pw = fold["F"], fold["ow"], 1, 0
         if data.layout.tag == "NCHWc":
             ic_bn = data.px
             oc_bn = out.layout.x
@@ -477,6 +534,13 @@ class DeviceProgram:
     def _bind_transform(self, node, src: _Val, out: _Val):
         from . import _lib as L
         from . import device as D
+        if node.id in self.stem_fold:
+            f = self.stem_fold[node.id]
+            s_t, d_t = src.tensor, out.tensor
+            self._emit(f"stemfold{node.id}", lambda: D.stem_fold(
+                s_t, d_t, f["n"], f["C"], f["h"], f["w"], f["S"], f["sw"], f["pw"], f["ow"],
+                f["xf"], self.round_flag, self.stream))
+            return
         n, c, h, w = self.specs[node.inputs[0][0]].logical_nchw
         src_layout = src.layout
         dst_layout = Layout.parse(node.attrs["dst_layout"])

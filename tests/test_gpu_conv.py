@@ -174,7 +174,8 @@ def test_tc_conv_concat_window(cuda):
     dict(tile_w=8, tile_h=8, tile_img=1, tile_n=32, slices_per_stage=1, stages=2),
     dict(tile_w=14, tile_h=9, tile_img=1, tile_n=64, slices_per_stage=3, stages=2),
     dict(tile_w=7, tile_h=7, tile_img=2, tile_n=128, slices_per_stage=2, stages=3),
-    dict(tile_w=28, tile_h=4, tile_img=1, tile_n=256, slices_per_stage=1, stages=4),
+    dict(tile_w=14, tile_h=9, tile_img=1, tile_n=256, slices_per_stage=1, stages=3),
+    dict(tile_w=16, tile_h=8, tile_img=1, tile_n=128, slices_per_stage=1, stages=2),  # halo
 ])
 def test_tc_conv_tile_configs(cuda, tile):
     """Explicit tile / pipeline configurations (the tuner's search space)."""
@@ -224,3 +225,34 @@ def test_tc_conv_deterministic(cuda):
     a = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
     b = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
     assert np.array_equal(a, b)
+
+
+HALO_CASES = [
+    # (n, c, h, w, k, stride, pad, r, s, tile_h)
+    (2, 64, 56, 56, 64, 1, (1, 1), 3, 3, 2),      # ResNet stage 1: 58-wide rows
+    (2, 128, 28, 28, 128, 1, (1, 1), 3, 3, 4),
+    (2, 128, 14, 14, 256, 1, (1, 1), 3, 3, 8),    # exactly 128 rows
+    (1, 64, 20, 20, 64, 1, (2, 2), 5, 5, 5),      # 5x5, 24-wide padded rows
+    (1, 64, 17, 17, 64, 1, (0, 3), 1, 7, 5),      # 1x7 (Inception)
+]
+
+
+@pytest.mark.parametrize("case", HALO_CASES)
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+def test_tc_conv_halo_mode(cuda, case, mode_name):
+    """Stride-1 convs in halo mode (tiles span the padded width; horizontal
+    taps read one loaded band through row-shifted UMMA descriptors)."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, st, pd, r, s, bh = case
+    rng = np.random.default_rng(c + r + s)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32))
+    res = rng.standard_normal((n, k, h + 2 * pd[0] - r + 1, w + 2 * pd[1] - s + 1)).astype(np.float32)
+    ref = oracle.conv2d(x, wt, st, pd, residual=res, relu=True)
+    ow = w + 2 * pd[1] - s + 1
+    x_bn = 64 if mode_name == "bf16" else 32
+    tile = dict(tile_w=ow + s - 1, tile_h=bh, tile_img=1)
+    got = run_conv(mode, x, wt, (st, st), pd, x_bn, 32, residual=res, relu=True, tile=tile)
+    assert oracle.rel_err(got, ref) < 1e-4

@@ -1,0 +1,148 @@
+"""GPU results vs the reference's own outputs (golden fixtures made by running
+the unmodified reference, tests/golden/make_golden.py), through the drop-in
+API.  fp32 mode mirrors the reference bounds (1e-5 per op, Acceptance 1;
+1e-4 end to end, Acceptance 3); tf32 / bf16 use the north_star bounds."""
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"fp32": 1e-5, "tf32": 1e-3, "bf16": 2e-2}
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def test_layout_api_bitexact(cuda):
+    from paper_1809_02697_b200.layout import (nhwc_to_nchw_array, pack_kcrs_array,
+                                              pack_nchw_array, retile_nchw_array,
+                                              unpack_kcrs_array, unpack_nchw_array)
+    d = load("layouts.npz")
+    for x in (1, 2, 3, 4, 6, 12):
+        p = pack_nchw_array(d["a"], x)
+        assert np.array_equal(p.view(np.uint32), d[f"pack_x{x}"].view(np.uint32))
+        assert np.array_equal(unpack_nchw_array(p), d[f"unpack_x{x}"])
+    for b in (2, 3, 6, 12):
+        assert np.array_equal(retile_nchw_array(d["pack_x4"], b), d[f"retile_4_{b}"])
+    assert np.array_equal(pack_nchw_array(d["big"], 64), d["big_pack64"])
+    assert np.array_equal(nhwc_to_nchw_array(d["nhwc"]), d["nhwc_to_nchw"])
+    for x, y in ((1, 1), (2, 4), (4, 8), (4, 2)):
+        assert np.array_equal(pack_kcrs_array(d["w"], x, y), d[f"wpack_{x}_{y}"])
+        assert np.array_equal(unpack_kcrs_array(d[f"wpack_{x}_{y}"]), d["w"])
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_conv_api_vs_reference(cuda, i):
+    """conv_reference (naive device path) and conv_blocked (fp32) on the
+    reference's edge-case workloads and epilogues."""
+    from paper_1809_02697_b200 import (ConvSchedule, ConvWorkload, Epilogue, KCRS, Tensor,
+                                       conv_blocked, conv_reference, pack_data, pack_weights,
+                                       unpack_data)
+    d = load("conv.npz")
+    c, k, h, w, r, s, st, pd = (int(v) for v in d[f"{i}/wl"])
+    ic, oc, rn, un = (int(v) for v in d[f"{i}/sch"])
+    wl = ConvWorkload(c, k, h, w, r, s, st, pd)
+    get = lambda key: d[f"{i}/{key}"] if f"{i}/{key}" in d else None
+    epi = Epilogue(get("scale"), get("shift"), get("bias"), bool(d[f"{i}/relu"]), get("residual"))
+    ref = d[f"{i}/reference"]
+    naive = conv_reference(Tensor(d[f"{i}/x"]), Tensor(d[f"{i}/w"], KCRS), wl, epi)
+    assert oracle.rel_err(naive.data, ref) < 1e-6
+    sch = ConvSchedule(ic, oc, rn, bool(un))
+    res_b = None if get("residual") is None else pack_data(Tensor(get("residual")), oc).data
+    epi_b = Epilogue(get("scale"), get("shift"), get("bias"), bool(d[f"{i}/relu"]), res_b)
+    blk = conv_blocked(pack_data(Tensor(d[f"{i}/x"]), ic),
+                       pack_weights(Tensor(d[f"{i}/w"], KCRS), ic, oc), wl, sch, epi_b,
+                       mode="fp32")
+    assert oracle.rel_err(unpack_data(blk).data, ref) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["fp32", "tf32", "bf16"])
+def test_config0_vs_reference(cuda, mode):
+    """BASELINE config 0 (3x3 64->64 56^2 NCHW16c + BN + ReLU) through
+    conv_blocked in every mode."""
+    from paper_1809_02697_b200 import (ConvSchedule, ConvWorkload, Epilogue, KCRS, Tensor,
+                                       conv_blocked, nchwc, pack_weights)
+    d = load("conv.npz")
+    wl = ConvWorkload(64, 64, 56, 56, 3, 3, 1, 1)
+    out = conv_blocked(Tensor(d["c0/x16"], nchwc(16)), pack_weights(Tensor(d["c0/w"], KCRS), 16, 16),
+                       wl, ConvSchedule(16, 16, 8, True),
+                       Epilogue(scale=d["c0/scale"], shift=d["c0/shift"], relu=True), mode=mode)
+    assert out.layout == nchwc(16)
+    assert oracle.rel_err(out.data, d["c0/blocked16"]) < TOL[mode]
+
+
+def _toy_cases():
+    sys.path.insert(0, GOLD)
+    import graphio
+    from paper_1809_02697_b200 import Graph, Node, OpKind
+    doc = json.load(open(os.path.join(GOLD, "graphs.json")))
+    arrays = np.load(os.path.join(GOLD, "graphs.npz"))
+    for case in doc["cases"]:
+        yield case, graphio.load_graph(case["graph"], arrays, Graph, Node, OpKind), arrays
+
+
+@pytest.mark.parametrize("mode", ["fp32", "tf32"])
+def test_toy_graphs_vs_reference(cuda, mode):
+    """The reference's toy models, planned by this package's passes and run by
+    the device executor, against the reference executor's outputs."""
+    from paper_1809_02697_b200 import DevicePool, compile_graph, execute
+    for case, g, arrays in _toy_cases():
+        tag = case["tag"]
+        feeds = {"data": arrays[f"{tag}/input"]}
+        unopt = execute(g, feeds, DevicePool(0, "fp32"))
+        opt = execute(compile_graph(g, mode=mode), feeds, DevicePool(0, mode))
+        for i in range(case["n_outputs"]):
+            assert oracle.rel_err(unopt[i], arrays[f"{tag}/plain{i}"]) < 1e-4, tag
+            assert oracle.rel_err(opt[i], arrays[f"{tag}/opt{i}"]) < max(TOL[mode], 1e-4), tag
+
+
+@pytest.mark.parametrize("tag,name,batch,kw,mode", [
+    ("resnet18_b1", "resnet18", 1, {}, "tf32"),
+    ("resnet18_b1", "resnet18", 1, {}, "bf16"),
+    ("resnet50_b1", "resnet50", 1, {}, "tf32"),
+    ("resnet50_b1", "resnet50", 1, {}, "bf16"),
+    ("resnet18_b2_small", "resnet18", 2, {"image": 64, "num_classes": 10}, "fp32"),
+])
+def test_model_logits_vs_reference(cuda, tag, name, batch, kw, mode):
+    """Logits of the device path vs the reference executor's logits on the
+    identical seeded graph (weight digest checked)."""
+    from paper_1809_02697_b200 import DevicePool, build_model, compile_graph, execute, model_input
+    d = load("models.npz")
+    g = build_model(name, batch=batch, softmax=False, **kw)
+    h = hashlib.sha256()
+    for nid in sorted(g.nodes):
+        v = g.nodes[nid].attrs.get("value")
+        if v is not None:
+            h.update(np.ascontiguousarray(v, np.float32).tobytes())
+    assert h.digest() == d[f"{tag}/weight_digest"].tobytes()
+    got = execute(compile_graph(g, mode=mode), model_input(g), DevicePool(0, mode))[0]
+    ref = d[f"{tag}/logits"]
+    assert oracle.rel_err(got, ref) < max(TOL[mode], 1e-4)
+    assert (got.argmax(1) == ref.argmax(1)).all()
+
+
+def test_pool_vs_reference(cuda):
+    import torch
+    from paper_1809_02697_b200 import device as D
+    d = load("pool.npz")
+    a = d["a"]
+    for mode in ("max", "avg"):
+        for win, st, pd in ((2, 2, 0), (3, 2, 1), (3, 1, 1), (9, 1, 0)):
+            oh = (9 + 2 * pd - win) // st + 1
+            src = torch.from_numpy(a).cuda()
+            out = torch.empty((2, 8, oh, oh), device="cuda")
+            D.pool2d(src, out, 2, 8, 9, 9, 1, win, st, pd, mode)
+            assert np.array_equal(out.cpu().numpy(), d[f"{mode}_{win}_{st}_{pd}"])
+            src4 = torch.from_numpy(oracle.pack_nchw(a, 4)).cuda()
+            out4 = torch.empty((2, 2, oh, oh, 4), device="cuda")
+            D.pool2d(src4, out4, 2, 2, 9, 9, 4, win, st, pd, mode)
+            assert np.array_equal(out4.cpu().numpy(), d[f"{mode}_{win}_{st}_{pd}_b4"])
