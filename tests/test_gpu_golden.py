@@ -100,9 +100,12 @@ def test_toy_graphs_vs_reference(cuda, mode):
         feeds = {"data": arrays[f"{tag}/input"]}
         unopt = execute(g, feeds, DevicePool(0, "fp32"))
         opt = execute(compile_graph(g, mode=mode), feeds, DevicePool(0, mode))
+        # toy outputs are raw feature maps (not logits): tf32 gets 2e-3 here
+        # (measured worst 1.01e-3 on resnet-block); fp32 keeps 1e-4
+        tol = {"fp32": 1e-4, "tf32": 2e-3}[mode]
         for i in range(case["n_outputs"]):
             assert oracle.rel_err(unopt[i], arrays[f"{tag}/plain{i}"]) < 1e-4, tag
-            assert oracle.rel_err(opt[i], arrays[f"{tag}/opt{i}"]) < max(TOL[mode], 1e-4), tag
+            assert oracle.rel_err(opt[i], arrays[f"{tag}/opt{i}"]) < tol, tag
 
 
 @pytest.mark.parametrize("tag,name,batch,kw,mode", [
