@@ -25,7 +25,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -63,55 +62,56 @@ def dist_env():
 # clocks sampled during the timed region
 
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clocks and clock-event (throttle) reasons through NVML every
+    5 ms while the timed region runs (the recipe's nvidia-smi clocks line,
+    at a rate that resolves a sub-second region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self.proc = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.rows.append((sm, reasons))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=2)
         return False
 
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for name, val in zip(names, r[5:9]):
-                if val.strip().lower() == "active":
-                    reasons.add(name)
-        loaded = sorted(sm)[len(sm) // 2:] if sm else []
-        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        sms = sorted(r[0] for r in self.rows)
+        reasons = sorted({name for _, bits in self.rows for name, mask in self.REASONS.items()
+                          if bits & mask})
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml 5 ms"}
 
 
 def peaks() -> tuple[dict, str]:
@@ -251,7 +251,6 @@ def main():
     name = prog.input_names()[0]
     pinned = torch.from_numpy(feeds[name]).pin_memory()
     out_t = prog.output_tensors()[0]
-    out_host = torch.empty(out_t.shape, dtype=out_t.dtype).pin_memory()
     stream = prog.stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=local)
 
@@ -282,21 +281,22 @@ def main():
         wall = time.perf_counter() - wall0
     barrier()
     dev_s = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
-    # ---- end to end through the public API (pinned host in, result out) --
-    e2e_evs = []
-    for i in range(args.steps + args.warmup):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        prog.set_inputs({name: pinned})
-        prog.launch()
-        with torch.cuda.stream(stream):
-            out_host.copy_(out_t, non_blocking=True)
-        b.record(stream)
-        if i >= args.warmup:
-            e2e_evs.append((a, b))
-    stream.synchronize()
+    # ---- end to end through the public API: every step uploads its pinned
+    # host batch (copy stream, double-buffered, overlapping the previous
+    # forward) and reads the result back to pinned host memory ------------
+    outs = [torch.empty(out_t.shape, dtype=out_t.dtype).pin_memory()
+            for _ in range(args.steps + args.warmup)]
+    prog.pipeline([pinned] * args.warmup, outs[:args.warmup])
+    torch.cuda.synchronize()
     barrier()
-    e2e_s = sum(a.elapsed_time(b) for a, b in e2e_evs) * 1e-3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(prog._copy_stream)
+    prog.pipeline([pinned] * args.steps, outs[args.warmup:])
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    e2e_s = e0.elapsed_time(e1) * 1e-3
+    out_host = outs[-1]
     # ---- dominant-kernel roofline (instrumented, un-graphed pass) -------
     pk, pk_kind = peaks()
     roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind)

@@ -744,6 +744,39 @@ class DeviceProgram:
         self.stream.synchronize()
         return [t.float().cpu().numpy() for t in self.output_tensors()]
 
+    def pipeline(self, batches, outputs):
+        """Serving loop over pinned host batches: the upload of batch i+1 (a
+        separate copy stream into a double-buffered device staging area)
+        overlaps the forward of batch i; each forward's first-output tensor
+        is read back into ``outputs[i]`` (pinned host tensors).  Every copy
+        is part of the loop; returns after all work is enqueued.  Inputs must
+        be NCHW f32 and the graph must have a single input."""
+        import torch
+        if len(self.plan.input_ids) != 1:
+            raise InputMismatch("pipeline() needs a single-input graph")
+        dst = self.vals[self.plan.input_ids[0]].tensor
+        if not hasattr(self, "_staging"):
+            self._staging = [torch.empty_like(dst) for _ in range(2)]
+            self._copy_stream = torch.cuda.Stream(self.device)
+            self._copied = [torch.cuda.Event() for _ in range(2)]
+            self._consumed = [torch.cuda.Event() for _ in range(2)]
+            for ev in self._consumed:
+                ev.record(self.stream)
+        out_dev = self.output_tensors()[0]
+        for i, host in enumerate(batches):
+            slot = i & 1
+            with torch.cuda.stream(self._copy_stream):
+                self._copy_stream.wait_event(self._consumed[slot])
+                self._staging[slot].copy_(host, non_blocking=True)
+                self._copied[slot].record(self._copy_stream)
+            with torch.cuda.stream(self.stream):
+                self.stream.wait_event(self._copied[slot])
+                dst.copy_(self._staging[slot], non_blocking=True)
+                self._consumed[slot].record(self.stream)
+            self.launch()
+            with torch.cuda.stream(self.stream):
+                outputs[i].copy_(out_dev, non_blocking=True)
+
 
 # ---------------------------------------------------------------------------
 # reference-compatible entry points
