@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--mode", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--untuned", action="store_true", help="ignore the tuned tile schedules")
     return ap.parse_args()
 
 
@@ -245,7 +246,11 @@ def main():
 
     g = build_model(args.model, batch=args.batch)
     flops_step = float(conv_flops(g))
-    planned = compile_graph(g, mode=args.mode)
+    from paper_1809_02697_b200 import ScheduleDb
+    from paper_1809_02697_b200.tuning import DEFAULT_DB, tuned_assignment
+    db = None if args.untuned else ScheduleDb(DEFAULT_DB)
+    tuned = db is not None and tuned_assignment(g, db, args.mode) is not None
+    planned = compile_graph(g, mode=args.mode, db=db)
     prog = DeviceProgram(ExecutablePlan.compile(planned), local, args.mode)
     feeds = model_input(g, seed=1 + rank)
     name = prog.input_names()[0]
@@ -332,6 +337,8 @@ def main():
                        "parallelism": f"dp{world} batch sharding (no collective)",
                        "l2": "flushed between timed steps (256 MiB write outside the events)",
                        "conv_gflop_per_image": flops_step / args.batch / 1e9,
+                       "schedules": "per-layer tuned tiles (schedules/b200.npsd)" if tuned
+                                    else "in-kernel default tiles",
                        "wall_s_timed_region": wall},
             "e2e": {"value": e2e_value, "unit": "images/s",
                     "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),

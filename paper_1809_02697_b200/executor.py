@@ -474,6 +474,8 @@ class DeviceProgram:
         sched = node.attrs.get("schedule") or {}
         tile = {f: sched.get(f, 0) for f in ("tile_w", "tile_h", "tile_img", "tile_n",
                                              "slices_per_stage", "stages")}
+        if fold is not None:      # tuned for the unfolded workload: let the kernel pick
+            tile = {}
         if use_tc:
             mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
             wk = self._upload(kcrs)

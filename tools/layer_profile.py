@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--mode", default="bf16")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default="")
+    ap.add_argument("--untuned", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -31,8 +32,10 @@ def main():
     from paper_1809_02697_b200 import device as D
     from paper_1809_02697_b200.graph import hw_pair, infer_shapes
 
+    from paper_1809_02697_b200 import ScheduleDb
+    from paper_1809_02697_b200.tuning import DEFAULT_DB
     g = build_model(args.model, batch=args.batch)
-    planned = compile_graph(g, mode=args.mode)
+    planned = compile_graph(g, mode=args.mode, db=None if args.untuned else ScheduleDb(DEFAULT_DB))
     prog = DeviceProgram(ExecutablePlan.compile(planned), 0, args.mode, use_graph=False)
     prog.set_inputs(model_input(g))
     specs = infer_shapes(planned)
@@ -49,7 +52,9 @@ def main():
         flops = 2 * n * k * c * r * s * oh * ow
         byts = es * (n * c * h * w + k * c * r * s + n * k * oh * ow *
                      (2 if (node.attrs.get("epilogue") or {}).get("residual") else 1))
-        info[f"conv{nid}"] = dict(c=c, k=k, h=h, w=w, r=r, s=s,
+        sch = node.attrs.get("schedule") or {}
+        tile = "/".join(str(sch.get(f, 0)) for f in ("tile_n", "slices_per_stage", "stages"))
+        info[f"conv{nid}"] = dict(c=c, k=k, h=h, w=w, r=r, s=s, tile=tile,
                                   stride=hw_pair(node.attrs["stride"])[0], flops=flops,
                                   bytes=byts)
     # tile config the kernel picks
@@ -87,7 +92,7 @@ def main():
         if "flops" in row:
             print(f"{row['launch']:>10} C{row['c']:>5} K{row['k']:>5} {row['h']:>3}x{row['w']:<3} "
                   f"{row['r']}x{row['s']} s{row['stride']} {row['us']:8.1f} us "
-                  f"{row['tflops']:7.1f} TF/s {row['gbs']:7.0f} GB/s")
+                  f"{row['tflops']:7.1f} TF/s {row['gbs']:7.0f} GB/s {row.get('tile', '')}")
         else:
             print(f"{row['launch']:>10} {row['us']:8.1f} us")
     if args.out:
