@@ -357,20 +357,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
           continue;
         }
+        // slice = (r, s, channel block), channel block fastest; walked with
+        // counters (no divisions on the single producer thread)
+        int co = 0, sc = 0, rc = 0, sl = 0;
         for (int ks = 0; ks < p.kstages; ++ks) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
           const uint32_t a_dst = sA + stage * p.a_stage;
-          for (int g = 0; g < p.G; ++g) {
-            const int sl = ks * p.G + g;
-            int co = p.Cb, r = 0, s = 0;  // padding slice: fully out of bounds -> zeros
+          for (int g = 0; g < p.G; ++g, ++sl) {
             if (sl < p.nslices) {
-              co = sl % p.Cb;
-              const int rs = sl / p.Cb;
-              s = rs % p.S;
-              r = rs / p.S;
+              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0 + sc, ih0 + rc, co,
+                          n0);
+              if (++co == p.Cb) {
+                co = 0;
+                if (++sc == p.S) {
+                  sc = 0;
+                  ++rc;
+                }
+              }
+            } else {   // stage padding slice: fully out of bounds -> zeros
+              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, 0, 0, p.Cb, n0);
             }
-            tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0 + s, ih0 + r, co, n0);
           }
           tma_load_3d(sB + stage * p.b_stage, &p.tmB, full_bar(stage), 0, k0, ks * p.G);
           if (++stage == p.stages) {
@@ -385,6 +392,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // ---------------- MMA issuer ----------------
       const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, kTileM, p.BN);
       const int ksteps = p.G * p.rowb / 32;
+      // descriptors of stage 0; other stages / K steps only move the 14-bit
+      // start-address field (byte offset >> 4), so they are formed by adds
+      const bool narrow = p.rowb == 16;
+      const uint64_t adesc0 = narrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
+                                     : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
+      const uint64_t bdesc0 = narrow ? umma_smem_desc(sB, p.b_sub, 128, 0)
+                                     : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
+      const int kpr_shift = p.rowb >= 128 ? 2 : p.rowb == 64 ? 1 : 0;  // K steps per row
+      const uint32_t kpr_mask = (1u << kpr_shift) - 1u;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -422,19 +438,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
             continue;
           }
+          const uint64_t ad_stage = adesc0 + ((uint64_t)(stage * p.a_stage) >> 4);
+          const uint64_t bd_stage = bdesc0 + ((uint64_t)(stage * p.b_stage) >> 4);
           for (int k = 0; k < ksteps; ++k) {
-            uint64_t ad, bd;
-            if (p.rowb == 16) {
+            uint32_t aoff, boff;
+            if (narrow) {
               // 16-byte rows: no swizzle; one K step spans two slices (LBO)
-              ad = umma_smem_desc(a0 + 2 * k * p.a_sub, p.a_sub, 128, 0);
-              bd = umma_smem_desc(b0 + 2 * k * p.b_sub, p.b_sub, 128, 0);
+              aoff = 2u * k * p.a_sub;
+              boff = 2u * k * p.b_sub;
             } else {
-              const uint32_t byte = 32u * k;
-              const uint32_t sub = byte / p.rowb, inrow = byte % p.rowb;
-              ad = umma_smem_desc(a0 + sub * p.a_sub + inrow, 16, 8 * p.rowb, p.swz);
-              bd = umma_smem_desc(b0 + sub * p.b_sub + inrow, 16, 8 * p.rowb, p.swz);
+              const uint32_t sub = (uint32_t)k >> kpr_shift, inrow = ((uint32_t)k & kpr_mask) << 5;
+              aoff = sub * p.a_sub + inrow;
+              boff = sub * p.b_sub + inrow;
             }
-            umma_ss<TF32>(d_tmem, ad, bd, idesc, (ks | k) != 0);
+            umma_ss<TF32>(d_tmem, ad_stage + (aoff >> 4), bd_stage + (boff >> 4), idesc,
+                          (ks | k) != 0);
           }
           umma_commit(empty_bar(stage));
           if (++stage == p.stages) {
