@@ -192,24 +192,23 @@ __device__ __forceinline__ void epi_chunk(const ConvTCParams& p, const uint32_t 
 //   v = fma(v, scale, shift) ; v += bias ; v += residual ; v = max(v, floor)
 // (floor = 0 for relu, -inf otherwise) -- the reference order of
 // kernels.py:185-197 with one rounding per reference operation.
-struct EpiVecs {
-  float sc[16], sh[16], bi[16];
-};
+// The tile's per-column epilogue vectors live in shared memory (staged once
+// per tile by the epilogue group, identity values for absent vectors), so the
+// per-element math is branch-free and no global load sits on its path:
+//   v = fma(v, scale, shift) ; v += bias ; v += residual ; v = max(v, floor)
+// (floor = 0 for relu, -inf otherwise) -- the reference order of
+// kernels.py:185-197 with one rounding per reference operation.
+constexpr int kParamFloats = 3 * 256;   // scale | shift | bias for BN <= 256
 
-__device__ __forceinline__ void load_vec16(const float* base, int k, float fill, float (&dst)[16]) {
-  if (base) {
-    const float4* v4 = reinterpret_cast<const float4*>(base + k);
+__device__ __forceinline__ void load_par16(const float* par, int col, float (&dst)[16]) {
+  const float4* v4 = reinterpret_cast<const float4*>(par + col);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 t = __ldg(v4 + q);
-      dst[4 * q] = t.x;
-      dst[4 * q + 1] = t.y;
-      dst[4 * q + 2] = t.z;
-      dst[4 * q + 3] = t.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) dst[j] = fill;
+  for (int q = 0; q < 4; ++q) {
+    const float4 t = v4[q];
+    dst[4 * q] = t.x;
+    dst[4 * q + 1] = t.y;
+    dst[4 * q + 2] = t.z;
+    dst[4 * q + 3] = t.w;
   }
 }
 
@@ -217,25 +216,26 @@ __device__ __forceinline__ void load_vec16(const float* base, int k, float fill,
 // epilogue -> swizzled smem row (which already holds the residual block when
 // HAS_RES).  OUT_F32 selects f32 vs bf16 storage.
 template <bool OUT_F32, bool HAS_RES>
-__device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int kbase,
-                                              int m, uint8_t* sbuf_gen, float relu_floor,
-                                              bool round, int c_begin, int c_step) {
+__device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int col0,
+                                              int m, uint8_t* sbuf_gen, const float* par,
+                                              float relu_floor, bool round, int c_begin,
+                                              int c_step) {
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
 #pragma unroll 1
   for (int c = c_begin; c < nchunk; c += c_step) {
     uint32_t v[16];
     tmem_ld16(tcol + c * 16, v);
-    EpiVecs e;
-    const int k = kbase + c * 16;
-    load_vec16(p.scale, k, 1.f, e.sc);
-    load_vec16(p.shift, k, 0.f, e.sh);
-    load_vec16(p.bias, k, 0.f, e.bi);
+    float sc[16], sh[16], bi[16];
+    const int col = col0 + c * 16;
+    load_par16(par, col, sc);
+    load_par16(par + 256, col, sh);
+    load_par16(par + 512, col, bi);
     tmem_ld_wait();
     float f[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      f[j] = fmaf(__uint_as_float(v[j]), e.sc[j], e.sh[j]) + e.bi[j];
+      f[j] = fmaf(__uint_as_float(v[j]), sc[j], sh[j]) + bi[j];
 #pragma unroll
     for (int q = 0; q < kChunks16; ++q) {
       const uint32_t off = swz_offset(m, c * kChunks16 + q, p.rowb_out);
@@ -274,6 +274,22 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
   }
 }
 
+#ifdef NEO_TRACE
+// debug builds only: CTA 0 logs (event, tile, globaltimer) records
+__device__ unsigned long long g_trace[1 << 16];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(int ev, int t) {
+  if (blockIdx.x != 0) return;
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  const unsigned int i = atomicAdd(&g_trace_n, 1u);
+  if (i < (1u << 16)) g_trace[i] = ((unsigned long long)ev << 56) | ((unsigned long long)(t & 0xFFFF) << 40) | (ns & 0xFFFFFFFFFFull);
+}
+#define TRACE(ev, t) trace(ev, t)
+#else
+#define TRACE(ev, t)
+#endif
+
 template <bool TF32>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -292,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   auto res_bar = [&](int g, int b) { return sBar + 160u + 16u * g + 8u * b; };
   const uint32_t tslot = sBar + 192u;
   volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 192);
+  float* par_gen = reinterpret_cast<float*>(bar_gen + 256);   // 2 groups x kParamFloats
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -361,7 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         // counters (no divisions on the single producer thread)
         int co = 0, sc = 0, rc = 0, sl = 0;
         for (int ks = 0; ks < p.kstages; ++ks) {
+          TRACE(1, t);
           mbar_wait(empty_bar(stage), phase ^ 1u);
+          TRACE(2, t);
           mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
           const uint32_t a_dst = sA + stage * p.a_stage;
           for (int g = 0; g < p.G; ++g, ++sl) {
@@ -407,11 +426,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
+        TRACE(10, t);
         mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+        TRACE(11, t);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.BN;
         for (int ks = 0; ks < p.kstages; ++ks) {
           mbar_wait(full_bar(stage), phase);
+          TRACE(12, t);
           tc_fence_after();
           const uint32_t a0 = sA + stage * p.a_stage;
           const uint32_t b0 = sB + stage * p.b_stage;
@@ -502,9 +524,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                           p.res_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
           }
         };
+        if (leader) TRACE(20 + grp, t);
         issue_res(0, min(nblk, p.nslot));
+        {
+          // stage this tile's channel vectors (identity where absent)
+          float* par = par_gen + grp * kParamFloats;
+          const int j = ((warp - 2) & 7) * 32 + lane;
+          const int k = k0 + j;
+          const bool in = j < p.BN && k < p.K;
+          par[j] = (in && p.scale) ? __ldg(p.scale + k) : 1.f;
+          par[256 + j] = (in && p.shift) ? __ldg(p.shift + k) : 0.f;
+          par[512 + j] = (in && p.bias) ? __ldg(p.bias + k) : 0.f;
+        }
+        if (leader) TRACE(22 + grp, t);
         named_bar_sync(bar_id, kEpiGroupThreads);
+        if (leader) TRACE(24 + grp, t);
         mbar_wait(tfull_bar(acc), acc_phase);
+        if (leader) TRACE(26 + grp, t);
         tc_fence_after();
         for (int b0 = 0; b0 < nblk; b0 += p.nslot) {
           const int cnt = min(p.nslot, nblk - b0);
@@ -516,22 +552,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             mbar_wait(res_bar(grp, 0), res_phase & 1u);
             res_phase ^= 1u;
           }
+          if (leader) TRACE(28 + grp, t);
           const float floor_v = p.relu ? 0.f : -INFINITY;
           const bool rnd = p.round_tf32 != 0;
           // the two warps of a lane quarter split the chunk's work: whole
           // blocks when there are several, 16-column pieces of one block else
           const int bstep = cnt >= 2 ? 2 : 1;
           const int cbeg = cnt >= 2 ? 0 : half, cstep = cnt >= 2 ? 1 : 2;
+          const float* par = par_gen + grp * kParamFloats;
           for (int i = (cnt >= 2 ? half : 0); i < cnt; i += bstep) {
             const uint32_t tcol = trow + (b0 + i) * p.y;
-            const int kb0 = k0 + (b0 + i) * p.y;
+            const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
             if (p.out_f32) {
-              if (has_res) epi_block_tma<true, true>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
-              else epi_block_tma<true, false>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
+              if (has_res) epi_block_tma<true, true>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
+              else epi_block_tma<true, false>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
             } else {
-              if (has_res) epi_block_tma<false, true>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
-              else epi_block_tma<false, false>(p, tcol, kb0, m, sg, floor_v, rnd, cbeg, cstep);
+              if (has_res) epi_block_tma<false, true>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
+              else epi_block_tma<false, false>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
             }
           }
           if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
@@ -539,8 +577,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(acc));
           }
+          if (leader) TRACE(30 + grp, t);
           fence_proxy_async_smem();
           named_bar_sync(bar_id, kEpiGroupThreads);
+          if (leader) TRACE(32 + grp, t);
           if (leader) {
             for (int i = 0; i < cnt; ++i)
               tma_store_5d(&p.tmO, sgrp + i * p.stage_out, 0, ow0, oh0,
@@ -782,7 +822,7 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   // and as many stages as fit, shrinking slices per stage if needed
   const int rb = epi_rowb_out(p, p->tile_n);
   const int64_t staging = rb ? 2ll * kTileM * rb * (p->tile_n / std::max(1, p->oc_bn)) : 0;
-  const int64_t budget = kSmemBudget - 2048;
+  const int64_t budget = kSmemBudget - 2048 - 2 * kParamFloats * 4;
   if (p->slices_per_stage <= 0 || p->stages <= 0) {
     int g = p->slices_per_stage > 0 ? p->slices_per_stage
                                     : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
@@ -957,7 +997,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   // TMA-store epilogue: output / residual tensor maps over (y, OW, OH, Kb_total, N)
   const int rb_out = epi_rowb_out(p, BN);
   {
-    const int64_t left = (int64_t)kSmemBudget - 2048 - (int64_t)p->stages * (kp.a_stage + kp.b_stage);
+    const int64_t left = (int64_t)kSmemBudget - 2048 - 2 * kParamFloats * 4 -
+                         (int64_t)p->stages * (kp.a_stage + kp.b_stage);
     const int64_t slots = rb_out ? left / (2ll * kTileM * rb_out) : 0;
     kp.nslot = (int)std::min<int64_t>(slots, BN / std::max(1, p->oc_bn));
   }
@@ -995,7 +1036,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   }
 
   const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) +
-                     2 * (size_t)kp.nslot * kp.stage_out + 256;
+                     2 * (size_t)kp.nslot * kp.stage_out + 256 + 2 * kParamFloats * 4;
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
   const int grid = (int)std::min<int64_t>(num_tiles, sm_count_of_current_device());
@@ -1021,3 +1062,16 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
+
+#ifdef NEO_TRACE
+extern "C" int neo_trace_dump(unsigned long long* host, int max_n) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
+  if (n > (unsigned)max_n) n = max_n;
+  if (n > (1u << 16)) n = 1u << 16;
+  cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
+  unsigned int zero = 0;
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+  return (int)n;
+}
+#endif

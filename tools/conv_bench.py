@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tile", default="", help="json dict of tile fields")
+    ap.add_argument("--flat", action="store_true", help="1x1 conv as a 1 x (H*W) image")
     args = ap.parse_args()
 
     import torch
@@ -52,8 +53,10 @@ def main():
     flops = 2 * n * k * c * r * r * oh * oh
     byts = (x.numel() + out.numel() * (2 if args.res else 1)) * x.element_size()
 
+    hh, ww = (1, hw * hw) if args.flat else (hw, hw)
+
     def run(tile):
-        p = D.conv_params(lmode, x, wd, out, n, c, hw, hw, k, r, r, (st, st), (pad, pad), args.x,
+        p = D.conv_params(lmode, x, wd, out, n, c, hh, ww, k, r, r, (st, st), (pad, pad), args.x,
                           args.y, bias=bias, residual=res, relu=True, tile=tile)
         cfg = D.default_tiles(p)
         for _ in range(3):
