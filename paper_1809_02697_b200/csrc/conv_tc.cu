@@ -163,11 +163,12 @@ __device__ __forceinline__ void epi_chunk(const ConvTCParams& p, const uint32_t 
     }
     return;
   }
-  // generic path: any y, partial chunk at the end of K
-#pragma unroll 1
+  // generic path: any y, partial chunk at the end of K (fully unrolled so
+  // f[] stays in registers)
+#pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = kbase + j;
-    if (k >= p.K) break;
+    if (k >= p.K) continue;
     const int kb = k / p.y, jj = k % p.y;
     float val = epi_apply(p, f[j], k);
     const size_t o = ea.out_base + (size_t)kb * ea.plane + jj;

@@ -38,6 +38,8 @@ def main():
     conv_bench.main()
     torch.cuda.synchronize()
     n = lib.neo_trace_dump(buf, 65536)
+    clk = [(buf[60000 + 2 * w], buf[60001 + 2 * w]) for w in range(16)]
+    print("epilogue warp cycles (tmem-ld+params, math+smem):", clk)
     recs = [(int(v >> 56), int((v >> 40) & 0xFFFF), int(v & 0xFFFFFFFFFF)) for v in buf[:n]]
     t0 = min(r[2] for r in recs)
     by = defaultdict(list)
@@ -55,6 +57,8 @@ def main():
     print(f"mma full-waits: {len(mma)} first {mma[0] / 1000:.2f}us last {mma[-1] / 1000:.2f}us")
     prod = sorted(v for (ev, t), vs in by.items() if ev == 2 for v in vs)
     print(f"producer stages: {len(prod)} first {prod[0] / 1000:.2f}us last {prod[-1] / 1000:.2f}us")
+    chunk = sorted((ns, ev) for ev, tile, ns in recs if 40 <= ev < 56)
+    print("chunk events (first 24):", [(ev, round((ns - t0) / 1000, 2)) for ns, ev in chunk[:24]])
     total = max(r[2] for r in recs) - t0
     print(f"CTA0 span {total / 1000:.2f} us, records {n}")
 
