@@ -152,12 +152,25 @@ int neo_conv_default_tiles(neo_conv_params* p);
  * (x = 1 is NCHW), replaces _pool2d executor.py:103-128. */
 int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb, int64_t h,
                int64_t w, int x, int win, int stride, int pad, int flags, neo_stream_t stream);
+/* Same with channel-block windows: the input is blocks [in_cb_off, +cb) of a
+ * (n, in_cb_total, h, w, x) buffer and the output blocks [out_cb_off, +cb) of
+ * a (n, out_cb_total, oh, ow, x) buffer (concat-in-place). */
+int neo_pool2d_window(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb,
+                      int64_t h, int64_t w, int x, int win, int stride, int pad,
+                      int64_t in_cb_off, int64_t in_cb_total, int64_t out_cb_off,
+                      int64_t out_cb_total, int flags, neo_stream_t stream);
 /* elementwise ops over (n, cb, hw, x) (x = 1 is NCHW); scale/shift indexed by
  * channel cb*x+lane.  Replaces executor.py:165-190 (ReLU, BatchNorm with
  * _channel_broadcast :96-100, ElementwiseAdd). */
 int neo_eltwise(int dtype, int op, const void* a, const void* b, void* out, const float* scale,
                 const float* shift, int64_t n, int64_t cb, int64_t hw, int x, int flags,
                 neo_stream_t stream);
+/* Same with channel-block windows on `a` and `out` (relu / scale-shift ops;
+ * add requires dense operands). */
+int neo_eltwise_window(int dtype, int op, const void* a, const void* b, void* out,
+                       const float* scale, const float* shift, int64_t n, int64_t cb, int64_t hw,
+                       int x, int64_t a_cb_off, int64_t a_cb_total, int64_t out_cb_off,
+                       int64_t out_cb_total, int flags, neo_stream_t stream);
 /* strided copy for np.concatenate (executor.py:191-193): src viewed as
  * (outer, chunk) elements is copied into dst viewed as (outer, dst_row) at
  * column dst_off.  Concat of k inputs = k calls. */

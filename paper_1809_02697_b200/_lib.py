@@ -86,6 +86,12 @@ SIGNATURES = {
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),
     "neo_pool2d": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
                             _c_int, _c_int, _c_int, _c_int, _c_int, _c_vp]),
+    "neo_pool2d_window": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
+                                   _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_i64,
+                                   _c_int, _c_vp]),
+    "neo_eltwise_window": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
+                                    _c_i64, _c_i64, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
+                                    _c_vp]),
     "neo_eltwise": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
                              _c_i64, _c_i64, _c_int, _c_int, _c_vp]),
     "neo_concat_copy": (_c_int, [_c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp]),

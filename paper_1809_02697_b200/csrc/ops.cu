@@ -9,6 +9,18 @@
 
 namespace {
 
+// channel-block windows: a tensor that is the [off, off + Cb) block range of
+// a (n, total, ...) buffer (concat-in-place destinations / sources)
+struct Win {
+  int64_t in_off, in_total, out_off, out_total;
+  __device__ __forceinline__ int64_t in_plane(int64_t plane, int64_t Cb) const {
+    return (plane / Cb) * in_total + in_off + plane % Cb;
+  }
+  __device__ __forceinline__ int64_t out_plane(int64_t plane, int64_t Cb) const {
+    return (plane / Cb) * out_total + out_off + plane % Cb;
+  }
+};
+
 int64_t grid_for(int64_t total, int threads = 256) {
   return std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, threads), 148 * 32));
 }
@@ -18,7 +30,7 @@ int64_t grid_for(int64_t total, int threads = 256) {
 template <typename T>
 __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t N, int64_t Cb,
                             int H, int W, int OH, int OW, int x, int win, int stride, int pad,
-                            bool is_max, bool round) {
+                            bool is_max, bool round, Win wnd) {
   const int64_t total = N * Cb * OH * OW * x;
   const float inv = (float)(win * win);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -30,7 +42,7 @@ __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64
     t /= OW;
     const int oh = (int)(t % OH);
     const int64_t plane = t / OH;  // n*Cb + cb
-    const T* src = in + plane * H * W * x + j;
+    const T* src = in + wnd.in_plane(plane, Cb) * H * W * x + j;
     float acc = is_max ? -INFINITY : 0.f;
     bool first = true;
     for (int r = 0; r < win; ++r) {
@@ -51,7 +63,7 @@ __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64
     }
     if (!is_max) acc = __fdiv_rn(acc, inv);
     if (round) acc = neo_round_tf32(acc);
-    out[i] = Elem<T>::from_f(acc);
+    out[((wnd.out_plane(plane, Cb) * OH + oh) * OW + ow) * x + j] = Elem<T>::from_f(acc);
   }
 }
 
@@ -59,7 +71,7 @@ __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64
 template <typename T, int V>
 __global__ void pool_kernel_vec(const T* __restrict__ in, T* __restrict__ out, int64_t N,
                                 int64_t Cb, int H, int W, int OH, int OW, int x, int win,
-                                int stride, int pad, bool is_max, bool round) {
+                                int stride, int pad, bool is_max, bool round, Win wnd) {
   const int groups = x / V;
   const int64_t total = N * Cb * OH * OW * groups;
   const float inv = (float)(win * win);
@@ -72,7 +84,7 @@ __global__ void pool_kernel_vec(const T* __restrict__ in, T* __restrict__ out, i
     t /= OW;
     const int oh = (int)(t % OH);
     const int64_t plane = t / OH;
-    const T* src = in + plane * H * W * x + gq * V;
+    const T* src = in + wnd.in_plane(plane, Cb) * H * W * x + gq * V;
     float acc[V];
     bool first = true;
     for (int r = 0; r < win; ++r) {
@@ -104,17 +116,21 @@ __global__ void pool_kernel_vec(const T* __restrict__ in, T* __restrict__ out, i
       if (round) a = neo_round_tf32(a);
       o[j] = Elem<T>::from_f(a);
     }
-    *reinterpret_cast<uint4*>(out + (((plane * OH + oh) * OW + ow) * x) + gq * V) = packed;
+    *reinterpret_cast<uint4*>(out + (((wnd.out_plane(plane, Cb) * OH + oh) * OW + ow) * x) +
+                              gq * V) = packed;
   }
 }
 
 template <typename T>
 __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
                                const float* __restrict__ scale, const float* __restrict__ shift,
-                               int64_t total, int64_t Cb, int64_t HW, int x, int op, bool round) {
+                               int64_t total, int64_t Cb, int64_t HW, int x, int op, bool round,
+                               Win wnd) {
+  const int64_t plane_sz = HW * x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float v = Elem<T>::to_f(a[i]);
+    const int64_t plane = i / plane_sz, inner = i % plane_sz;
+    float v = Elem<T>::to_f(a[wnd.in_plane(plane, Cb) * plane_sz + inner]);
     switch (op) {
       case NEO_ELT_RELU: v = fmaxf(v, 0.f); break;
       case NEO_ELT_ADD: v = __fadd_rn(v, Elem<T>::to_f(b[i])); break;
@@ -129,7 +145,7 @@ __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b,
       }
     }
     if (round) v = neo_round_tf32(v);
-    out[i] = Elem<T>::from_f(v);
+    out[wnd.out_plane(plane, Cb) * plane_sz + inner] = Elem<T>::from_f(v);
   }
 }
 
@@ -228,35 +244,81 @@ __global__ void softmax_kernel(const float* __restrict__ in, float* __restrict__
 
 }  // namespace
 
-extern "C" int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb,
-                          int64_t h, int64_t w, int x, int win, int stride, int pad, int flags,
-                          neo_stream_t stream) {
+extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out, int64_t n,
+                                 int64_t cb, int64_t h, int64_t w, int x, int win, int stride,
+                                 int pad, int64_t in_cb_off, int64_t in_cb_total,
+                                 int64_t out_cb_off, int64_t out_cb_total, int flags,
+                                 neo_stream_t stream) {
   NEO_CHECK_ARG(in && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
   NEO_CHECK_ARG(win >= 1 && stride >= 1 && pad >= 0 && x >= 1, NEO_ERR_INVALID_ARG,
                 "bad pool window/stride/pad");
+  NEO_CHECK_ARG(in_cb_off >= 0 && in_cb_off + cb <= in_cb_total && out_cb_off >= 0 &&
+                    out_cb_off + cb <= out_cb_total,
+                NEO_ERR_SHAPE_MISMATCH, "channel-block window out of range");
   const int64_t OH = (h + 2 * pad - win) / stride + 1, OW = (w + 2 * pad - win) / stride + 1;
   NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "pool has empty output");
   const int64_t total = n * cb * OH * OW * x;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  const Win wnd{in_cb_off, in_cb_total, out_cb_off, out_cb_total};
   if (dtype == NEO_BF16 && x % 8 == 0) {
     const int64_t tv = total / 8;
     pool_kernel_vec<__nv_bfloat16, 8><<<(unsigned)grid_for(tv), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
-        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   } else if (dtype == NEO_F32 && x % 4 == 0) {
     const int64_t tv = total / 4;
     pool_kernel_vec<float, 4><<<(unsigned)grid_for(tv), 256, 0, st>>>(
         static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
-        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   } else if (dtype == NEO_BF16)
     pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
-        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   else
     pool_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
         static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
-        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round);
+        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb,
+                          int64_t h, int64_t w, int x, int win, int stride, int pad, int flags,
+                          neo_stream_t stream) {
+  return neo_pool2d_window(dtype, mode, in, out, n, cb, h, w, x, win, stride, pad, 0, cb, 0, cb,
+                           flags, stream);
+}
+
+extern "C" int neo_eltwise_window(int dtype, int op, const void* a, const void* b, void* out,
+                                  const float* scale, const float* shift, int64_t n, int64_t cb,
+                                  int64_t hw, int x, int64_t a_cb_off, int64_t a_cb_total,
+                                  int64_t out_cb_off, int64_t out_cb_total, int flags,
+                                  neo_stream_t stream) {
+  NEO_CHECK_ARG(a && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(op >= 0 && op <= 4, NEO_ERR_INVALID_ARG, "bad eltwise op %d", op);
+  NEO_CHECK_ARG(!(op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) || b, NEO_ERR_INVALID_ARG,
+                "add needs two inputs");
+  NEO_CHECK_ARG(op < NEO_ELT_SCALE_SHIFT || (scale && shift), NEO_ERR_INVALID_ARG,
+                "scale/shift needs both vectors");
+  NEO_CHECK_ARG(!(op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) ||
+                    (a_cb_off == 0 && a_cb_total == cb && out_cb_off == 0 && out_cb_total == cb),
+                NEO_ERR_UNSUPPORTED, "windowed add is not supported");
+  NEO_CHECK_ARG(a_cb_off >= 0 && a_cb_off + cb <= a_cb_total && out_cb_off >= 0 &&
+                    out_cb_off + cb <= out_cb_total,
+                NEO_ERR_SHAPE_MISMATCH, "channel-block window out of range");
+  const int64_t total = n * cb * hw * x;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  const Win wnd{a_cb_off, a_cb_total, out_cb_off, out_cb_total};
+  if (dtype == NEO_BF16)
+    eltwise_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
+        static_cast<__nv_bfloat16*>(out), scale, shift, total, cb, hw, x, op, round, wnd);
+  else
+    eltwise_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+        static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out), scale,
+        shift, total, cb, hw, x, op, round, wnd);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
@@ -264,25 +326,8 @@ extern "C" int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_
 extern "C" int neo_eltwise(int dtype, int op, const void* a, const void* b, void* out,
                            const float* scale, const float* shift, int64_t n, int64_t cb,
                            int64_t hw, int x, int flags, neo_stream_t stream) {
-  NEO_CHECK_ARG(a && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
-  NEO_CHECK_ARG(op >= 0 && op <= 4, NEO_ERR_INVALID_ARG, "bad eltwise op %d", op);
-  NEO_CHECK_ARG(!(op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) || b, NEO_ERR_INVALID_ARG,
-                "add needs two inputs");
-  NEO_CHECK_ARG(op < NEO_ELT_SCALE_SHIFT || (scale && shift), NEO_ERR_INVALID_ARG,
-                "scale/shift needs both vectors");
-  const int64_t total = n * cb * hw * x;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
-  if (dtype == NEO_BF16)
-    eltwise_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
-        static_cast<__nv_bfloat16*>(out), scale, shift, total, cb, hw, x, op, round);
-  else
-    eltwise_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
-        static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out), scale,
-        shift, total, cb, hw, x, op, round);
-  NEO_LAUNCH_CHECK();
-  return NEO_OK;
+  return neo_eltwise_window(dtype, op, a, b, out, scale, shift, n, cb, hw, x, 0, cb, 0, cb, flags,
+                            stream);
 }
 
 extern "C" int neo_concat_copy(int dtype, const void* src, void* dst, int64_t outer, int64_t chunk,

@@ -132,6 +132,21 @@ def pool2d(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, flags=0, strea
            _ptr(inp), _ptr(out), n, cb, h, w, x, win, stride, pad, flags, stream_handle(stream))
 
 
+def pool2d_window(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, in_win, out_win,
+                  flags=0, stream=None):
+    """Pooling between channel-block windows ((offset, total) pairs)."""
+    L.call("neo_pool2d_window", dtype_code(inp), L.POOL_MAX if mode == "max" else L.POOL_AVG,
+           _ptr(inp), _ptr(out), n, cb, h, w, x, win, stride, pad, in_win[0], in_win[1],
+           out_win[0], out_win[1], flags, stream_handle(stream))
+
+
+def eltwise_window(op: int, a, out, n, cb, hw, x, a_win, out_win, scale=None, shift=None,
+                   flags=0, stream=None):
+    L.call("neo_eltwise_window", dtype_code(a), op, _ptr(a), None, _ptr(out), _ptr(scale),
+           _ptr(shift), n, cb, hw, x, a_win[0], a_win[1], out_win[0], out_win[1], flags,
+           stream_handle(stream))
+
+
 def eltwise(op: int, a, b, out, n, cb, hw, x, scale=None, shift=None, flags=0, stream=None):
     L.call("neo_eltwise", dtype_code(a), op, _ptr(a), _ptr(b), _ptr(out), _ptr(scale),
            _ptr(shift), n, cb, hw, x, flags, stream_handle(stream))

@@ -78,6 +78,7 @@ class _Val:
     layout: Layout        # logical layout
     px: int = 0           # physical block size of an NCHW[x]c value
     alias: int | None = None  # value whose storage this one views (Flatten)
+    win: tuple | None = None  # (root nid, block offset) inside a concat buffer
     first: int = 0
     last: int = 0
     offset: int = -1
@@ -221,6 +222,7 @@ class DeviceProgram:
                     and src.shape[2] == 1 and src.shape[3] == 1 and src.dtype == out.dtype
                     and src.px == src.layout.x and not node.attrs.get("pad_channels")):
                 out.alias = node.inputs[0][0]
+        self._plan_concat_windows()
         # lifetimes
         last_step = len(order)
         for nid, v in self.vals.items():
@@ -244,6 +246,87 @@ class DeviceProgram:
                 tgt.last = last_step
         for nid in self.plan.input_ids:
             self.vals[nid].first = -1
+        # a concat buffer lives as long as any of its windows
+        for v in self.vals.values():
+            if v.win is not None:
+                root = self.vals[v.win[0]]
+                root.first = min(root.first, v.first)
+                root.last = max(root.last, v.last)
+
+    # -- concat in place ---------------------------------------------------------
+    def _plan_concat_windows(self):
+        """Channel-axis concats of NCHW[x]c maps are done in place: every
+        eligible input is produced straight into its channel-block window of
+        the concat's buffer (conv epilogues, pools and scale-shift launches
+        all take a window), so the concat launch copies only the rest.
+        Nested concats (DenseNet's growing feature stack) compose: processing
+        in reverse order gives each inner concat its window in the outer
+        buffer first, and its own inputs then land in sub-windows of that."""
+        g = self.g
+        self.concat_windowed: dict[int, set] = {}
+        for nid in reversed(self.plan.order):
+            node = g.nodes[nid]
+            if node.kind != OpKind.Concat or nid not in self.vals:
+                continue
+            out = self.vals[nid]
+            if (node.attrs.get("axis", 1) != 1 or out.layout.tag != "NCHWc"
+                    or out.alias is not None or out.px != out.layout.x):
+                continue
+            root, base = out.win if out.win is not None else (nid, 0)
+            srcs = [src for src, _ in node.inputs]
+            done = set()
+            off = 0
+            for src in srcs:
+                v = self.vals.get(src)
+                if v is None:
+                    break
+                if srcs.count(src) == 1 and self._window_eligible(src, nid):
+                    v.win = (root, base + off)
+                    done.add(src)
+                off += v.shape[1]
+            self.concat_windowed[nid] = done
+
+    def _window_eligible(self, nid: int, concat: int) -> bool:
+        g = self.g
+        v, out = self.vals[nid], self.vals[concat]
+        node = g.nodes[nid]
+        if (v.alias is not None or v.win is not None or nid in g.outputs or nid in self.keep
+                or v.layout.tag != "NCHWc" or v.px != v.layout.x or v.px != out.px
+                or v.dtype != out.dtype or v.shape[0] != out.shape[0]
+                or v.shape[2:] != out.shape[2:] or nid in self.phys_x
+                or nid in self.stem_fold):
+            return False
+        if self.mode != "fp32" and not tc_legal_block(v.px, self.mode):
+            return False
+        kind = node.kind
+        if kind == OpKind.ReLU:
+            if nid in self.fused_dense_relu:
+                return False
+        elif kind not in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool, OpKind.Concat,
+                          OpKind.BatchNorm):
+            return False
+        if kind == OpKind.Conv2d and g.nodes[node.inputs[0][0]].kind == OpKind.Input:
+            return False
+        for u in self.users[nid]:
+            un = g.nodes[u]
+            if u == concat:
+                continue
+            pos = [i for i, (s, _) in enumerate(un.inputs) if s == nid]
+            if un.kind == OpKind.Conv2d:
+                if pos != [0]:
+                    return False
+            elif un.kind in (OpKind.MaxPool, OpKind.AvgPool, OpKind.ReLU, OpKind.BatchNorm):
+                if pos != [0] or u in self.fused_dense_relu:
+                    return False
+            else:
+                return False
+        return True
+
+    def _window(self, v: _Val) -> tuple:
+        """(block offset, blocks in the buffer) of a value's storage."""
+        if v.win is None:
+            return 0, v.shape[1]
+        return v.win[1], self.vals[v.win[0]].shape[1]
 
     def _stem_fold_info(self, nid) -> dict | None:
         """Fold parameters if ``nid`` packs a few-channel graph input that
@@ -348,7 +431,7 @@ class DeviceProgram:
     # -- memory ----------------------------------------------------------------
     def _allocate(self):
         import torch
-        owners = [v for v in self.vals.values() if v.alias is None]
+        owners = [v for v in self.vals.values() if v.alias is None and v.win is None]
         inputs = [v for v in owners if v.first < 0]
         arena_vals = [v for v in owners if v.first >= 0]
         size = _plan_arena(arena_vals)
@@ -359,6 +442,10 @@ class DeviceProgram:
             v.tensor = self.arena[v.offset:v.offset + nb].view(v.dtype).view(v.shape)
         for v in inputs:
             v.tensor = torch.empty(v.shape, dtype=v.dtype, device=self.device)
+        for v in self.vals.values():
+            if v.win is not None:
+                # kernels take the root buffer plus the (offset, total) window
+                v.tensor = self.vals[v.win[0]].tensor
         for v in self.vals.values():
             if v.alias is not None:
                 base = self._storage(v.nid)
@@ -488,7 +575,8 @@ class DeviceProgram:
             flags = self.round_flag | (L.FLAG_PAD_CHANNELS if pad_c else 0)
             p = D.conv_params(mode, x_t, wd, o_t, n, c, h, w, k, r, s, (sh, sw), (ph, pw),
                               ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t,
-                              bool(epi.get("relu")), flags=flags,
+                              bool(epi.get("relu")), x_cb=self._window(data),
+                              out_cb=self._window(out), flags=flags,
                               tile=tile if any(tile.values()) else None)
             self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream))
             return
@@ -509,6 +597,8 @@ class DeviceProgram:
             self.weights.append(o_t)
         p = D.conv_params(L.MODE_FP32, x_t, wdev, o_t, n, c, h, w, k, r, s, (sh, sw), (ph, pw),
                           ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t, bool(epi.get("relu")),
+                          x_cb=self._window(data) if x_t is data.tensor else (0, 0),
+                          out_cb=self._window(out) if o_t is out.tensor else (0, 0),
                           flags=self.round_flag)
         self._emit(f"conv{node.id}_simt", lambda p=p: D.conv2d(p, self.stream))
         if o_t is not out.tensor:
@@ -575,6 +665,11 @@ class DeviceProgram:
         win, st, pad = node.attrs["window"], node.attrs["stride"], node.attrs.get("pad", 0)
         flags = self.round_flag if src.layout.tag == "NCHWc" else 0
         s_t, d_t = src.tensor, out.tensor
+        if src.win is not None or out.win is not None:
+            iw, ow = self._window(src), self._window(out)
+            self._emit(f"{mode}pool{node.id}", lambda: D.pool2d_window(
+                s_t, d_t, n, cb, h, w, x, win, st, pad, mode, iw, ow, flags, self.stream))
+            return
         self._emit(f"{mode}pool{node.id}", lambda: D.pool2d(
             s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream))
 
@@ -583,6 +678,13 @@ class DeviceProgram:
         n, cb, h, w, x = self._geom(a)
         flags = self.round_flag if a.layout.tag == "NCHWc" else 0
         a_t, b_t, o_t = a.tensor, (b.tensor if b is not None else None), out.tensor
+        if b is None and (a.win is not None or out.win is not None):
+            aw, ow = self._window(a), self._window(out)
+            self._emit(f"eltwise{out.nid}", lambda: D.eltwise_window(
+                op, a_t, o_t, n, cb, h * w, x, aw, ow, None, None, flags, self.stream))
+            return
+        if (b is not None and b.win is not None) or a.win is not None or out.win is not None:
+            raise InputMismatch(f"eltwise {out.nid}: windowed add")
         self._emit(f"eltwise{out.nid}", lambda: D.eltwise(
             op, a_t, b_t, o_t, n, cb, h * w, x, None, None, flags, self.stream))
 
@@ -601,22 +703,37 @@ class DeviceProgram:
         op = L.ELT_SCALE_SHIFT_RELU if relu else L.ELT_SCALE_SHIFT
         flags = self.round_flag if src.layout.tag == "NCHWc" else 0
         a_t, o_t = src.tensor, out.tensor
+        if src.win is not None or out.win is not None:
+            aw, ow = self._window(src), self._window(out)
+            self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise_window(
+                op, a_t, o_t, n, cb, h * w, x, aw, ow, t_scale, t_shift, flags, self.stream))
+            return
         self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise(
             op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream))
 
     def _bind_concat(self, node, ins, out: _Val):
         from . import device as D
         axis = node.attrs.get("axis", 1)
-        outer = int(np.prod(out.shape[:axis]))
-        row = int(np.prod(out.shape[axis:]))
-        off = 0
-        for v in ins:
+        done = self.concat_windowed.get(node.id, set())
+        dst = out
+        base_blocks = 0
+        if out.win is not None:     # this concat is itself a window of a wider one
+            dst = self.vals[out.win[0]]
+            base_blocks = out.win[1]
+        outer = int(np.prod(dst.shape[:axis]))
+        row = int(np.prod(dst.shape[axis:]))
+        plane = int(np.prod(dst.shape[2:])) if axis == 1 else 0
+        off = base_blocks * plane
+        for (src, _), v in zip(node.inputs, ins):
             if v.tensor.dtype != out.tensor.dtype:
                 raise InputMismatch(f"concat {node.id}: mixed storage types")
             chunk = int(np.prod(v.shape[axis:]))
-            s_t, d_t = v.tensor, out.tensor
-            self._emit(f"concat{node.id}", lambda s_t=s_t, d_t=d_t, chunk=chunk, off=off:
-                       D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream))
+            if src not in done:
+                if v.win is not None:
+                    raise InputMismatch(f"concat {node.id}: input {src} is a foreign window")
+                s_t, d_t = v.tensor, dst.tensor
+                self._emit(f"concat{node.id}", lambda s_t=s_t, d_t=d_t, chunk=chunk, off=off:
+                           D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream))
             off += chunk
 
     def _bind_dense(self, node, src: _Val, out: _Val, relu: bool = False):

@@ -149,3 +149,34 @@ def test_pool_vs_reference(cuda):
             out4 = torch.empty((2, 2, oh, oh, 4), device="cuda")
             D.pool2d(src4, out4, 2, 2, 9, 9, 4, win, st, pd, mode)
             assert np.array_equal(out4.cpu().numpy(), d[f"{mode}_{win}_{st}_{pd}_b4"])
+
+
+def test_pool_and_eltwise_windows(cuda):
+    """Pool / scale-shift-relu between channel-block windows of wider
+    buffers (concat in place) equal the dense launches bit for bit."""
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    a = load("pool.npz")["a"]
+    for dt, x in ((torch.float32, 4), (torch.float32, 1), (torch.bfloat16, 8)):
+        src = torch.from_numpy(oracle.pack_nchw(np.concatenate([a] * 2, 1), x)).cuda().to(dt)
+        cb = src.shape[1]
+        wide_in = torch.randn((2, cb + 3) + src.shape[2:], device="cuda").to(dt)
+        wide_in[:, 2:2 + cb] = src
+        for mode in ("max", "avg"):
+            ref = torch.empty((2, cb, 5, 5, x), device="cuda", dtype=dt)
+            D.pool2d(src, ref, 2, cb, 9, 9, x, 3, 2, 1, mode)
+            wide_out = torch.zeros((2, cb + 5, 5, 5, x), device="cuda", dtype=dt)
+            D.pool2d_window(wide_in, wide_out, 2, cb, 9, 9, x, 3, 2, 1, mode, (2, cb + 3),
+                            (4, cb + 5))
+            assert torch.equal(wide_out[:, 4:4 + cb], ref)
+            assert not wide_out[:, :4].any() and not wide_out[:, 4 + cb:].any()
+        scale = torch.randn(cb * x, device="cuda")
+        shift = torch.randn(cb * x, device="cuda")
+        ref = torch.empty_like(src)
+        D.eltwise(L.ELT_SCALE_SHIFT_RELU, src, None, ref, 2, cb, 81, x, scale, shift)
+        wide_out = torch.zeros((2, cb + 1, 9, 9, x), device="cuda", dtype=dt)
+        D.eltwise_window(L.ELT_SCALE_SHIFT_RELU, wide_in, wide_out, 2, cb, 81, x, (2, cb + 3),
+                         (1, cb + 1), scale, shift)
+        assert torch.equal(wide_out[:, 1:], ref)
+        assert not wide_out[:, :1].any()
