@@ -67,60 +67,6 @@ __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64
   }
 }
 
-// vector variant: V consecutive lanes of x per thread (16-byte loads/stores)
-template <typename T, int V>
-__global__ void pool_kernel_vec(const T* __restrict__ in, T* __restrict__ out, int64_t N,
-                                int64_t Cb, int H, int W, int OH, int OW, int x, int win,
-                                int stride, int pad, bool is_max, bool round, Win wnd) {
-  const int groups = x / V;
-  const int64_t total = N * Cb * OH * OW * groups;
-  const float inv = (float)(win * win);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int gq = (int)(t % groups);
-    t /= groups;
-    const int ow = (int)(t % OW);
-    t /= OW;
-    const int oh = (int)(t % OH);
-    const int64_t plane = t / OH;
-    const T* src = in + wnd.in_plane(plane, Cb) * H * W * x + gq * V;
-    float acc[V];
-    bool first = true;
-    for (int r = 0; r < win; ++r) {
-      const int ih = oh * stride + r - pad;
-      for (int s = 0; s < win; ++s) {
-        const int iw = ow * stride + s - pad;
-        const bool inb = ih >= 0 && ih < H && iw >= 0 && iw < W;
-        float v[V];
-        if (inb) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(src + ((int64_t)ih * W + iw) * x);
-          const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-          for (int j = 0; j < V; ++j) v[j] = Elem<T>::to_f(e[j]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < V; ++j) v[j] = is_max ? -INFINITY : 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          acc[j] = first ? v[j] : (is_max ? fmaxf(acc[j], v[j]) : __fadd_rn(acc[j], v[j]));
-        first = false;
-      }
-    }
-    uint4 packed;
-    T* o = reinterpret_cast<T*>(&packed);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      float a = is_max ? acc[j] : __fdiv_rn(acc[j], inv);
-      if (round) a = neo_round_tf32(a);
-      o[j] = Elem<T>::from_f(a);
-    }
-    *reinterpret_cast<uint4*>(out + (((wnd.out_plane(plane, Cb) * OH + oh) * OW + ow) * x) +
-                              gq * V) = packed;
-  }
-}
-
 template <typename T>
 __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
                                const float* __restrict__ scale, const float* __restrict__ shift,
@@ -148,6 +94,132 @@ __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b,
     out[wnd.out_plane(plane, Cb) * plane_sz + inner] = Elem<T>::from_f(v);
   }
 }
+
+// Plane-major vector kernels: blockIdx.y walks the (n, cb) planes (window
+// mapping once per plane), blockIdx.x the V-lane vectors inside a plane with
+// 32-bit index math, 16-byte loads and stores.
+inline __device__ void unpack_vec(const uint4& raw, float* v, const float*) {
+  const float* e = reinterpret_cast<const float*>(&raw);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = e[j];
+}
+inline __device__ void unpack_vec(const uint4& raw, float* v, const __nv_bfloat16*) {
+  const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(e[j]);
+}
+template <typename T, int V>
+__device__ __forceinline__ uint4 pack_vec(const float* v) {
+  uint4 raw;
+  T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+  for (int j = 0; j < V; ++j) e[j] = Elem<T>::from_f(v[j]);
+  return raw;
+}
+
+template <typename T, int V>
+__global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, int64_t Cb,
+                               int64_t P, int H, int W, int OH, int OW, int x, int win,
+                               int stride, int pad, bool is_max, bool round, Win wnd) {
+  const uint32_t groups = x / V;
+  const uint32_t per_plane = (uint32_t)OH * OW * groups;
+  const float inv = (float)(win * win);
+  for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
+    const T* src = in + wnd.in_plane(plane, Cb) * H * W * x;
+    T* dst = out + wnd.out_plane(plane, Cb) * OH * OW * x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_plane;
+         i += gridDim.x * blockDim.x) {
+      const uint32_t gq = i % groups, t = i / groups;
+      const int ow = (int)(t % (uint32_t)OW), oh = (int)(t / (uint32_t)OW);
+      float acc[V];
+      bool first = true;
+      for (int r = 0; r < win; ++r) {
+        const int ih = oh * stride + r - pad;
+        for (int s = 0; s < win; ++s) {
+          const int iw = ow * stride + s - pad;
+          float v[V];
+          if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+            unpack_vec(__ldg(reinterpret_cast<const uint4*>(src + (ih * W + iw) * x + gq * V)), v,
+                       (const T*)nullptr);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) v[j] = is_max ? -INFINITY : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j)
+            acc[j] = first ? v[j] : (is_max ? fmaxf(acc[j], v[j]) : __fadd_rn(acc[j], v[j]));
+          first = false;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (!is_max) acc[j] = __fdiv_rn(acc[j], inv);
+        if (round) acc[j] = neo_round_tf32(acc[j]);
+      }
+      *reinterpret_cast<uint4*>(dst + (oh * OW + ow) * x + gq * V) = pack_vec<T, V>(acc);
+    }
+  }
+}
+
+template <typename T, int V>
+__global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__ b,
+                                  T* __restrict__ out, const float* __restrict__ scale,
+                                  const float* __restrict__ shift, int64_t Cb, int64_t P,
+                                  int64_t plane_sz, int x, int op, bool round, Win wnd) {
+  const uint32_t vecs = (uint32_t)(plane_sz / V);
+  for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
+    const T* ap = a + wnd.in_plane(plane, Cb) * plane_sz;
+    const T* bp = b ? b + plane * plane_sz : nullptr;
+    T* op_ = out + wnd.out_plane(plane, Cb) * plane_sz;
+    const int ch_base = (int)(plane % Cb) * x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < vecs;
+         i += gridDim.x * blockDim.x) {
+      float v[V];
+      unpack_vec(__ldg(reinterpret_cast<const uint4*>(ap) + i), v, (const T*)nullptr);
+      if (op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) {
+        float w[V];
+        unpack_vec(__ldg(reinterpret_cast<const uint4*>(bp) + i), w, (const T*)nullptr);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          v[j] = __fadd_rn(v[j], w[j]);
+          if (op == NEO_ELT_ADD_RELU) v[j] = fmaxf(v[j], 0.f);
+        }
+      } else if (op == NEO_ELT_RELU) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) v[j] = fmaxf(v[j], 0.f);
+      } else {
+        const int ch = ch_base + (int)((i * V) % (uint32_t)x);
+        float sc[V], sh[V];
+#pragma unroll
+        for (int j = 0; j < V; j += 4) {
+          const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + ch + j));
+          const float4 h4 = __ldg(reinterpret_cast<const float4*>(shift + ch + j));
+          sc[j] = s4.x; sc[j + 1] = s4.y; sc[j + 2] = s4.z; sc[j + 3] = s4.w;
+          sh[j] = h4.x; sh[j + 1] = h4.y; sh[j + 2] = h4.z; sh[j + 3] = h4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          // executor.py:180-181: a * scale + shift as two rounded numpy ops
+          v[j] = __fadd_rn(__fmul_rn(v[j], sc[j]), sh[j]);
+          if (op == NEO_ELT_SCALE_SHIFT_RELU) v[j] = fmaxf(v[j], 0.f);
+        }
+      }
+      if (round) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) v[j] = neo_round_tf32(v[j]);
+      }
+      reinterpret_cast<uint4*>(op_)[i] = pack_vec<T, V>(v);
+    }
+  }
+}
+
+dim3 plane_grid(int64_t planes, int64_t per_plane, int threads = 256) {
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(per_plane, threads), 1024));
+  const int64_t by = std::max<int64_t>(1, std::min<int64_t>(planes, 65535));
+  return dim3((unsigned)bx, (unsigned)by);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename T>
 __global__ void concat_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t outer,
@@ -261,15 +333,15 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
   const Win wnd{in_cb_off, in_cb_total, out_cb_off, out_cb_total};
-  if (dtype == NEO_BF16 && x % 8 == 0) {
-    const int64_t tv = total / 8;
-    pool_kernel_vec<__nv_bfloat16, 8><<<(unsigned)grid_for(tv), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
+  const int64_t P = n * cb;
+  const bool al = aligned16(in) && aligned16(out);
+  if (dtype == NEO_BF16 && x % 8 == 0 && al) {
+    pool_plane_vec<__nv_bfloat16, 8><<<plane_grid(P, OH * OW * (x / 8)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), cb, P, (int)h,
         (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
-  } else if (dtype == NEO_F32 && x % 4 == 0) {
-    const int64_t tv = total / 4;
-    pool_kernel_vec<float, 4><<<(unsigned)grid_for(tv), 256, 0, st>>>(
-        static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
+  } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
+    pool_plane_vec<float, 4><<<plane_grid(P, OH * OW * (x / 4)), 256, 0, st>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), cb, P, (int)h, (int)w, (int)OH,
         (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   } else if (dtype == NEO_BF16)
     pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
@@ -311,7 +383,18 @@ extern "C" int neo_eltwise_window(int dtype, int op, const void* a, const void* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
   const Win wnd{a_cb_off, a_cb_total, out_cb_off, out_cb_total};
-  if (dtype == NEO_BF16)
+  const int64_t P = n * cb, plane_sz = hw * x;
+  const bool al = aligned16(a) && aligned16(out) && (!b || aligned16(b)) &&
+                  (op < NEO_ELT_SCALE_SHIFT || (aligned16(scale) && aligned16(shift)));
+  if (dtype == NEO_BF16 && x % 8 == 0 && al) {
+    eltwise_plane_vec<__nv_bfloat16, 8><<<plane_grid(P, plane_sz / 8), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
+        static_cast<__nv_bfloat16*>(out), scale, shift, cb, P, plane_sz, x, op, round, wnd);
+  } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
+    eltwise_plane_vec<float, 4><<<plane_grid(P, plane_sz / 4), 256, 0, st>>>(
+        static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out),
+        scale, shift, cb, P, plane_sz, x, op, round, wnd);
+  } else if (dtype == NEO_BF16)
     eltwise_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
         static_cast<__nv_bfloat16*>(out), scale, shift, total, cb, hw, x, op, round, wnd);
