@@ -780,8 +780,12 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
   const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
   NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "conv has empty output");
-  if (p->tile_w <= 0 || p->tile_h <= 0 || p->tile_img <= 0) {
+  const bool auto_geom = p->tile_w <= 0 || p->tile_h <= 0 || p->tile_img <= 0;
+  const bool auto_tn = p->tile_n <= 0;
+  Geometry g0{0, 0, 0};
+  if (auto_geom) {
     Geometry g = pick_geometry(p->n, OH, OW);
+    g0 = g;
     p->tile_w = g.BW;
     p->tile_h = g.BH;
     p->tile_img = g.BNI;
@@ -801,9 +805,14 @@ int neo_conv_default_tiles(neo_conv_params* p) {
       }
     }
   }
-  const bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
-  const int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
-                          neo_ceil_div(p->n, p->tile_img);
+  bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
+  int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
+                    neo_ceil_div(p->n, p->tile_img);
+  const int64_t budget = kSmemBudget - 2048 - 2 * kParamFloats * 4;
+  auto staging_of = [&](int tn) -> int64_t {
+    const int rbo = epi_rowb_out(p, tn);
+    return rbo ? 2ll * kTileM * rbo * (tn / std::max(1, p->oc_bn)) : 0;
+  };
   if (p->tile_n <= 0) {
     // widest N tile that still gives every SM at least one tile (halo
     // stages carry S weight slices, so their N tile stops at 128)
@@ -816,14 +825,37 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     }
     if (p->tile_n > widest) p->tile_n = widest;
   }
+  if (halo) {
+    // a halo stage carries S weight slices: two stages must fit beside the
+    // epilogue staging (wide kernels such as 1x7 shrink the N tile first,
+    // then fall back to plain tiles)
+    auto fits = [&]() {
+      return 2 * halo_pair_bytes(p, rowb) + staging_of(p->tile_n) <= budget;
+    };
+    while (!fits() && auto_tn && p->tile_n > 32) p->tile_n /= 2;
+    if (!fits() && auto_geom) {
+      p->tile_w = g0.BW;
+      p->tile_h = g0.BH;
+      p->tile_img = g0.BNI;
+      halo = false;
+      m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
+                neo_ceil_div(p->n, p->tile_img);
+      if (auto_tn) {
+        p->tile_n = pick_tile_n(p->k);
+        for (int bn : {256, 128, 64}) {
+          if (bn > pick_tile_n(p->k)) continue;
+          p->tile_n = bn;
+          if (m_tiles * neo_ceil_div(p->k, bn) >= sm_count_of_current_device()) break;
+        }
+      }
+    }
+  }
   const int64_t nslices = halo ? p->r * neo_ceil_div(p->c, p->ic_bn)
                                : p->r * p->s * neo_ceil_div(p->c, p->ic_bn);
   // pipeline: keep the full epilogue staging (every output block of a tile
   // in smem, so residual loads are issued before the accumulator is ready)
   // and as many stages as fit, shrinking slices per stage if needed
-  const int rb = epi_rowb_out(p, p->tile_n);
-  const int64_t staging = rb ? 2ll * kTileM * rb * (p->tile_n / std::max(1, p->oc_bn)) : 0;
-  const int64_t budget = kSmemBudget - 2048 - 2 * kParamFloats * 4;
+  const int64_t staging = staging_of(p->tile_n);
   if (p->slices_per_stage <= 0 || p->stages <= 0) {
     int g = p->slices_per_stage > 0 ? p->slices_per_stage
                                     : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));

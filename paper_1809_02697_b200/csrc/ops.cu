@@ -4,6 +4,7 @@
 // consecutive threads take consecutive lanes / pixels and every access is
 // coalesced; fp32 arithmetic follows the reference's numpy op order.
 #include <cfloat>
+#include <type_traits>
 
 #include "neo_common.cuh"
 
@@ -117,10 +118,39 @@ __device__ __forceinline__ uint4 pack_vec(const float* v) {
   return raw;
 }
 
-template <typename T, int V>
+dim3 plane_grid(int64_t planes, int64_t per_plane, int threads = 256) {
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(per_plane, threads), 1024));
+  const int64_t by = std::max<int64_t>(1, std::min<int64_t>(planes, 65535));
+  return dim3((unsigned)bx, (unsigned)by);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// 16-byte vector of V lanes as V/2 f32 pairs (sm_100 packed f32x2 adds)
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> {
+  static __device__ __forceinline__ float2 get(const uint4& r, int k) {
+    return reinterpret_cast<const float2*>(&r)[k];
+  }
+};
+template <>
+struct Pair<__nv_bfloat16> {
+  static __device__ __forceinline__ float2 get(const uint4& r, int k) {
+    return __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&r)[k]);
+  }
+};
+
+// _pool2d (executor.py:103-128).  Avg: padding taps add zero (skipped) and
+// the sum runs r-major then divides by win*win, lane pairs in packed f32x2
+// adds; max: padding is -inf (skipped), bf16 max is exact in bf16x2.
+template <typename T, int V, bool IS_MAX, int WIN>
 __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, int64_t Cb,
-                               int64_t P, int H, int W, int OH, int OW, int x, int win,
-                               int stride, int pad, bool is_max, bool round, Win wnd) {
+                               int64_t P, int H, int W, int OH, int OW, int x, int win_rt,
+                               int stride, int pad, bool round, Win wnd) {
+  constexpr int NP = V / 2;
+  const int win = WIN > 0 ? WIN : win_rt;
   const uint32_t groups = x / V;
   const uint32_t per_plane = (uint32_t)OH * OW * groups;
   const float inv = (float)(win * win);
@@ -131,34 +161,134 @@ __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, in
          i += gridDim.x * blockDim.x) {
       const uint32_t gq = i % groups, t = i / groups;
       const int ow = (int)(t % (uint32_t)OW), oh = (int)(t / (uint32_t)OW);
-      float acc[V];
-      bool first = true;
-      for (int r = 0; r < win; ++r) {
-        const int ih = oh * stride + r - pad;
-        for (int s = 0; s < win; ++s) {
-          const int iw = ow * stride + s - pad;
-          float v[V];
-          if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
-            unpack_vec(__ldg(reinterpret_cast<const uint4*>(src + (ih * W + iw) * x + gq * V)), v,
-                       (const T*)nullptr);
-          } else {
+      const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+      const T* base = src + gq * V;
+      uint4 res;
+      if constexpr (IS_MAX && sizeof(T) == 2) {
+        __nv_bfloat162 m[NP];
 #pragma unroll
-            for (int j = 0; j < V; ++j) v[j] = is_max ? -INFINITY : 0.f;
+        for (int k = 0; k < NP; ++k) m[k] = __bfloat162bfloat162(__float2bfloat16(-INFINITY));
+#pragma unroll
+        for (int r = 0; r < (WIN > 0 ? WIN : 1); ++r) {
+          for (int rr = r; rr < (WIN > 0 ? r + 1 : win); ++rr) {
+            const int ih = ih0 + rr;
+            if (ih < 0 || ih >= H) continue;
+#pragma unroll
+            for (int s_ = 0; s_ < (WIN > 0 ? WIN : 1); ++s_) {
+              for (int ss = s_; ss < (WIN > 0 ? s_ + 1 : win); ++ss) {
+                const int iw = iw0 + ss;
+                if (iw < 0 || iw >= W) continue;
+                const uint4 raw = __ldg(reinterpret_cast<const uint4*>(base + (ih * W + iw) * x));
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+                  m[k] = __hmax2(m[k], reinterpret_cast<const __nv_bfloat162*>(&raw)[k]);
+              }
+            }
           }
-#pragma unroll
-          for (int j = 0; j < V; ++j)
-            acc[j] = first ? v[j] : (is_max ? fmaxf(acc[j], v[j]) : __fadd_rn(acc[j], v[j]));
-          first = false;
         }
-      }
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        if (!is_max) acc[j] = __fdiv_rn(acc[j], inv);
-        if (round) acc[j] = neo_round_tf32(acc[j]);
+        for (int k = 0; k < NP; ++k) reinterpret_cast<__nv_bfloat162*>(&res)[k] = m[k];
+      } else {
+        float2 acc[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) acc[k] = IS_MAX ? make_float2(-INFINITY, -INFINITY)
+                                                     : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < (WIN > 0 ? WIN : 1); ++r) {
+          for (int rr = r; rr < (WIN > 0 ? r + 1 : win); ++rr) {
+            const int ih = ih0 + rr;
+            if (ih < 0 || ih >= H) continue;
+#pragma unroll
+            for (int s_ = 0; s_ < (WIN > 0 ? WIN : 1); ++s_) {
+              for (int ss = s_; ss < (WIN > 0 ? s_ + 1 : win); ++ss) {
+                const int iw = iw0 + ss;
+                if (iw < 0 || iw >= W) continue;
+                const uint4 raw = __ldg(reinterpret_cast<const uint4*>(base + (ih * W + iw) * x));
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                  const float2 v = Pair<T>::get(raw, k);
+                  if (IS_MAX)
+                    acc[k] = make_float2(fmaxf(acc[k].x, v.x), fmaxf(acc[k].y, v.y));
+                  else
+                    acc[k] = __fadd2_rn(acc[k], v);
+                }
+              }
+            }
+          }
+        }
+        float o[V];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          o[2 * k] = IS_MAX ? acc[k].x : __fdiv_rn(acc[k].x, inv);
+          o[2 * k + 1] = IS_MAX ? acc[k].y : __fdiv_rn(acc[k].y, inv);
+        }
+        if (round) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) o[j] = neo_round_tf32(o[j]);
+        }
+        res = pack_vec<T, V>(o);
       }
-      *reinterpret_cast<uint4*>(dst + (oh * OW + ow) * x + gq * V) = pack_vec<T, V>(acc);
+      *reinterpret_cast<uint4*>(dst + (oh * OW + ow) * x + gq * V) = res;
     }
   }
+}
+
+// Global pooling (window == H == W, no padding, 1x1 output: the classifier
+// head): one thread per lane pair, taps summed r-major in order like the
+// reference, loads issued 8 at a time for memory-level parallelism.
+template <typename T, bool IS_MAX>
+__global__ void pool_global(const T* __restrict__ in, T* __restrict__ out, int64_t Cb,
+                            int64_t P, int HW, int x, float inv, bool round, Win wnd) {
+  using T2 = typename std::conditional<sizeof(T) == 2, __nv_bfloat162, float2>::type;
+  const int pairs = x / 2;
+  const int64_t total = P * pairs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t plane = i / pairs;
+    const int lp = (int)(i % pairs);
+    const T2* src = reinterpret_cast<const T2*>(in + wnd.in_plane(plane, Cb) * HW * x) + lp;
+    float2 acc = IS_MAX ? make_float2(-INFINITY, -INFINITY) : make_float2(0.f, 0.f);
+    int t = 0;
+    for (; t + 8 <= HW; t += 8) {
+      T2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (t + u) * pairs);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float2 f;
+        if constexpr (sizeof(T) == 2) f = __bfloat1622float2(v[u]);
+        else f = v[u];
+        acc = IS_MAX ? make_float2(fmaxf(acc.x, f.x), fmaxf(acc.y, f.y)) : __fadd2_rn(acc, f);
+      }
+    }
+    for (; t < HW; ++t) {
+      float2 f;
+      if constexpr (sizeof(T) == 2) f = __bfloat1622float2(__ldg(src + t * pairs));
+      else f = __ldg(src + t * pairs);
+      acc = IS_MAX ? make_float2(fmaxf(acc.x, f.x), fmaxf(acc.y, f.y)) : __fadd2_rn(acc, f);
+    }
+    if (!IS_MAX) acc = make_float2(__fdiv_rn(acc.x, inv), __fdiv_rn(acc.y, inv));
+    if (round) acc = make_float2(neo_round_tf32(acc.x), neo_round_tf32(acc.y));
+    T2 o;
+    if constexpr (sizeof(T) == 2) o = __float22bfloat162_rn(acc);
+    else o = acc;
+    reinterpret_cast<T2*>(out + wnd.out_plane(plane, Cb) * x)[lp] = o;
+  }
+}
+
+template <typename T, int V, bool IS_MAX>
+void launch_pool_vec(const T* in, T* out, int64_t cb, int64_t P, int h, int w, int OH, int OW,
+                     int x, int win, int stride, int pad, bool round, Win wnd, cudaStream_t st) {
+  const dim3 grid = plane_grid(P, (int64_t)OH * OW * (x / V));
+  if (win == 3)
+    pool_plane_vec<T, V, IS_MAX, 3><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+                                                          stride, pad, round, wnd);
+  else if (win == 2)
+    pool_plane_vec<T, V, IS_MAX, 2><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+                                                          stride, pad, round, wnd);
+  else
+    pool_plane_vec<T, V, IS_MAX, 0><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+                                                          stride, pad, round, wnd);
 }
 
 template <typename T, int V>
@@ -212,14 +342,6 @@ __global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__
     }
   }
 }
-
-dim3 plane_grid(int64_t planes, int64_t per_plane, int threads = 256) {
-  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(per_plane, threads), 1024));
-  const int64_t by = std::max<int64_t>(1, std::min<int64_t>(planes, 65535));
-  return dim3((unsigned)bx, (unsigned)by);
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename T>
 __global__ void concat_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t outer,
@@ -335,14 +457,48 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
   const Win wnd{in_cb_off, in_cb_total, out_cb_off, out_cb_total};
   const int64_t P = n * cb;
   const bool al = aligned16(in) && aligned16(out);
-  if (dtype == NEO_BF16 && x % 8 == 0 && al) {
-    pool_plane_vec<__nv_bfloat16, 8><<<plane_grid(P, OH * OW * (x / 8)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), cb, P, (int)h,
-        (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
+  const bool is_max = mode == NEO_POOL_MAX;
+  const bool global = OH == 1 && OW == 1 && pad == 0 && win == h && win == w && x % 2 == 0;
+  if (global) {
+    const float inv = (float)(win * win);
+    const unsigned grid = (unsigned)grid_for(P * (x / 2));
+    if (dtype == NEO_BF16) {
+      auto i = static_cast<const __nv_bfloat16*>(in);
+      auto o = static_cast<__nv_bfloat16*>(out);
+      if (is_max)
+        pool_global<__nv_bfloat16, true><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv,
+                                                               round, wnd);
+      else
+        pool_global<__nv_bfloat16, false><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x,
+                                                                inv, round, wnd);
+    } else {
+      auto i = static_cast<const float*>(in);
+      auto o = static_cast<float*>(out);
+      if (is_max)
+        pool_global<float, true><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv, round,
+                                                       wnd);
+      else
+        pool_global<float, false><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv, round,
+                                                        wnd);
+    }
+  } else if (dtype == NEO_BF16 && x % 8 == 0 && al) {
+    auto i = static_cast<const __nv_bfloat16*>(in);
+    auto o = static_cast<__nv_bfloat16*>(out);
+    if (is_max)
+      launch_pool_vec<__nv_bfloat16, 8, true>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x,
+                                              win, stride, pad, round, wnd, st);
+    else
+      launch_pool_vec<__nv_bfloat16, 8, false>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x,
+                                               win, stride, pad, round, wnd, st);
   } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
-    pool_plane_vec<float, 4><<<plane_grid(P, OH * OW * (x / 4)), 256, 0, st>>>(
-        static_cast<const float*>(in), static_cast<float*>(out), cb, P, (int)h, (int)w, (int)OH,
-        (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
+    auto i = static_cast<const float*>(in);
+    auto o = static_cast<float*>(out);
+    if (is_max)
+      launch_pool_vec<float, 4, true>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x, win,
+                                      stride, pad, round, wnd, st);
+    else
+      launch_pool_vec<float, 4, false>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x, win,
+                                       stride, pad, round, wnd, st);
   } else if (dtype == NEO_BF16)
     pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,

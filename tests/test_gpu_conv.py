@@ -256,3 +256,17 @@ def test_tc_conv_halo_mode(cuda, case, mode_name):
     tile = dict(tile_w=ow + s - 1, tile_h=bh, tile_img=1)
     got = run_conv(mode, x, wt, (st, st), pd, x_bn, 32, residual=res, relu=True, tile=tile)
     assert oracle.rel_err(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("rs,pd", [((1, 7), (0, 3)), ((7, 1), (3, 0))])
+def test_tc_conv_default_tiles_wide_kernels(cuda, rs, pd):
+    """Kernel-picked tiles for Inception's 1x7 / 7x1 convs at 64-lane blocks
+    (the halo stage of a 7-tap 1x7 must shrink its N tile to fit)."""
+    from paper_1809_02697_b200 import _lib as L
+    r, s = rs
+    rng = np.random.default_rng(7)
+    x = bf16_round(rng.standard_normal((4, 128, 17, 17)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((192, 128, r, s)) * 0.05).astype(np.float32))
+    ref = oracle.conv2d(x, wt, (1, 1), pd, relu=True)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), pd, 64, 64, relu=True)
+    assert oracle.rel_err(got, ref) < 1e-4
