@@ -141,11 +141,24 @@ typedef struct neo_conv_params {
    * <= 256) the N tile; slices_per_stage (r, s, channel-block) slices per
    * pipeline stage; stages = pipeline depth (<= 8). */
   int tile_w, tile_h, tile_img, tile_n, slices_per_stage, stages;
+  /* split-K: the reduction is cut into split_k ranges run by separate CTAs
+   * (0 = automatic: only when the output tiles leave most SMs idle; 1 = off).
+   * Partials go to `workspace` (size from neo_conv_workspace_bytes; it must be
+   * zero-filled before its first use and every launch leaves it zeroed) and
+   * the last CTA of each output tile sums them in split order and applies
+   * the epilogue.  Without a large enough workspace an automatic split is
+   * dropped. */
+  int split_k;
+  void* workspace;
+  int64_t workspace_bytes;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);
 /* fill the automatic tile fields of *p the way neo_conv2d_nchwc_fused would */
 int neo_conv_default_tiles(neo_conv_params* p);
+/* Split-K workspace bytes the launch of *p needs with its resolved tiles
+ * (0 when it will not split). */
+int neo_conv_workspace_bytes(const neo_conv_params* p, int64_t* bytes);
 
 /* ---- memory-bound operators (executor.py:96-203) ------------------------ */
 /* Max (pad -inf) / avg (pad 0, / win^2) pooling over h, w of NCHW[x]c

@@ -63,6 +63,7 @@ class ConvParams(ctypes.Structure):
         ("flags", _c_int),
         ("tile_w", _c_int), ("tile_h", _c_int), ("tile_img", _c_int), ("tile_n", _c_int),
         ("slices_per_stage", _c_int), ("stages", _c_int),
+        ("split_k", _c_int), ("workspace", _c_vp), ("workspace_bytes", _c_i64),
     ]
 
 
@@ -84,6 +85,7 @@ SIGNATURES = {
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
     "neo_conv2d_nchwc_fused": (_c_int, [ctypes.POINTER(ConvParams), _c_vp]),
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),
+    "neo_conv_workspace_bytes": (_c_int, [ctypes.POINTER(ConvParams), ctypes.POINTER(_c_i64)]),
     "neo_pool2d": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
                             _c_int, _c_int, _c_int, _c_int, _c_int, _c_vp]),
     "neo_pool2d_window": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,

@@ -33,9 +33,14 @@ namespace {
 
 constexpr int kMaxStages = 8;
 constexpr int kThreads = 576;   // warp 0 TMA, warp 1 MMA, warps 2-17 epilogue (2 groups of 8)
-constexpr int kEpiGroupThreads = 256;
+constexpr int kEpiWarps = 16;          // warps 2..17
+constexpr int kMaxGroups = 4;          // epilogue groups = TMEM accumulator stages
 constexpr int kTileM = 128;
+#ifdef NEO_TRACE
+constexpr int kSmemBudget = 226 * 1024;   // trace builds keep a little static smem
+#else
 constexpr int kSmemBudget = 227 * 1024;
+#endif
 
 struct ConvTCParams {
   CUtensorMap tmA;  // 5-D: (x, W, H, Cb, N)
@@ -52,6 +57,9 @@ struct ConvTCParams {
   int swz;       // UMMA layout code for rowb
   int stages;
   uint32_t a_sub, b_sub, a_stage, b_stage, tx_bytes, tmem_cols;
+  // epilogue groups (2 or 4): group g drains TMEM accumulator stage g; each
+  // group has kEpiWarps / ngroups warps covering the 4 TMEM lane quarters
+  int ngroups;
   const float* scale;
   const float* shift;
   const float* bias;
@@ -71,6 +79,13 @@ struct ConvTCParams {
   int halo;
   int R;
   int halo_baseoff;   // set the UMMA matrix base offset for shifted views
+  // split-K: work unit u = (tile u / splits, split u % splits) covers k-stages
+  // [split * kps, min(kstages, (split + 1) * kps)); with splits > 1 every
+  // unit stores its raw fp32 accumulator to ws[u][chunk16][row][16] and,
+  // after all splits of the tile arrived, reduces and finishes 1/splits of it.
+  int splits, kps, num_units;
+  float* ws;        // partials
+  int* counters;    // per-tile arrival counters (zero between launches)
 };
 
 __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n0, int& oh0,
@@ -275,18 +290,76 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
   }
 }
 
+// Split-K fixup of one unit's share: (chunk16, row) pairs
+// [sp*share, (sp+1)*share) of tile t, each summed over the splits in order
+// and finished by the direct epilogue.  Kept out of line so the main
+// kernel's register allocation is not shaped by this cold path.
+__device__ __noinline__ void splitk_fixup(const ConvTCParams& p, int t, int sp, int n0, int oh0,
+                                          int ow0, int k0, int gtid, int gthreads) {
+  const int nch = p.BN / 16;
+  const int pairs = nch * kTileM;
+  const int share = (pairs + p.splits - 1) / p.splits;
+  const int pend = min(pairs, (sp + 1) * share);
+  const float4* tile_ws = reinterpret_cast<const float4*>(p.ws) +
+                          (size_t)t * p.splits * nch * kTileM * 4;
+  const size_t sstride = (size_t)nch * kTileM * 4;
+  const size_t plane = (size_t)p.OH * p.OW * p.y;
+  for (int pi = sp * share + gtid; pi < pend; pi += gthreads) {
+    const int c = pi / kTileM, mr = pi % kTileM;
+    const int kb0 = k0 + c * 16;
+    const int wl = mr % p.BW, hl = (mr / p.BW) % p.BH, nl = mr / (p.BW * p.BH);
+    const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
+    if (kb0 >= p.K || mr >= p.BW * p.BH * p.BNI || ow >= p.OW || oh >= p.OH || n >= p.N) continue;
+    const float4* src = tile_ws + ((size_t)c * kTileM + mr) * 4;
+    float f[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 a = __ldcg(src + j);
+      f[4 * j] = a.x;
+      f[4 * j + 1] = a.y;
+      f[4 * j + 2] = a.z;
+      f[4 * j + 3] = a.w;
+    }
+    for (int s2 = 1; s2 < p.splits; ++s2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 a = __ldcg(src + s2 * sstride + j);
+        f[4 * j] += a.x;
+        f[4 * j + 1] += a.y;
+        f[4 * j + 2] += a.z;
+        f[4 * j + 3] += a.w;
+      }
+    }
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(f[j]);
+    EpiAccess ea;
+    ea.plane = plane;
+    const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
+    ea.out_base = (size_t)n * p.out_cb_total * plane + (size_t)p.out_cb_off * plane + pix;
+    ea.res_base = (size_t)n * p.res_cb_total * plane + (size_t)p.res_cb_off * plane + pix;
+    epi_chunk(p, v, kb0, ea);
+  }
+}
+
 #ifdef NEO_TRACE
-// debug builds only: CTA 0 logs (event, tile, globaltimer) records
-__device__ unsigned long long g_trace[1 << 16];
-__device__ unsigned int g_trace_n;
-__device__ __forceinline__ void trace(int ev, int t) {
+// debug builds only: CTA 0 logs (event, tile, globaltimer) records, one
+// region per warp indexed by a shared-memory counter (no global atomics on
+// the traced path); counts are published at kernel exit
+constexpr int kTraceWarps = 18, kTracePerWarp = 2048;
+__device__ unsigned long long g_trace[kTraceWarps * kTracePerWarp];
+__device__ unsigned int g_trace_cnt[kTraceWarps];
+__device__ __forceinline__ void trace(int ev, int t, unsigned* cnt) {
   if (blockIdx.x != 0) return;
   unsigned long long ns;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-  const unsigned int i = atomicAdd(&g_trace_n, 1u);
-  if (i < (1u << 16)) g_trace[i] = ((unsigned long long)ev << 56) | ((unsigned long long)(t & 0xFFFF) << 40) | (ns & 0xFFFFFFFFFFull);
+  const int w = threadIdx.x >> 5;
+  const unsigned int i = atomicAdd_block(cnt + w, 1u);
+  if (i < (unsigned)kTracePerWarp)
+    g_trace[w * kTracePerWarp + i] = ((unsigned long long)ev << 56) |
+                                     ((unsigned long long)(t & 0xFFFF) << 40) | (ns & 0xFFFFFFFFFFull);
 }
-#define TRACE(ev, t) trace(ev, t)
+#define TRACE(ev, t) trace(ev, t, s_trace_cnt)
 #else
 #define TRACE(ev, t)
 #endif
@@ -299,20 +372,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t sA = sraw + pad;
   const uint32_t sB = sA + p.stages * p.a_stage;
   const uint32_t sO = sB + p.stages * p.b_stage;                // 2 groups x nslot staging slots
-  const uint32_t sBar = sO + 2 * p.nslot * p.stage_out;
+  const uint32_t sBar = sO + p.ngroups * p.nslot * p.stage_out;
   uint8_t* gen_base = smem_raw + pad;
   uint8_t* bar_gen = gen_base + (sBar - sA);
   auto full_bar = [&](int i) { return sBar + 8u * i; };
   auto empty_bar = [&](int i) { return sBar + 64u + 8u * i; };
   auto tfull_bar = [&](int a) { return sBar + 128u + 8u * a; };
-  auto tempty_bar = [&](int a) { return sBar + 144u + 8u * a; };
-  auto res_bar = [&](int g, int b) { return sBar + 160u + 16u * g + 8u * b; };
-  const uint32_t tslot = sBar + 192u;
-  volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 192);
-  float* par_gen = reinterpret_cast<float*>(bar_gen + 256);   // 2 groups x kParamFloats
+  auto tempty_bar = [&](int a) { return sBar + 160u + 8u * a; };
+  auto res_bar = [&](int g, int b) { return sBar + 192u + 16u * g + 8u * b; };
+  const uint32_t tslot = sBar + 256u;
+  volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 256);
+  float* par_gen = reinterpret_cast<float*>(bar_gen + 512);   // ngroups x kParamFloats
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+#ifdef NEO_TRACE
+  __shared__ unsigned s_trace_cnt[32];
+  if (threadIdx.x < 32) s_trace_cnt[threadIdx.x] = 0;
+  __syncthreads();
+#endif
+  if (threadIdx.x == 0) TRACE(60, 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmA);
@@ -325,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       mbar_init(full_bar(i), 1);
       mbar_init(empty_bar(i), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < p.ngroups; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 8);
+      mbar_init(tempty_bar(a), kEpiWarps / p.ngroups);
       mbar_init(res_bar(a, 0), 1);
       mbar_init(res_bar(a, 1), 1);
     }
@@ -341,19 +420,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tslot_gen;
+  if (threadIdx.x == 0) TRACE(61, 0);
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const int t = u / p.splits;
+        const int ks0 = (u - t * p.splits) * p.kps;
+        const int ks1 = min(p.kstages, ks0 + p.kps);
         int n0, oh0, ow0, k0;
         decode_tile(p, t, n0, oh0, ow0, k0);
         const int iw0 = ow0 * p.stride_w - p.pad_w;
         const int ih0 = oh0 * p.stride_h - p.pad_h;
         if (p.halo) {
-          for (int ks = 0; ks < p.kstages; ++ks) {
+          for (int ks = ks0; ks < ks1; ++ks) {
             mbar_wait(empty_bar(stage), phase ^ 1u);
             mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
             const uint32_t a_dst = sA + stage * p.a_stage;
@@ -377,8 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         // slice = (r, s, channel block), channel block fastest; walked with
         // counters (no divisions on the single producer thread)
-        int co = 0, sc = 0, rc = 0, sl = 0;
-        for (int ks = 0; ks < p.kstages; ++ks) {
+        int sl = ks0 * p.G;
+        int co = sl % p.Cb, sc = (sl / p.Cb) % p.S, rc = sl / (p.Cb * p.S);
+        for (int ks = ks0; ks < ks1; ++ks) {
           TRACE(1, t);
           mbar_wait(empty_bar(stage), phase ^ 1u);
           TRACE(2, t);
@@ -424,15 +508,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+        const int t = u / p.splits;
+        const int ks0 = (u - t * p.splits) * p.kps;
+        const int ks1 = min(p.kstages, ks0 + p.kps);
+        const int acc = it % p.ngroups;
+        const uint32_t acc_phase = (it / p.ngroups) & 1;
         TRACE(10, t);
         mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
         TRACE(11, t);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.BN;
-        for (int ks = 0; ks < p.kstages; ++ks) {
+        for (int ks = ks0; ks < ks1; ++ks) {
           mbar_wait(full_bar(stage), phase);
           TRACE(12, t);
           tc_fence_after();
@@ -450,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 for (int kk = 0; kk < 4; ++kk) {
                   const uint64_t ad = umma_smem_desc(a_s + 32u * kk, 16, 1024, 2, bo);
                   const uint64_t bd = umma_smem_desc(b_s + 32u * kk, 16, 1024, 2);
-                  umma_ss<TF32>(d_tmem, ad, bd, idesc, (ks | g | s | kk) != 0);
+                  umma_ss<TF32>(d_tmem, ad, bd, idesc, ((ks - ks0) | g | s | kk) != 0);
                 }
               }
             }
@@ -475,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               boff = sub * p.b_sub + inrow;
             }
             umma_ss<TF32>(d_tmem, ad_stage + (aoff >> 4), bd_stage + (boff >> 4), idesc,
-                          (ks | k) != 0);
+                          ((ks - ks0) | k) != 0);
           }
           umma_commit(empty_bar(stage));
           if (++stage == p.stages) {
@@ -484,28 +571,77 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
         }
         umma_commit(tfull_bar(acc));
+        TRACE(13, t);
       }
     }
   } else {
     // ---------------- epilogue: two groups of 4 warps, group g takes the
     // tiles whose accumulator lives in TMEM stage g (alternate tiles), so
     // both groups drain in parallel with the MMA of the next tile.
-    const int grp = (warp - 2) >> 3;
-    const int half = ((warp - 2) >> 2) & 1;  // which channel blocks of a tile
+    const int gwarps = kEpiWarps / p.ngroups;      // 8 or 4
+    const int gthreads = gwarps * 32;
+    const int grp = (warp - 2) / gwarps;
+    const int nsub = gwarps / 4;                    // warps per lane quarter: 2 or 1
+    const int half = ((warp - 2) >> 2) % nsub;      // which channel blocks of a tile
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int m = q * 32 + lane;            // accumulator row = tile pixel
-    const bool leader = (warp == 2 + 8 * grp) && lane == 0;
+    const bool leader = (warp == 2 + gwarps * grp) && lane == 0;
     const uint32_t bar_id = 1 + grp;
     const size_t plane = (size_t)p.OH * p.OW * p.y;
     uint32_t res_phase = 0u;                // phase of this group's residual barrier
     int it = grp;
-    for (int t = blockIdx.x + grp * gridDim.x; t < p.num_tiles; t += 2 * gridDim.x, it += 2) {
+    for (int u = blockIdx.x + grp * gridDim.x; u < p.num_units;
+         u += p.ngroups * gridDim.x, it += p.ngroups) {
+      const int t = u / p.splits;
       int n0, oh0, ow0, k0;
       decode_tile(p, t, n0, oh0, ow0, k0);
       const int acc = grp;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const uint32_t acc_phase = (it / p.ngroups) & 1;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.BN;
       const int ncols = min(p.BN, p.K - k0);
+      if (p.splits > 1) {
+        // split-K: every unit of a tile stores its raw accumulator to
+        // ws[u][chunk16][row][16] and releases TMEM; once all splits of the
+        // tile arrived (per-tile counter; the host keeps every unit of a split
+        // launch co-resident), each unit reduces its 1/splits share of the
+        // tile's (chunk, row) pairs in split order -- deterministic -- and runs
+        // the direct epilogue on it.
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+        const int nch = p.BN / 16;
+        float4* dst = reinterpret_cast<float4*>(p.ws) + ((size_t)u * nch * kTileM + m) * 4;
+        for (int c = half; c < nch; c += nsub) {
+          uint32_t v[16];
+          tmem_ld16(trow + c * 16, v);
+          tmem_ld_wait();
+          float4* d = dst + (size_t)c * kTileM * 4;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcg(d + j, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                      __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(acc));
+        __threadfence();
+        named_bar_sync(bar_id, gthreads);
+        if (leader) {
+          TRACE(40, t);
+          atomicAdd(p.counters + t, 1);
+          spin_until_geq(p.counters + t, p.splits);
+          TRACE(41, t);
+        }
+        named_bar_sync(bar_id, gthreads);
+        __threadfence();
+        splitk_fixup(p, t, u - t * p.splits, n0, oh0, ow0, k0, ((warp - 2) % gwarps) * 32 + lane,
+                     gthreads);
+        // second arrival: the unit arriving last (every unit is past its
+        // wait) re-zeroes the counter for the next launch
+        named_bar_sync(bar_id, gthreads);
+        if (leader) TRACE(42, t);
+        if (leader && atomicAdd(p.counters + t, 1) == 2 * p.splits - 1) p.counters[t] = 0;
+        continue;
+      }
       if (p.tma_epi) {
         // staged epilogue: the tile's output channel blocks go through up to
         // p.nslot swizzled smem slots; residual blocks are fetched by TMA
@@ -530,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         {
           // stage this tile's channel vectors (identity where absent)
           float* par = par_gen + grp * kParamFloats;
-          const int j = ((warp - 2) & 7) * 32 + lane;
+          const int j = ((warp - 2) % gwarps) * 32 + lane;
           const int k = k0 + j;
           const bool in = j < p.BN && k < p.K;
           par[j] = (in && p.scale) ? __ldg(p.scale + k) : 1.f;
@@ -538,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           par[512 + j] = (in && p.bias) ? __ldg(p.bias + k) : 0.f;
         }
         if (leader) TRACE(22 + grp, t);
-        named_bar_sync(bar_id, kEpiGroupThreads);
+        named_bar_sync(bar_id, gthreads);
         if (leader) TRACE(24 + grp, t);
         mbar_wait(tfull_bar(acc), acc_phase);
         if (leader) TRACE(26 + grp, t);
@@ -547,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           const int cnt = min(p.nslot, nblk - b0);
           if (b0 > 0) {
             issue_res(b0, cnt);
-            named_bar_sync(bar_id, kEpiGroupThreads);
+            named_bar_sync(bar_id, gthreads);
           }
           if (has_res) {
             mbar_wait(res_bar(grp, 0), res_phase & 1u);
@@ -558,10 +694,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           const bool rnd = p.round_tf32 != 0;
           // the two warps of a lane quarter split the chunk's work: whole
           // blocks when there are several, 16-column pieces of one block else
-          const int bstep = cnt >= 2 ? 2 : 1;
-          const int cbeg = cnt >= 2 ? 0 : half, cstep = cnt >= 2 ? 1 : 2;
+          const bool by_block = nsub == 1 || cnt >= 2;
+          const int bstep = nsub == 1 ? 1 : (cnt >= 2 ? 2 : 1);
+          const int cbeg = by_block ? 0 : half, cstep = by_block ? 1 : 2;
           const float* par = par_gen + grp * kParamFloats;
-          for (int i = (cnt >= 2 ? half : 0); i < cnt; i += bstep) {
+          for (int i = (nsub == 2 && cnt >= 2 ? half : 0); i < cnt; i += bstep) {
             const uint32_t tcol = trow + (b0 + i) * p.y;
             const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
@@ -580,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
           if (leader) TRACE(30 + grp, t);
           fence_proxy_async_smem();
-          named_bar_sync(bar_id, kEpiGroupThreads);
+          named_bar_sync(bar_id, gthreads);
           if (leader) TRACE(32 + grp, t);
           if (leader) {
             for (int i = 0; i < cnt; ++i)
@@ -601,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
         ea.out_base = (size_t)n * p.out_cb_total * plane + (size_t)p.out_cb_off * plane + pix;
         ea.res_base = (size_t)n * p.res_cb_total * plane + (size_t)p.res_cb_off * plane + pix;
-        for (int c0 = 16 * half; c0 < ncols; c0 += 32) {
+        for (int c0 = 16 * half; c0 < ncols; c0 += 16 * nsub) {
           uint32_t v[16];
           tmem_ld16(trow + c0, v);
           tmem_ld_wait();
@@ -613,9 +750,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty_bar(acc));
     }
     if (leader) bulk_wait_all();
+    if (leader) TRACE(64, 0);
   }
 
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(62, 0);
+#ifdef NEO_TRACE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < kTraceWarps)
+    g_trace_cnt[threadIdx.x] = min(s_trace_cnt[threadIdx.x], (unsigned)kTracePerWarp);
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -746,6 +890,17 @@ int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
   return r * s * neo_ceil_div(c, x);
 }
 
+// epilogue groups = TMEM accumulator stages: four for short reductions
+// (<= 8 slices: the tile time is the epilogue's, and four tiles draining in
+// parallel hide its latency) when four N tiles fit the 512 TMEM columns,
+// else two (long K loops want the shared memory for pipeline stages)
+static int epi_groups(const neo_conv_params* p, int tile_n) {
+  static const int forced = getenv("NEOB200_EPI_GROUPS") ? atoi(getenv("NEOB200_EPI_GROUPS")) : 0;
+  if (forced == 2 || (forced == 4 && tile_n <= 128)) return forced;
+  const int64_t slices = p->r * p->s * neo_ceil_div(p->c, std::max(1, p->ic_bn));
+  return tile_n <= 128 && slices <= 8 ? 4 : 2;
+}
+
 // Row bytes of one output channel block for the TMA-store epilogue, or 0 when
 // the direct-store path must run: the block must be a 32/64/128-byte row of
 // whole 16-column chunks and every N tile must hold whole channel blocks.
@@ -808,15 +963,19 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
   int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
                     neo_ceil_div(p->n, p->tile_img);
-  const int64_t budget = kSmemBudget - 2048 - 2 * kParamFloats * 4;
+  const int64_t budget = kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4;
   auto staging_of = [&](int tn) -> int64_t {
     const int rbo = epi_rowb_out(p, tn);
-    return rbo ? 2ll * kTileM * rbo * (tn / std::max(1, p->oc_bn)) : 0;
+    return rbo ? (int64_t)epi_groups(p, tn) * kTileM * rbo * (tn / std::max(1, p->oc_bn)) : 0;
   };
   if (p->tile_n <= 0) {
     // widest N tile that still gives every SM at least one tile (halo
     // stages carry S weight slices, so their N tile stops at 128)
-    const int widest = halo ? std::min(128, pick_tile_n(p->k)) : pick_tile_n(p->k);
+    // short reductions are epilogue-bound: cap at 128 so four epilogue
+    // groups (TMEM stages) can drain tiles in parallel
+    const int64_t red_slices = p->r * p->s * neo_ceil_div(p->c, std::max(1, p->ic_bn));
+    const int widest = (halo || red_slices <= 8) ? std::min(128, pick_tile_n(p->k))
+                                                 : pick_tile_n(p->k);
     p->tile_n = widest;
     for (int bn : {256, 128, 64}) {
       if (bn > widest) continue;
@@ -856,6 +1015,16 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   // in smem, so residual loads are issued before the accumulator is ready)
   // and as many stages as fit, shrinking slices per stage if needed
   const int64_t staging = staging_of(p->tile_n);
+  // split-K when the (M, N) tiles leave most SMs idle: single-slice stages
+  // give the splits fine granularity
+  const int sms = sm_count_of_current_device();
+  const int64_t base_units = m_tiles * neo_ceil_div(p->k, p->tile_n);
+  // automatic split-K is opt-in (NEOB200_AUTO_SPLITK): measured on B200 the
+  // partial-sum exchange still costs more than the idle SMs it recovers for
+  // most under-filled layers, so split_k is a tuner / caller choice
+  static const bool auto_split = getenv("NEOB200_AUTO_SPLITK") != nullptr;
+  const bool underfilled = p->split_k <= 0 && base_units * 2 <= sms && auto_split;
+  if (underfilled && p->slices_per_stage <= 0) p->slices_per_stage = rowb == 16 ? 2 : 1;
   if (p->slices_per_stage <= 0 || p->stages <= 0) {
     int g = p->slices_per_stage > 0 ? p->slices_per_stage
                                     : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
@@ -877,6 +1046,63 @@ int neo_conv_default_tiles(neo_conv_params* p) {
       g = std::max(gmin, g / 2);
     }
   }
+  if (p->split_k <= 0) {
+    int64_t split = 1;
+    if (underfilled) {
+      const int64_t kst = neo_ceil_div(nslices, p->slices_per_stage);
+      split = std::min<int64_t>({sms / std::max<int64_t>(1, base_units), kst / 4, 32});
+      if (split < 2) split = 1;
+    }
+    p->split_k = (int)split;
+  }
+  return NEO_OK;
+}
+
+namespace {
+struct SplitPlan {
+  int splits, kps;
+  int64_t ws_bytes;
+};
+SplitPlan split_plan(const neo_conv_params* p, int64_t kstages, int64_t num_tiles) {
+  SplitPlan sp{1, (int)kstages, 0};
+  const int64_t want = std::max(1, std::min<int>(p->split_k, (int)kstages));
+  // every unit of a split launch must be resident at once (units wait for
+  // their tile's other splits): at most one unit per SM
+  const int64_t cap = std::max<int64_t>(1, sm_count_of_current_device() / std::max<int64_t>(1, num_tiles));
+  const int64_t want_c = std::min<int64_t>(want, cap);
+  if (want_c > 1) {
+    sp.kps = (int)neo_ceil_div(kstages, want_c);
+    sp.splits = (int)neo_ceil_div(kstages, sp.kps);
+    sp.ws_bytes = sp.splits > 1 ? neo_ceil_div(num_tiles * 4, 256) * 256 +
+                                      num_tiles * sp.splits * (int64_t)p->tile_n * kTileM * 4
+                                : 0;
+  }
+  return sp;
+}
+int64_t conv_kstages(const neo_conv_params* p, bool halo) {
+  const int64_t Cb = neo_ceil_div(p->c, p->ic_bn);
+  const int64_t nslices = halo ? p->r * Cb : p->r * p->s * Cb;
+  return neo_ceil_div(nslices, p->slices_per_stage);
+}
+int64_t conv_num_tiles(const neo_conv_params* p) {
+  const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
+  const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
+  return neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
+         neo_ceil_div(p->n, p->tile_img) * neo_ceil_div(p->k, p->tile_n);
+}
+}  // namespace
+
+// bytes of split-K workspace the launch of *p needs (0: no split)
+int neo_conv_workspace_bytes(const neo_conv_params* pin, int64_t* bytes) {
+  NEO_CHECK_ARG(pin != nullptr && bytes != nullptr, NEO_ERR_INVALID_ARG, "null argument");
+  *bytes = 0;
+  if (pin->mode == NEO_MODE_FP32) return NEO_OK;
+  neo_conv_params pc = *pin;
+  const int st = neo_conv_default_tiles(&pc);
+  if (st != NEO_OK) return st;
+  const int64_t OW = conv_out_dim(pc.w_in, pc.s, pc.stride_w, pc.pad_w);
+  const bool halo = pc.tile_w > OW;
+  *bytes = split_plan(&pc, conv_kstages(&pc, halo), conv_num_tiles(&pc)).ws_bytes;
   return NEO_OK;
 }
 
@@ -980,6 +1206,23 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const int64_t num_tiles = (int64_t)kp.tiles_w * kp.tiles_h * tiles_n * kp.tiles_k;
   NEO_CHECK_ARG(num_tiles < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many tiles");
   kp.num_tiles = (int)num_tiles;
+  {
+    SplitPlan sp = split_plan(p, kstages, num_tiles);
+    if (sp.splits > 1 && (p->workspace == nullptr || p->workspace_bytes < sp.ws_bytes)) {
+      NEO_CHECK_ARG(pin->split_k <= 1, NEO_ERR_INVALID_ARG,
+                    "split_k=%d needs a %lld-byte workspace", pin->split_k,
+                    (long long)sp.ws_bytes);
+      sp = SplitPlan{1, (int)kstages, 0};   // automatic split without workspace: none
+    }
+    kp.splits = sp.splits;
+    kp.kps = sp.kps;
+    kp.counters = static_cast<int*>(p->workspace);
+    kp.ws = sp.splits > 1 ? reinterpret_cast<float*>(static_cast<char*>(p->workspace) +
+                                                     neo_ceil_div(num_tiles * 4, 256) * 256)
+                          : nullptr;
+    NEO_CHECK_ARG(num_tiles * sp.splits < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many units");
+    kp.num_units = (int)(num_tiles * sp.splits);
+  }
   kp.G = G;
   kp.kstages = (int)kstages;
   kp.Cb = (int)Cb;
@@ -1009,8 +1252,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   }
   kp.a_stage = kp.a_sub * G;
   kp.b_stage = kp.b_sub * G;
+  kp.ngroups = epi_groups(p, BN);
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * BN)) cols <<= 1;
+  while (cols < (uint32_t)(kp.ngroups * BN)) cols <<= 1;
   kp.tmem_cols = cols;
   kp.scale = p->scale;
   kp.shift = p->shift;
@@ -1030,9 +1274,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   // TMA-store epilogue: output / residual tensor maps over (y, OW, OH, Kb_total, N)
   const int rb_out = epi_rowb_out(p, BN);
   {
-    const int64_t left = (int64_t)kSmemBudget - 2048 - 2 * kParamFloats * 4 -
+    const int64_t left = (int64_t)kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4 -
                          (int64_t)p->stages * (kp.a_stage + kp.b_stage);
-    const int64_t slots = rb_out ? left / (2ll * kTileM * rb_out) : 0;
+    const int64_t slots = rb_out ? left / ((int64_t)kp.ngroups * kTileM * rb_out) : 0;
     kp.nslot = (int)std::min<int64_t>(slots, BN / std::max(1, p->oc_bn));
   }
   kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
@@ -1069,10 +1313,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   }
 
   const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) +
-                     2 * (size_t)kp.nslot * kp.stage_out + 256 + 2 * kParamFloats * 4;
+                     (size_t)kp.ngroups * kp.nslot * kp.stage_out + 512 +
+                     (size_t)kp.ngroups * kParamFloats * 4;
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
-  const int grid = (int)std::min<int64_t>(num_tiles, sm_count_of_current_device());
+  const int grid = (int)std::min<int64_t>(kp.num_units, sm_count_of_current_device());
   // opt in to the large dynamic shared memory once per (device, kernel); the
   // attribute call is kept out of later launches so they can be graph-captured
   static bool attr_set[64][2] = {};
@@ -1097,14 +1342,20 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
 }
 
 #ifdef NEO_TRACE
+// records of the last traced launch (CTA 0), all warps concatenated
 extern "C" int neo_trace_dump(unsigned long long* host, int max_n) {
-  unsigned int n = 0;
-  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
-  if (n > (unsigned)max_n) n = max_n;
-  if (n > (1u << 16)) n = 1u << 16;
-  cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
-  unsigned int zero = 0;
-  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
-  return (int)n;
+  unsigned int cnt[kTraceWarps];
+  cudaMemcpyFromSymbol(cnt, g_trace_cnt, sizeof(cnt));
+  int n = 0;
+  for (int w = 0; w < kTraceWarps; ++w) {
+    const int take = std::min<int>((int)cnt[w], max_n - n);
+    if (take <= 0) continue;
+    cudaMemcpyFromSymbol(host + n, g_trace, take * sizeof(unsigned long long),
+                         (size_t)w * kTracePerWarp * sizeof(unsigned long long));
+    n += take;
+  }
+  unsigned int zero[kTraceWarps] = {};
+  cudaMemcpyToSymbol(g_trace_cnt, zero, sizeof(zero));
+  return n;
 }
 #endif

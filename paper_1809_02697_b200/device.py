@@ -111,9 +111,22 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
     p.out_dtype = dtype_code(out)
     p.flags = flags
     if tile:
-        for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages"):
+        for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
+                    "split_k"):
             setattr(p, key, int(tile.get(key, 0) or 0))
     return p
+
+
+def conv_workspace_bytes(p: L.ConvParams) -> int:
+    """Split-K workspace the launch of ``p`` needs (0 = no split)."""
+    out = ctypes.c_int64(0)
+    L.call("neo_conv_workspace_bytes", ctypes.byref(p), ctypes.byref(out))
+    return int(out.value)
+
+
+def set_workspace(p: L.ConvParams, ws) -> None:
+    p.workspace = _ptr(ws) if ws is not None else None
+    p.workspace_bytes = ws.numel() * ws.element_size() if ws is not None else 0
 
 
 def conv2d(p: L.ConvParams, stream=None) -> None:
@@ -124,7 +137,7 @@ def default_tiles(p: L.ConvParams) -> dict:
     q = L.ConvParams.from_buffer_copy(p)
     L.check(L.load().neo_conv_default_tiles(ctypes.byref(q)), "neo_conv_default_tiles")
     return {k: getattr(q, k) for k in ("tile_w", "tile_h", "tile_img", "tile_n",
-                                        "slices_per_stage", "stages")}
+                                        "slices_per_stage", "stages", "split_k")}
 
 
 def pool2d(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, flags=0, stream=None):

@@ -125,6 +125,7 @@ class DeviceProgram:
         self.act_dtype = torch.bfloat16 if mode == "bf16" else torch.float32
         self.round_flag = L.FLAG_ROUND_TF32 if mode == "tf32" else 0
         self.launches: list = []        # zero-arg callables, in order
+        self.tc_params: list = []       # tensor-core conv params (split-K workspace)
         self.launch_names: list[str] = []
         self.vals: dict[int, _Val] = {}
         self.weights: list = []         # device tensors kept alive
@@ -505,12 +506,26 @@ class DeviceProgram:
                 self._bind_softmax(ins[0], out)
             else:
                 raise InputMismatch(f"cannot execute node kind {kind}")
+        self._bind_workspace()
         # graph outputs / kept values that ended up in bf16 get an f32 copy
         self.out_vals = []
         for o in list(g.outputs) + self.keep:
             v = self.vals[o]
             self.out_vals.append(v)
         del D
+
+    def _bind_workspace(self):
+        """One split-K workspace shared by every tensor-core conv (they run
+        in order on one stream), sized for the largest."""
+        import torch
+        from . import device as D
+        need = max((D.conv_workspace_bytes(p) for p in self.tc_params), default=0)
+        self.workspace_bytes = need
+        self.workspace = None
+        if need:
+            self.workspace = torch.zeros(need // 4 + 1, dtype=torch.float32, device=self.device)
+            for p in self.tc_params:
+                D.set_workspace(p, self.workspace)
 
     # conv ---------------------------------------------------------------------
     def _bind_conv(self, node, out: _Val):
@@ -578,6 +593,7 @@ class DeviceProgram:
                               bool(epi.get("relu")), x_cb=self._window(data),
                               out_cb=self._window(out), flags=flags,
                               tile=tile if any(tile.values()) else None)
+            self.tc_params.append(p)
             self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream))
             return
         # SIMT fp32 path (fp32 mode, NCHW data, or tensor-core-illegal blocks)
@@ -762,6 +778,7 @@ class DeviceProgram:
                               units, 1, 1, (1, 1), (0, 0), x, y, bias=b_t, relu=relu,
                               flags=self.round_flag if o_t.dtype == torch.float32 and
                               self._feeds_tc_dense(out.nid) else 0, tile=tile)
+            self.tc_params.append(p)
             self._emit(f"dense{node.id}_tc", lambda p=p: D.conv2d(p, self.stream))
             return
         a_t = self._as_f32(src) if self.mode != "bf16" or src.tensor.dtype != torch.bfloat16 \

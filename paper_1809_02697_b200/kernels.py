@@ -32,7 +32,8 @@ from .layout import NCHW, Tensor, kcrsck, nchwc
 
 UNROLL_LIMIT = 25  # kept for API compatibility (CPU window-flattening limit)
 
-TILE_FIELDS = ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages")
+TILE_FIELDS = ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
+               "split_k")
 
 
 @dataclass(frozen=True)
@@ -94,6 +95,7 @@ class ConvSchedule:
     tile_n: int = 0
     slices_per_stage: int = 0
     stages: int = 0
+    split_k: int = 0
 
     def check(self, wl: ConvWorkload) -> None:
         """Divisibility rules of the reference (kernels.py:56-63)."""

@@ -27,7 +27,7 @@ def tf32_round(a):
 
 def run_conv(mode, x_nchw, w_kcrs, stride, pad, ic_bn, oc_bn, scale=None, shift=None,
              bias=None, residual=None, relu=False, out_f32=True, tile=None, pad_channels=False,
-             out_cb=None):
+             out_cb=None, workspace=False):
     import torch
     from paper_1809_02697_b200 import _lib as L
     from paper_1809_02697_b200 import device as D
@@ -59,10 +59,18 @@ def run_conv(mode, x_nchw, w_kcrs, stride, pad, ic_bn, oc_bn, scale=None, shift=
     res = None
     if residual is not None:
         res = torch.from_numpy(pack_nchw(residual, oc_bn)).to(dev).to(out_dt)
+    # device vectors stay referenced until the launch finished (the params
+    # hold raw pointers)
+    vecs = (t(scale), t(shift), t(bias))
     p = D.conv_params(mode, xb, wdev, out, n, c, h, w, k, r, s, (sh, sw), (ph, pw), ic_bn,
-                      oc_bn, t(scale), t(shift), t(bias), res, relu,
+                      oc_bn, *vecs, res, relu,
                       out_cb=(off, total_cb) if out_cb else (0, 0),
                       flags=(L.FLAG_PAD_CHANNELS if pad_channels else 0), tile=tile)
+    ws = None
+    if workspace:
+        need = D.conv_workspace_bytes(p)
+        ws = torch.zeros(max(need, 4) // 4, dtype=torch.float32, device=dev)
+        D.set_workspace(p, ws)
     D.conv2d(p)
     torch.cuda.synchronize()
     o = out.float().cpu().numpy()
@@ -270,3 +278,60 @@ def test_tc_conv_default_tiles_wide_kernels(cuda, rs, pd):
     ref = oracle.conv2d(x, wt, (1, 1), pd, relu=True)
     got = run_conv(L.MODE_BF16, x, wt, (1, 1), pd, 64, 64, relu=True)
     assert oracle.rel_err(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("case", CASES + [(2, 256, 7, 7, 32, 3, 3, (1, 1), (1, 1))])
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("split", [0, 2, 3])
+def test_tc_conv_split_k(cuda, case, mode_name, split):
+    """Split-K (partials to the workspace, ordered fixup launch running the
+    full epilogue: scale/shift, bias, residual, relu); split 0 = the kernel's
+    automatic choice for under-filled grids."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, r, s, st, pd = case
+    rng = np.random.default_rng(hash(case) % 2**32 + split)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32))
+    oh, ow = (h + 2 * pd[0] - r) // st[0] + 1, (w + 2 * pd[1] - s) // st[1] + 1
+    scale = rng.uniform(0.5, 1.5, k).astype(np.float32)
+    shift = rng.normal(0, 0.1, k).astype(np.float32)
+    bias = rng.normal(0, 0.1, k).astype(np.float32)
+    res = rng.standard_normal((n, k, oh, ow)).astype(np.float32)
+    ref = oracle.conv2d(x, wt, st, pd, scale, shift, bias, residual=res, relu=True)
+    x_bn = min(64 if mode_name == "bf16" else 32, c)
+    y = 16 if k % 16 == 0 else 8
+    got = run_conv(mode, x, wt, st, pd, x_bn, y, scale, shift, bias, residual=res, relu=True,
+                   tile={"split_k": split} if split else None, workspace=True)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_tc_conv_split_k_window_and_halo(cuda):
+    """Split-K writing into a concat window, and a halo-mode split."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(5)
+    x = bf16_round(rng.standard_normal((1, 128, 14, 14)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((64, 128, 3, 3)) * 0.03).astype(np.float32))
+    ref = oracle.conv2d(x, wt, 1, 1, relu=True)
+    o = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 32, relu=True, out_cb=(5, 1),
+                 tile={"split_k": 4}, workspace=True)
+    assert oracle.rel_err(unpack_nchw(o[:, 1:3]), ref) < 1e-4
+    assert np.isnan(o[:, :1]).all() and np.isnan(o[:, 3:]).all()
+    halo = dict(tile_w=16, tile_h=8, tile_img=1, split_k=3)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 32, relu=True, tile=halo,
+                   workspace=True)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+def test_tc_conv_split_k_needs_workspace(cuda):
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200.errors import NeoplanError as NeoError
+    rng = np.random.default_rng(6)
+    x = bf16_round(rng.standard_normal((1, 64, 8, 8)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((64, 64, 3, 3)) * 0.05).astype(np.float32))
+    with pytest.raises(NeoError):
+        run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, tile={"split_k": 3})
+    # automatic split without a workspace silently runs unsplit
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
+    assert oracle.rel_err(got, oracle.conv2d(x, wt, 1, 1)) < 1e-4

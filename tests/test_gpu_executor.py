@@ -103,7 +103,9 @@ def _with_outputs(g, outs):
 
 def test_nhwc_input_and_per_conv_packing(cuda):
     from paper_1809_02697_b200 import (DevicePool, build_model, execute, model_input, passes)
-    g = build_model("resnet18", batch=1, image=64, num_classes=10, softmax=False)
+    # 224x224 (the BASELINE input size): at toy sizes the tf32 logits error of
+    # random-init ResNet-18 spreads around 0.4e-3..1.3e-3 from seed to seed
+    g = build_model("resnet18", batch=1, softmax=False)
     feeds = model_input(g)
     ref = oracle.execute_reference(g, feeds)[0]
     s = passes.simplify(g)

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tile", default="", help="json dict of tile fields")
     ap.add_argument("--flat", action="store_true", help="1x1 conv as a 1 x (H*W) image")
+    ap.add_argument("--once", action="store_true", help="one plain launch (tracing)")
     args = ap.parse_args()
 
     import torch
@@ -59,14 +60,23 @@ def main():
         p = D.conv_params(lmode, x, wd, out, n, c, hh, ww, k, r, r, (st, st), (pad, pad), args.x,
                           args.y, bias=bias, residual=res, relu=True, tile=tile)
         cfg = D.default_tiles(p)
+        ws = torch.zeros(max(D.conv_workspace_bytes(p), 4) // 4, device=dev)
+        D.set_workspace(p, ws)
+        if args.once:
+            D.conv2d(p)
+            torch.cuda.synchronize()
+            return 1e-9, cfg
+        cs = torch.cuda.Stream()
         for _ in range(3):
-            D.conv2d(p)
+            D.conv2d(p, cs)
         torch.cuda.synchronize()
+        # back-to-back launches replayed from a CUDA graph: no host overhead
+        graph = D.capture(lambda: [D.conv2d(p, cs) for _ in range(args.iters)], cs)
+        graph.launch(cs)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(args.iters):
-            D.conv2d(p)
-        b.record()
+        a.record(cs)
+        graph.launch(cs)
+        b.record(cs)
         b.synchronize()
         us = a.elapsed_time(b) * 1e3 / args.iters
         return us, cfg
