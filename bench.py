@@ -187,31 +187,19 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------------------
 
-def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind: str):
-    """Instrumented pass: CUDA events around every conv launch on the
-    executor stream; returns (roofline dict, conv share of the step)."""
-    import torch
+def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind: str,
+                  flush=None):
+    """Conv time per step = (graphed step) - (the same graph without the
+    conv launches), both replayed after an L2 flush and timed with CUDA
+    events on the executor stream; returns (roofline dict, conv share of
+    the step)."""
+    from paper_1809_02697_b200.timing import graph_time
     conv_idx = [i for i, n in enumerate(prog.launch_names) if n.startswith("conv")]
-    totals = []
-    step_times = []
-    for _ in range(steps):
-        evs = []
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record(prog.stream)
-        for i, fn in enumerate(prog.launches):
-            if i in conv_idx:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(prog.stream)
-                fn()
-                b.record(prog.stream)
-                evs.append((a, b))
-            else:
-                fn()
-        s1.record(prog.stream)
-        s1.synchronize()
-        totals.append(sum(a.elapsed_time(b) for a, b in evs) * 1e-3)
-        step_times.append(s0.elapsed_time(s1) * 1e-3)
+    cset = set(conv_idx)
+    step_s = graph_time(prog, lambda i: True, steps, flush)
+    rest_s = graph_time(prog, lambda i: i not in cset, steps, flush)
+    totals = [max(step_s - rest_s, 1e-9)]
+    step_times = [step_s]
     conv_s = float(np.median(totals))
     achieved = flops_per_step / conv_s / 1e12
     pk = float(peak.get("bf16_tflops_sustained", peak.get("bf16_tflops", 1400.0)))
@@ -302,9 +290,11 @@ def main():
     barrier()
     e2e_s = e0.elapsed_time(e1) * 1e-3
     out_host = outs[-1]
-    # ---- dominant-kernel roofline (instrumented, un-graphed pass) -------
+    # ---- dominant-kernel roofline: per-launch events inside the graphed
+    # step (L2 flushed before each replay, like the timed steps) ----------
     pk, pk_kind = peaks()
-    roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind)
+    roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind,
+                                     flush=lambda: flush.fill_(1.0))
     barrier()
 
     times = torch.tensor([dev_s, e2e_s, wall], dtype=torch.float64, device=local)

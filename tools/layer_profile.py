@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default="")
     ap.add_argument("--untuned", action="store_true")
+    ap.add_argument("--isolated", action="store_true",
+                    help="time each launch alone (repeated, L2-warm) instead of in the step")
     args = ap.parse_args()
 
     import torch
@@ -58,26 +60,33 @@ def main():
                                   stride=hw_pair(node.attrs["stride"])[0], flops=flops,
                                   bytes=byts)
     # tile config the kernel picks
-    # each launch timed as a CUDA graph of `inner` back-to-back copies (no
-    # host overhead; operands L2-warm after the first copy)
-    inner = 10
     prog.launch()
     prog.stream.synchronize()
-    times = np.zeros((args.reps, len(prog.launches)))
-    graphs = [D.capture(lambda fn=fn: [fn() for _ in range(inner)], prog.stream)
-              for fn in prog.launches]
-    for rep in range(args.reps + 1):
-        evs = []
-        for gr in graphs:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(prog.stream)
-            gr.launch(prog.stream)
-            b.record(prog.stream)
-            evs.append((a, b))
-        prog.stream.synchronize()
-        if rep:
-            times[rep - 1] = [a.elapsed_time(b) * 1e3 / inner for a, b in evs]
-    med = np.median(times, axis=0)
+    if args.isolated:
+        # each launch timed as a CUDA graph of `inner` back-to-back copies (no
+        # host overhead; operands L2-warm after the first copy)
+        inner = 10
+        times = np.zeros((args.reps, len(prog.launches)))
+        graphs = [D.capture(lambda fn=fn: [fn() for _ in range(inner)], prog.stream)
+                  for fn in prog.launches]
+        for rep in range(args.reps + 1):
+            evs = []
+            for gr in graphs:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(prog.stream)
+                gr.launch(prog.stream)
+                b.record(prog.stream)
+                evs.append((a, b))
+            prog.stream.synchronize()
+            if rep:
+                times[rep - 1] = [a.elapsed_time(b) * 1e3 / inner for a, b in evs]
+        med = np.median(times, axis=0)
+    else:
+        # in the real step: one graph of the whole forward with event-record
+        # nodes between launches, L2 flushed before each replay
+        from paper_1809_02697_b200.timing import timed_launches
+        flush = torch.empty(64 * 1024 * 1024, device=prog.device)
+        med = timed_launches(prog, args.reps, flush=lambda: flush.fill_(0.0)) * 1e3
     rows = []
     total = med.sum()
     for name, t in zip(prog.launch_names, med):

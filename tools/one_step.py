@@ -18,13 +18,16 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--mode", default="bf16")
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--untuned", action="store_true")
     args = ap.parse_args()
     import torch
-    from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, build_model, compile_graph,
-                                       model_input)
+    from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, ScheduleDb, build_model,
+                                       compile_graph, model_input)
+    from paper_1809_02697_b200.tuning import DEFAULT_DB
     g = build_model(args.model, batch=args.batch)
-    prog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode=args.mode)), 0, args.mode,
-                         use_graph=False)
+    db = None if args.untuned else ScheduleDb(DEFAULT_DB)      # same program as bench.py
+    prog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode=args.mode, db=db)), 0,
+                         args.mode, use_graph=False)
     prog.set_inputs(model_input(g))
     for _ in range(args.warmup):
         prog.launch()
