@@ -28,6 +28,7 @@ struct ConvSimtParams {
 };
 
 __global__ void conv_simt_kernel(const ConvSimtParams p) {
+  neo_pdl_enter();
   const int Kb = (p.K + p.y - 1) / p.y;
   const int64_t total = (int64_t)p.N * Kb * p.y * p.OH * p.OW;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -114,7 +115,7 @@ int neo_conv_simt_launch(const neo_conv_params* p, cudaStream_t stream) {
   const int64_t total = (int64_t)k.N * kbt * p->oc_bn * k.OH * k.OW;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>(neo_ceil_div(total, threads), 148 * 64);
-  conv_simt_kernel<<<(int)std::max<int64_t>(blocks, 1), threads, 0, stream>>>(k);
+  neo_launch(conv_simt_kernel, (int)std::max<int64_t>(blocks, 1), threads, 0, stream, k);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

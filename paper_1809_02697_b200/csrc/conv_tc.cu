@@ -421,6 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *tslot_gen;
   if (threadIdx.x == 0) TRACE(61, 0);
+  // PDL: barrier init, TMEM allocation and descriptor prefetch above overlap
+  // the previous kernel's tail; nothing global is touched before this wait
+  neo_pdl_trigger();
+  neo_pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1334,9 +1338,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     done = true;
   }
   if (tf32)
-    conv_tc_kernel<true><<<grid, kThreads, smem, stream>>>(kp);
+    neo_launch(conv_tc_kernel<true>, grid, kThreads, smem, stream, kp);
   else
-    conv_tc_kernel<false><<<grid, kThreads, smem, stream>>>(kp);
+    neo_launch(conv_tc_kernel<false>, grid, kThreads, smem, stream, kp);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

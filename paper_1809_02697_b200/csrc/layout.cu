@@ -74,6 +74,7 @@ struct NhwcMap {  // NHWC -> NCHW; b = n; rows = pixels, cols = channels
 template <typename Ts, typename Td, class Map>
 __global__ void transpose_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, Map m,
                                  int64_t B, int64_t R, int64_t C, bool round) {
+  neo_pdl_enter();
   __shared__ Ts tile[32][33];
   __shared__ bool ok[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -105,7 +106,7 @@ void launch_transpose(const void* src, void* dst, Map m, int64_t B, int64_t R, i
   dim3 block(32, 8);
   dim3 grid((unsigned)neo_ceil_div(C, 32), (unsigned)neo_ceil_div(R, 32),
             (unsigned)std::min<int64_t>(B, 65535));
-  transpose_kernel<Ts, Td, Map><<<grid, block, 0, st>>>(static_cast<const Ts*>(src),
+  neo_launch(transpose_kernel<Ts, Td, Map>, grid, block, 0, st, static_cast<const Ts*>(src),
                                                         static_cast<Td*>(dst), m, B, R, C, round);
 }
 
@@ -114,6 +115,7 @@ void launch_transpose(const void* src, void* dst, Map m, int64_t B, int64_t R, i
 template <typename Ts, typename Td>
 __global__ void retile_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, int64_t N,
                               int64_t Call, int64_t HW, int a, int b, bool round) {
+  neo_pdl_enter();
   const int64_t cbd = (Call + b - 1) / b, cbs = (Call + a - 1) / a;
   const int64_t total = N * cbd * HW * b;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -141,6 +143,7 @@ __global__ void retile_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, 
 template <typename Ts, typename Td, int X>
 __global__ void pack_small_kernel(const Ts* __restrict__ src, Td* __restrict__ dst, int64_t N,
                                   int64_t Call, int64_t HW, bool round) {
+  neo_pdl_enter();
   const int64_t Cb = (Call + X - 1) / X;
   const int64_t total = N * Cb * HW;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -176,9 +179,9 @@ bool try_pack_small(const void* src, void* dst, int64_t n, int64_t c, int64_t hw
   auto s = static_cast<const Ts*>(src);
   auto d = static_cast<Td*>(dst);
   switch (x) {
-    case 4: pack_small_kernel<Ts, Td, 4><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
-    case 8: pack_small_kernel<Ts, Td, 8><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
-    case 16: pack_small_kernel<Ts, Td, 16><<<grid, 256, 0, st>>>(s, d, n, c, hw, round); return true;
+    case 4: neo_launch(pack_small_kernel<Ts, Td, 4>, grid, 256, 0, st, s, d, n, c, hw, round); return true;
+    case 8: neo_launch(pack_small_kernel<Ts, Td, 8>, grid, 256, 0, st, s, d, n, c, hw, round); return true;
+    case 16: neo_launch(pack_small_kernel<Ts, Td, 16>, grid, 256, 0, st, s, d, n, c, hw, round); return true;
     default: return false;
   }
 }
@@ -204,7 +207,7 @@ int dispatch_layout(const void* src, void* dst, int64_t n, int64_t c, int64_t h,
     const int b = dst_tag == NEO_NCHW ? 1 : dst_x;
     const int64_t total = n * neo_ceil_div(c, b) * HW * b;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
-    retile_kernel<Ts, Td><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const Ts*>(src),
+    neo_launch(retile_kernel<Ts, Td>, (unsigned)blocks, 256, 0, st, static_cast<const Ts*>(src),
                                                             static_cast<Td*>(dst), n, c, HW, a, b,
                                                             round);
   }
@@ -217,6 +220,7 @@ int dispatch_layout(const void* src, void* dst, int64_t n, int64_t c, int64_t h,
 template <typename T>
 __global__ void weights_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t K, int64_t C,
                                int64_t RS, int x, int y, bool pack) {
+  neo_pdl_enter();
   const int64_t total = K * C * RS;
   const int64_t Cb = C / x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -241,6 +245,7 @@ template <typename Td>
 __global__ void weights_umma_kernel(const float* __restrict__ src, Td* __restrict__ dst, int64_t K,
                                     int64_t C, int64_t R, int64_t S, int x, int64_t slices,
                                     int64_t nslices, bool round) {
+  neo_pdl_enter();
   const int64_t Cb = (C + x - 1) / x;
   const int64_t total = slices * K * x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -315,10 +320,10 @@ static int weights_common(int dtype, const void* src, void* dst, int64_t k, int6
                 "(K=%lld, C=%lld) not divisible by (y=%d, x=%d)", (long long)k, (long long)c, y, x);
   const int64_t total = k * c * r * s;
   if (dtype == NEO_BF16)
-    weights_kernel<uint16_t><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(weights_kernel<uint16_t>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), k, c, r * s, x, y, pack);
   else
-    weights_kernel<uint32_t><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(weights_kernel<uint32_t>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), k, c, r * s, x, y, pack);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
@@ -348,10 +353,10 @@ extern "C" int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_d
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
   if (dst_dtype == NEO_BF16)
-    weights_umma_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(weights_umma_kernel<__nv_bfloat16>, (unsigned)grid_for(total), 256, 0, st, 
         src_kcrs, static_cast<__nv_bfloat16*>(dst), k, c, r, s, x, slices_padded, nslices, round);
   else
-    weights_umma_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(weights_umma_kernel<float>, (unsigned)grid_for(total), 256, 0, st, 
         src_kcrs, static_cast<float*>(dst), k, c, r, s, x, slices_padded, nslices, round);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
@@ -370,6 +375,7 @@ namespace {
 template <typename Td, int XF>
 __global__ void stem_fold_kernel(const float* __restrict__ src, Td* __restrict__ dst, int64_t N,
                                  int C, int H, int W, int S, int sw, int pw, int OW, bool round) {
+  neo_pdl_enter();
   const int F = S * C;
   const int Cb = (F + XF - 1) / XF;
   const int64_t total = N * Cb * H * (int64_t)OW;
@@ -426,7 +432,7 @@ extern "C" int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
 #define NEO_FOLD(T, X)                                                                      \
-  stem_fold_kernel<T, X><<<grid, 256, 0, st>>>(src, static_cast<T*>(dst), n, (int)c, (int)h, \
+  neo_launch(stem_fold_kernel<T, X>, grid, 256, 0, st, src, static_cast<T*>(dst), n, (int)c, (int)h, \
                                                (int)w, s, stride_w, pad_w, (int)ow, round)
   if (dst_dtype == NEO_BF16) {
     if (xf == 8) NEO_FOLD(__nv_bfloat16, 8);

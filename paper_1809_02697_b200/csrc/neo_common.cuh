@@ -8,7 +8,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "../../include/neob200.h"
 
@@ -35,7 +37,45 @@ void neo_set_error(const char* fmt, ...);
     }                                                                          \
   } while (0)
 
-#define NEO_LAUNCH_CHECK() NEO_CUDA_TRY(cudaGetLastError())
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel is launched with
+// programmaticStreamSerialization, so its CTAs may start (and run their
+// prologue) while the previous kernel on the stream drains; each kernel calls
+// neo_pdl_wait() before touching any global memory the previous kernels
+// produce or read (griddepcontrol.wait returns once they completed and their
+// writes are visible) and neo_pdl_trigger() as early as possible so the next
+// kernel can be scheduled.  NEOB200_NO_PDL=1 launches plainly.
+inline bool neo_pdl_enabled() {
+  static const bool on = getenv("NEOB200_NO_PDL") == nullptr;
+  return on;
+}
+inline cudaError_t& neo_launch_err() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+inline cudaError_t neo_consume_launch_error() {
+  cudaError_t e = neo_launch_err();
+  neo_launch_err() = cudaSuccess;
+  const cudaError_t last = cudaGetLastError();
+  return e != cudaSuccess ? e : last;
+}
+template <typename... KArgs, typename... Args>
+inline void neo_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = neo_pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess && neo_launch_err() == cudaSuccess) neo_launch_err() = e;
+}
+#define NEO_LAUNCH_CHECK() NEO_CUDA_TRY(neo_consume_launch_error())
 
 static inline int64_t neo_ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline size_t neo_dtype_size(int dt) { return dt == NEO_BF16 ? 2 : 4; }
@@ -65,6 +105,18 @@ __device__ __forceinline__ float neo_round_tf32(float v) {
 
 // ---------------------------------------------------------------------------
 // sm_100a PTX wrappers
+
+__device__ __forceinline__ void neo_pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void neo_pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// simple kernels: wait for the producers, then let the next kernel launch
+__device__ __forceinline__ void neo_pdl_enter() {
+  neo_pdl_wait();
+  neo_pdl_trigger();
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -32,6 +32,7 @@ template <typename T>
 __global__ void pool_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t N, int64_t Cb,
                             int H, int W, int OH, int OW, int x, int win, int stride, int pad,
                             bool is_max, bool round, Win wnd) {
+  neo_pdl_enter();
   const int64_t total = N * Cb * OH * OW * x;
   const float inv = (float)(win * win);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -73,6 +74,7 @@ __global__ void eltwise_kernel(const T* __restrict__ a, const T* __restrict__ b,
                                const float* __restrict__ scale, const float* __restrict__ shift,
                                int64_t total, int64_t Cb, int64_t HW, int x, int op, bool round,
                                Win wnd) {
+  neo_pdl_enter();
   const int64_t plane_sz = HW * x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -149,6 +151,7 @@ template <typename T, int V, bool IS_MAX, int WIN>
 __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, int64_t Cb,
                                int64_t P, int H, int W, int OH, int OW, int x, int win_rt,
                                int stride, int pad, bool round, Win wnd) {
+  neo_pdl_enter();
   constexpr int NP = V / 2;
   const int win = WIN > 0 ? WIN : win_rt;
   const uint32_t groups = x / V;
@@ -239,6 +242,7 @@ __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, in
 template <typename T, bool IS_MAX>
 __global__ void pool_global(const T* __restrict__ in, T* __restrict__ out, int64_t Cb,
                             int64_t P, int HW, int x, float inv, bool round, Win wnd) {
+  neo_pdl_enter();
   using T2 = typename std::conditional<sizeof(T) == 2, __nv_bfloat162, float2>::type;
   const int pairs = x / 2;
   const int64_t total = P * pairs;
@@ -281,13 +285,13 @@ void launch_pool_vec(const T* in, T* out, int64_t cb, int64_t P, int h, int w, i
                      int x, int win, int stride, int pad, bool round, Win wnd, cudaStream_t st) {
   const dim3 grid = plane_grid(P, (int64_t)OH * OW * (x / V));
   if (win == 3)
-    pool_plane_vec<T, V, IS_MAX, 3><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+    neo_launch(pool_plane_vec<T, V, IS_MAX, 3>, grid, 256, 0, st, in, out, cb, P, h, w, OH, OW, x, win,
                                                           stride, pad, round, wnd);
   else if (win == 2)
-    pool_plane_vec<T, V, IS_MAX, 2><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+    neo_launch(pool_plane_vec<T, V, IS_MAX, 2>, grid, 256, 0, st, in, out, cb, P, h, w, OH, OW, x, win,
                                                           stride, pad, round, wnd);
   else
-    pool_plane_vec<T, V, IS_MAX, 0><<<grid, 256, 0, st>>>(in, out, cb, P, h, w, OH, OW, x, win,
+    neo_launch(pool_plane_vec<T, V, IS_MAX, 0>, grid, 256, 0, st, in, out, cb, P, h, w, OH, OW, x, win,
                                                           stride, pad, round, wnd);
 }
 
@@ -296,6 +300,7 @@ __global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__
                                   T* __restrict__ out, const float* __restrict__ scale,
                                   const float* __restrict__ shift, int64_t Cb, int64_t P,
                                   int64_t plane_sz, int x, int op, bool round, Win wnd) {
+  neo_pdl_enter();
   const uint32_t vecs = (uint32_t)(plane_sz / V);
   for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
     const T* ap = a + wnd.in_plane(plane, Cb) * plane_sz;
@@ -346,6 +351,7 @@ __global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__
 template <typename T>
 __global__ void concat_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t outer,
                               int64_t chunk, int64_t dst_row, int64_t dst_off) {
+  neo_pdl_enter();
   const int64_t total = outer * chunk;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -357,6 +363,7 @@ __global__ void concat_kernel(const T* __restrict__ src, T* __restrict__ dst, in
 // 16-byte vector variant when every row boundary is 16-byte aligned
 __global__ void concat_kernel_v4(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                  int64_t outer, int64_t chunk, int64_t dst_row, int64_t dst_off) {
+  neo_pdl_enter();
   const int64_t total = outer * chunk;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -371,6 +378,7 @@ template <typename T, int NB>
 __global__ void dense_kernel(const T* __restrict__ a, const T* __restrict__ w,
                              const float* __restrict__ bias, float* __restrict__ out, int64_t n,
                              int64_t in_f, int64_t units) {
+  neo_pdl_enter();
   const int warps = blockDim.x / 32;
   const int64_t u = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -398,6 +406,7 @@ __global__ void dense_kernel(const T* __restrict__ a, const T* __restrict__ w,
 // softmax over the last axis: e = exp(a - max); e / sum(e)   (executor.py:167-170)
 __global__ void softmax_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t rows,
                                int64_t cols) {
+  neo_pdl_enter();
   __shared__ float red[32];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* a = in + row * cols;
@@ -466,19 +475,19 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
       auto i = static_cast<const __nv_bfloat16*>(in);
       auto o = static_cast<__nv_bfloat16*>(out);
       if (is_max)
-        pool_global<__nv_bfloat16, true><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv,
+        neo_launch(pool_global<__nv_bfloat16, true>, grid, 256, 0, st, i, o, cb, P, (int)(h * w), x, inv,
                                                                round, wnd);
       else
-        pool_global<__nv_bfloat16, false><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x,
+        neo_launch(pool_global<__nv_bfloat16, false>, grid, 256, 0, st, i, o, cb, P, (int)(h * w), x,
                                                                 inv, round, wnd);
     } else {
       auto i = static_cast<const float*>(in);
       auto o = static_cast<float*>(out);
       if (is_max)
-        pool_global<float, true><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv, round,
+        neo_launch(pool_global<float, true>, grid, 256, 0, st, i, o, cb, P, (int)(h * w), x, inv, round,
                                                        wnd);
       else
-        pool_global<float, false><<<grid, 256, 0, st>>>(i, o, cb, P, (int)(h * w), x, inv, round,
+        neo_launch(pool_global<float, false>, grid, 256, 0, st, i, o, cb, P, (int)(h * w), x, inv, round,
                                                         wnd);
     }
   } else if (dtype == NEO_BF16 && x % 8 == 0 && al) {
@@ -500,11 +509,11 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
       launch_pool_vec<float, 4, false>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x, win,
                                        stride, pad, round, wnd, st);
   } else if (dtype == NEO_BF16)
-    pool_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(pool_kernel<__nv_bfloat16>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const __nv_bfloat16*>(in), static_cast<__nv_bfloat16*>(out), n, cb, (int)h,
         (int)w, (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   else
-    pool_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(pool_kernel<float>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
         (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
   NEO_LAUNCH_CHECK();
@@ -543,19 +552,19 @@ extern "C" int neo_eltwise_window(int dtype, int op, const void* a, const void* 
   const bool al = aligned16(a) && aligned16(out) && (!b || aligned16(b)) &&
                   (op < NEO_ELT_SCALE_SHIFT || (aligned16(scale) && aligned16(shift)));
   if (dtype == NEO_BF16 && x % 8 == 0 && al) {
-    eltwise_plane_vec<__nv_bfloat16, 8><<<plane_grid(P, plane_sz / 8), 256, 0, st>>>(
+    neo_launch(eltwise_plane_vec<__nv_bfloat16, 8>, plane_grid(P, plane_sz / 8), 256, 0, st, 
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
         static_cast<__nv_bfloat16*>(out), scale, shift, cb, P, plane_sz, x, op, round, wnd);
   } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
-    eltwise_plane_vec<float, 4><<<plane_grid(P, plane_sz / 4), 256, 0, st>>>(
+    neo_launch(eltwise_plane_vec<float, 4>, plane_grid(P, plane_sz / 4), 256, 0, st, 
         static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out),
         scale, shift, cb, P, plane_sz, x, op, round, wnd);
   } else if (dtype == NEO_BF16)
-    eltwise_kernel<__nv_bfloat16><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(eltwise_kernel<__nv_bfloat16>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
         static_cast<__nv_bfloat16*>(out), scale, shift, total, cb, hw, x, op, round, wnd);
   else
-    eltwise_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(eltwise_kernel<float>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out), scale,
         shift, total, cb, hw, x, op, round, wnd);
   NEO_LAUNCH_CHECK();
@@ -581,15 +590,15 @@ extern "C" int neo_concat_copy(int dtype, const void* src, void* dst, int64_t ou
   if (chunk % per == 0 && dst_row % per == 0 && dst_off % per == 0 &&
       ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0) {
     const int64_t total = outer * (chunk / per);
-    concat_kernel_v4<<<(unsigned)grid_for(total), 256, 0, st>>>(
+    neo_launch(concat_kernel_v4, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), outer, chunk / per,
         dst_row / per, dst_off / per);
   } else if (es == 2) {
-    concat_kernel<uint16_t><<<(unsigned)grid_for(outer * chunk), 256, 0, st>>>(
+    neo_launch(concat_kernel<uint16_t>, (unsigned)grid_for(outer * chunk), 256, 0, st, 
         static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), outer, chunk, dst_row,
         dst_off);
   } else {
-    concat_kernel<uint32_t><<<(unsigned)grid_for(outer * chunk), 256, 0, st>>>(
+    neo_launch(concat_kernel<uint32_t>, (unsigned)grid_for(outer * chunk), 256, 0, st, 
         static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), outer, chunk, dst_row,
         dst_off);
   }
@@ -607,11 +616,11 @@ extern "C" int neo_dense(int dtype, const void* a, const void* w, const float* b
   dim3 grid((unsigned)neo_ceil_div(units, threads / 32),
             (unsigned)std::min<int64_t>(neo_ceil_div(n, NB), 65535));
   if (dtype == NEO_BF16)
-    dense_kernel<__nv_bfloat16, NB><<<grid, threads, 0, st>>>(
+    neo_launch(dense_kernel<__nv_bfloat16, NB>, grid, threads, 0, st, 
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(w), bias, out, n,
         in_features, units);
   else
-    dense_kernel<float, NB><<<grid, threads, 0, st>>>(static_cast<const float*>(a),
+    neo_launch(dense_kernel<float, NB>, grid, threads, 0, st, static_cast<const float*>(a),
                                                       static_cast<const float*>(w), bias, out, n,
                                                       in_features, units);
   NEO_LAUNCH_CHECK();
@@ -622,8 +631,8 @@ extern "C" int neo_softmax(const float* in, float* out, int64_t rows, int64_t co
                            neo_stream_t stream) {
   NEO_CHECK_ARG(in && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
   NEO_CHECK_ARG(rows >= 1 && cols >= 1, NEO_ERR_SHAPE_MISMATCH, "bad softmax dims");
-  softmax_kernel<<<(unsigned)std::min<int64_t>(rows, 148 * 8), 256, 0,
-                   static_cast<cudaStream_t>(stream)>>>(in, out, rows, cols);
+  neo_launch(softmax_kernel, (unsigned)std::min<int64_t>(rows, 148 * 8), 256, 0,
+                   static_cast<cudaStream_t>(stream), in, out, rows, cols);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
