@@ -574,8 +574,8 @@ class DeviceProgram:
         vec = lambda v: None if v is None else self._upload(np.asarray(v, np.float32))
         t_scale, t_shift, t_bias = vec(scale), vec(shift), vec(bias)
         sched = node.attrs.get("schedule") or {}
-        tile = {f: sched.get(f, 0) for f in ("tile_w", "tile_h", "tile_img", "tile_n",
-                                             "slices_per_stage", "stages")}
+        from .kernels import TILE_FIELDS
+        tile = {f: sched.get(f, 0) for f in TILE_FIELDS}
         if fold is not None:      # tuned for the unfolded workload: let the kernel pick
             tile = {}
         if use_tc:
