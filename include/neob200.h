@@ -151,6 +151,10 @@ typedef struct neo_conv_params {
   int split_k;
   void* workspace;
   int64_t workspace_bytes;
+  /* CTA pairs (cta_group::2): two CTAs of a cluster compute one 256-row M
+   * tile, each holding half of the A rows and half of the weight rows, so a
+   * weight byte serves 256 pixels (0 = automatic, 1 = off, 2 = on). */
+  int cta_pair;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);

@@ -64,6 +64,7 @@ class ConvParams(ctypes.Structure):
         ("tile_w", _c_int), ("tile_h", _c_int), ("tile_img", _c_int), ("tile_n", _c_int),
         ("slices_per_stage", _c_int), ("stages", _c_int),
         ("split_k", _c_int), ("workspace", _c_vp), ("workspace_bytes", _c_i64),
+        ("cta_pair", _c_int),
     ]
 
 

@@ -84,6 +84,13 @@ struct ConvTCParams {
   // unit stores its raw fp32 accumulator to ws[u][chunk16][row][16] and,
   // after all splits of the tile arrived, reduces and finishes 1/splits of it.
   int splits, kps, num_units;
+  // CTA pair (cta_group::2): the two CTAs of a cluster own the two 128-row
+  // halves of a 256-row M tile and the two halves of its N tile; the leader
+  // (rank 0) issues M=256 MMAs reading both CTAs' shared memory, so every
+  // weight byte fetched serves 256 output pixels.  Group g -> N tile
+  // g % tiles_k, M tiles 2 * (g / tiles_k) + rank (a missing odd tile is a
+  // dummy: loads out of bounds, stores clipped).
+  int pair, tiles_m, num_groups;
   float* ws;        // partials
   int* counters;    // per-tile arrival counters (zero between launches)
 };
@@ -99,6 +106,19 @@ __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n
   oh0 = hi * p.BH;
   ow0 = wi * p.BW;
   k0 = kt * p.BN;
+}
+
+// i-th work unit of this CTA, or -1 when done
+__device__ __forceinline__ int cta_unit(const ConvTCParams& p, int i, int rank) {
+  if (!p.pair) {
+    const int u = (int)blockIdx.x + i * (int)gridDim.x;
+    return u < p.num_units ? u : -1;
+  }
+  const int g = (int)blockIdx.x / 2 + i * ((int)gridDim.x / 2);
+  if (g >= p.num_groups) return -1;
+  const int kt = g % p.tiles_k;
+  const int tm = (g / p.tiles_k) * 2 + rank;
+  return tm * p.tiles_k + kt;
 }
 
 struct EpiAccess {
@@ -364,7 +384,10 @@ __device__ __forceinline__ void trace(int ev, int t, unsigned* cnt) {
 #define TRACE(ev, t)
 #endif
 
-template <bool TF32>
+// PAIR: CTA-pair (cta_group::2) instantiation, launched as 2-CTA clusters;
+// kernels containing cta_group::2 instructions cannot run unclustered, so
+// single-CTA tiles use the PAIR=false instantiation
+template <bool TF32, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
@@ -386,6 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const bool leader_cta = rank == 0;
 #ifdef NEO_TRACE
   __shared__ unsigned s_trace_cnt[32];
   if (threadIdx.x < 32) s_trace_cnt[threadIdx.x] = 0;
@@ -406,15 +431,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     }
     for (int a = 0; a < p.ngroups; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), kEpiWarps / p.ngroups);
+      // pair: the leader's MMA waits for both CTAs' epilogue warps
+      mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * (kEpiWarps / p.ngroups));
       mbar_init(res_bar(a, 0), 1);
       mbar_init(res_bar(a, 1), 1);
     }
     fence_mbar_init();
   }
+  if constexpr (PAIR) cluster_sync_all();   // peer barriers initialised before any remote arrive
   if (warp == 1) {
-    tmem_alloc(tslot, p.tmem_cols);
-    tmem_relinquish();
+    if constexpr (PAIR) {
+      tmem_alloc2(tslot, p.tmem_cols);
+      tmem_relinquish2();
+    } else {
+      tmem_alloc(tslot, p.tmem_cols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -431,7 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      // pair: the peer's loads complete on the leader's full barriers
+      const uint32_t fbar_base = PAIR ? mapa_shared(full_bar(0), 0) : full_bar(0);
+      const int bofs = PAIR ? rank * (p.BN / 2) : 0;   // weight rows this CTA fetches
+      for (int i = 0;; ++i) {
+        const int u = cta_unit(p, i, rank);
+        if (u < 0) break;
         const int t = u / p.splits;
         const int ks0 = (u - t * p.splits) * p.kps;
         const int ks1 = min(p.kstages, ks0 + p.kps);
@@ -442,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         if (p.halo) {
           for (int ks = ks0; ks < ks1; ++ks) {
             mbar_wait(empty_bar(stage), phase ^ 1u);
-            mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
+            const uint32_t fb = fbar_base + 8u * stage;
+            if (leader_cta) mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
             const uint32_t a_dst = sA + stage * p.a_stage;
             const uint32_t b_dst = sB + stage * p.b_stage;
             for (int g = 0; g < p.G; ++g) {
@@ -452,8 +490,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 co = pi % p.Cb;
                 r = pi / p.Cb;
               }
-              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0, ih0 + r, co, n0);
-              tma_load_4d(b_dst + g * p.b_sub, &p.tmB, full_bar(stage), 0, k0, co, r * p.S);
+              if (!PAIR || leader_cta) {
+                tma_load_5d(a_dst + g * p.a_sub, &p.tmA, fb, 0, iw0, ih0 + r, co, n0);
+                tma_load_4d(b_dst + g * p.b_sub, &p.tmB, fb, 0, k0 + bofs, co, r * p.S);
+              } else if constexpr (PAIR) {
+                tma_load_5d_pair(a_dst + g * p.a_sub, &p.tmA, fb, 0, iw0, ih0 + r, co, n0);
+                tma_load_4d_pair(b_dst + g * p.b_sub, &p.tmB, fb, 0, k0 + bofs, co, r * p.S);
+              }
             }
             if (++stage == p.stages) {
               stage = 0;
@@ -470,12 +513,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           TRACE(1, t);
           mbar_wait(empty_bar(stage), phase ^ 1u);
           TRACE(2, t);
-          mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
+          const uint32_t fb = fbar_base + 8u * stage;
+          if (leader_cta) mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
           const uint32_t a_dst = sA + stage * p.a_stage;
           for (int g = 0; g < p.G; ++g, ++sl) {
+            const int cx = sl < p.nslices ? iw0 + sc : 0;     // stage padding slice:
+            const int cy = sl < p.nslices ? ih0 + rc : 0;     // fully out of bounds -> zeros
+            const int cc = sl < p.nslices ? co : p.Cb;
+            if (!PAIR || leader_cta) tma_load_5d(a_dst + g * p.a_sub, &p.tmA, fb, 0, cx, cy, cc, n0);
+            else if constexpr (PAIR) tma_load_5d_pair(a_dst + g * p.a_sub, &p.tmA, fb, 0, cx, cy, cc, n0);
             if (sl < p.nslices) {
-              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, iw0 + sc, ih0 + rc, co,
-                          n0);
               if (++co == p.Cb) {
                 co = 0;
                 if (++sc == p.S) {
@@ -483,11 +530,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                   ++rc;
                 }
               }
-            } else {   // stage padding slice: fully out of bounds -> zeros
-              tma_load_5d(a_dst + g * p.a_sub, &p.tmA, full_bar(stage), 0, 0, 0, p.Cb, n0);
             }
           }
-          tma_load_3d(sB + stage * p.b_stage, &p.tmB, full_bar(stage), 0, k0, ks * p.G);
+          if (!PAIR || leader_cta) tma_load_3d(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
+          else if constexpr (PAIR) tma_load_3d_pair(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1u;
@@ -496,9 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, kTileM, p.BN);
+    if (lane == 0 && leader_cta) {
+      // ---------------- MMA issuer (pair: the leader issues M=256) ----------
+      const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, PAIR ? 2 * kTileM : kTileM, p.BN);
       const int ksteps = p.G * p.rowb / 32;
       // descriptors of stage 0; other stages / K steps only move the 14-bit
       // start-address field (byte offset >> 4), so they are formed by adds
@@ -511,8 +557,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       const uint32_t kpr_mask = (1u << kpr_shift) - 1u;
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
+        const int u = cta_unit(p, it, rank);
+        if (u < 0) break;
         const int t = u / p.splits;
         const int ks0 = (u - t * p.splits) * p.kps;
         const int ks1 = min(p.kstages, ks0 + p.kps);
@@ -531,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           const uint32_t b0 = sB + stage * p.b_stage;
           if (p.halo) {
             // 128-byte rows (SW128): tap s = A view shifted by s rows
-            const uint32_t b_tap = (uint32_t)p.BN * 128u;
+            const uint32_t b_tap = (uint32_t)(PAIR ? p.BN / 2 : p.BN) * 128u;
             for (int g = 0; g < p.G; ++g) {
               for (int s = 0; s < p.S; ++s) {
                 const uint32_t a_s = a0 + g * p.a_sub + s * 128u;
@@ -541,11 +588,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 for (int kk = 0; kk < 4; ++kk) {
                   const uint64_t ad = umma_smem_desc(a_s + 32u * kk, 16, 1024, 2, bo);
                   const uint64_t bd = umma_smem_desc(b_s + 32u * kk, 16, 1024, 2);
-                  umma_ss<TF32>(d_tmem, ad, bd, idesc, ((ks - ks0) | g | s | kk) != 0);
+                  if constexpr (PAIR) umma_ss2<TF32>(d_tmem, ad, bd, idesc, ((ks - ks0) | g | s | kk) != 0);
+                  else umma_ss<TF32>(d_tmem, ad, bd, idesc, ((ks - ks0) | g | s | kk) != 0);
                 }
               }
             }
-            umma_commit(empty_bar(stage));
+            if constexpr (PAIR) umma_commit2_mc(empty_bar(stage), 3);
+            else umma_commit(empty_bar(stage));
             if (++stage == p.stages) {
               stage = 0;
               phase ^= 1u;
@@ -565,16 +614,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               aoff = sub * p.a_sub + inrow;
               boff = sub * p.b_sub + inrow;
             }
-            umma_ss<TF32>(d_tmem, ad_stage + (aoff >> 4), bd_stage + (boff >> 4), idesc,
-                          ((ks - ks0) | k) != 0);
+            if constexpr (PAIR)
+              umma_ss2<TF32>(d_tmem, ad_stage + (aoff >> 4), bd_stage + (boff >> 4), idesc,
+                             ((ks - ks0) | k) != 0);
+            else
+              umma_ss<TF32>(d_tmem, ad_stage + (aoff >> 4), bd_stage + (boff >> 4), idesc,
+                            ((ks - ks0) | k) != 0);
           }
-          umma_commit(empty_bar(stage));
+          if constexpr (PAIR) umma_commit2_mc(empty_bar(stage), 3);
+          else umma_commit(empty_bar(stage));
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(tfull_bar(acc));
+        if constexpr (PAIR) umma_commit2_mc(tfull_bar(acc), 3);
+        else umma_commit(tfull_bar(acc));
         TRACE(13, t);
       }
     }
@@ -593,9 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const uint32_t bar_id = 1 + grp;
     const size_t plane = (size_t)p.OH * p.OW * p.y;
     uint32_t res_phase = 0u;                // phase of this group's residual barrier
-    int it = grp;
-    for (int u = blockIdx.x + grp * gridDim.x; u < p.num_units;
-         u += p.ngroups * gridDim.x, it += p.ngroups) {
+    // pair: accumulator releases go to the leader CTA's tempty barriers
+    const uint32_t tempty_base = PAIR ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
+    for (int it = grp;; it += p.ngroups) {
+      const int u = cta_unit(p, it, rank);
+      if (u < 0) break;
       const int t = u / p.splits;
       int n0, oh0, ow0, k0;
       decode_tile(p, t, n0, oh0, ow0, k0);
@@ -626,7 +683,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(acc));
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
         __threadfence();
         named_bar_sync(bar_id, gthreads);
         if (leader) {
@@ -717,7 +777,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(acc));
+            if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
           }
           if (leader) TRACE(30 + grp, t);
           fence_proxy_async_smem();
@@ -751,7 +814,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
     }
     if (leader) bulk_wait_all();
     if (leader) TRACE(64, 0);
@@ -764,9 +830,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (blockIdx.x == 0 && threadIdx.x < kTraceWarps)
     g_trace_cnt[threadIdx.x] = min(s_trace_cnt[threadIdx.x], (unsigned)kTracePerWarp);
 #endif
+  if constexpr (PAIR) cluster_sync_all();   // the peer's TMEM is written by the leader's MMAs
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+    if constexpr (PAIR) tmem_dealloc2(tmem_base, p.tmem_cols);
+    else tmem_dealloc(tmem_base, p.tmem_cols);
   }
 }
 
@@ -927,8 +995,20 @@ static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
 static int halo_a_rows(const neo_conv_params* p) {
   return (int)neo_ceil_div(kTileM + p->s - 1, 8) * 8;
 }
-static int64_t halo_pair_bytes(const neo_conv_params* p, int rowb) {
-  return (int64_t)halo_a_rows(p) * rowb + (int64_t)p->s * p->tile_n * rowb;
+// CTA-pair (cta_group::2) tiles: explicit cta_pair (2 on, 1 off) or
+// NEOB200_PAIR=1; needs an unsplit reduction, at least two M tiles and an N
+// tile whose halves are whole 16-row pieces
+static bool use_pair(const neo_conv_params* p, int tile_n, int64_t m_tiles) {
+  static const bool env_on = getenv("NEOB200_PAIR") && atoi(getenv("NEOB200_PAIR")) > 0;
+  const bool want = p->cta_pair == 2 || (p->cta_pair == 0 && env_on);
+  return want && p->split_k <= 1 && m_tiles >= 2 && tile_n % 32 == 0;
+}
+// weight rows one CTA holds per slice
+static int b_rows(const neo_conv_params* p, int tile_n, int64_t m_tiles) {
+  return use_pair(p, tile_n, m_tiles) ? tile_n / 2 : tile_n;
+}
+static int64_t halo_pair_bytes(const neo_conv_params* p, int rowb, int64_t m_tiles) {
+  return (int64_t)halo_a_rows(p) * rowb + (int64_t)p->s * b_rows(p, p->tile_n, m_tiles) * rowb;
 }
 
 int neo_conv_default_tiles(neo_conv_params* p) {
@@ -993,7 +1073,7 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     // epilogue staging (wide kernels such as 1x7 shrink the N tile first,
     // then fall back to plain tiles)
     auto fits = [&]() {
-      return 2 * halo_pair_bytes(p, rowb) + staging_of(p->tile_n) <= budget;
+      return 2 * halo_pair_bytes(p, rowb, m_tiles) + staging_of(p->tile_n) <= budget;
     };
     while (!fits() && auto_tn && p->tile_n > 32) p->tile_n /= 2;
     if (!fits() && auto_geom) {
@@ -1034,8 +1114,8 @@ int neo_conv_default_tiles(neo_conv_params* p) {
                                     : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
     const int gmin = rowb == 16 ? 2 : 1;
     for (;;) {
-      const int64_t stage = halo ? (int64_t)g * halo_pair_bytes(p, rowb)
-                                 : (int64_t)g * (kTileM + p->tile_n) * rowb;
+      const int64_t stage = halo ? (int64_t)g * halo_pair_bytes(p, rowb, m_tiles)
+                                 : (int64_t)g * (kTileM + b_rows(p, p->tile_n, m_tiles)) * rowb;
       const int64_t kst = neo_ceil_div(nslices, g);
       const int64_t want = kst <= 1 ? 2 : std::min<int64_t>(6, kst + 1);
       const int64_t fit = (budget - staging) / stage;
@@ -1150,6 +1230,13 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const int64_t nslices = halo ? p->r * Cb : p->r * p->s * Cb;
   const int64_t kstages = neo_ceil_div(nslices, G);
 
+  const int64_t tiles_m_all = neo_ceil_div(OW, BW) * neo_ceil_div(OH, BH) * neo_ceil_div(p->n, BNI);
+  const bool pair = use_pair(p, BN, tiles_m_all);
+  NEO_CHECK_ARG(!(p->cta_pair == 2 && !pair), NEO_ERR_SCHEDULE_INVALID,
+                "cta_pair not possible here (split_k=%d, tile_n=%d, %lld M tiles)", p->split_k,
+                BN, (long long)tiles_m_all);
+  const int bro = pair ? BN / 2 : BN;       // weight rows this CTA loads per slice
+
   ConvTCParams kp;
   memset(&kp, 0, sizeof(kp));
   auto encode = get_encode_fn();
@@ -1178,7 +1265,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                           (cuuint64_t)(p->r * p->s)};
     cuuint64_t strides[3] = {(cuuint64_t)rowb, (cuuint64_t)p->k * rowb,
                              (cuuint64_t)Cb * p->k * rowb};
-    cuuint32_t box[4] = {(cuuint32_t)x, (cuuint32_t)BN, 1u, (cuuint32_t)p->s};
+    cuuint32_t box[4] = {(cuuint32_t)x, (cuuint32_t)bro, 1u, (cuuint32_t)p->s};
     cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
     CUresult r = encode(&kp.tmB, dt, 4, const_cast<void*>(p->w), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
@@ -1188,7 +1275,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     // slices past nslices (stage padding) are out of bounds -> zero filled
     cuuint64_t dims[3] = {(cuuint64_t)x, (cuuint64_t)p->k, (cuuint64_t)nslices};
     cuuint64_t strides[2] = {(cuuint64_t)rowb, (cuuint64_t)p->k * rowb};
-    cuuint32_t box[3] = {(cuuint32_t)x, (cuuint32_t)BN, (cuuint32_t)G};
+    cuuint32_t box[3] = {(cuuint32_t)x, (cuuint32_t)bro, (cuuint32_t)G};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult r = encode(&kp.tmB, dt, 3, const_cast<void*>(p->w), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_code_tma(rowb),
@@ -1226,6 +1313,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                           : nullptr;
     NEO_CHECK_ARG(num_tiles * sp.splits < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many units");
     kp.num_units = (int)(num_tiles * sp.splits);
+    NEO_CHECK_ARG(!pair || sp.splits == 1, NEO_ERR_SCHEDULE_INVALID,
+                  "CTA-pair tiles need an unsplit reduction");
+    kp.pair = pair ? 1 : 0;
+    kp.tiles_m = (int)tiles_m_all;
+    kp.num_groups = pair ? (int)(kp.tiles_k * neo_ceil_div(tiles_m_all, 2)) : kp.num_units;
   }
   kp.G = G;
   kp.kstages = (int)kstages;
@@ -1247,12 +1339,12 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   }
   if (halo) {
     kp.a_sub = (uint32_t)(halo_a_rows(p) * rowb);
-    kp.b_sub = (uint32_t)(p->s * BN * rowb);
-    kp.tx_bytes = (uint32_t)(G * (BW * BH * rowb + p->s * BN * rowb));
+    kp.b_sub = (uint32_t)(p->s * bro * rowb);
+    kp.tx_bytes = (uint32_t)((pair ? 2 : 1) * G * (BW * BH * rowb + p->s * bro * rowb));
   } else {
     kp.a_sub = (uint32_t)(kTileM * rowb);
-    kp.b_sub = (uint32_t)(BN * rowb);
-    kp.tx_bytes = (uint32_t)(G * (BW * BH * BNI * rowb + BN * rowb));
+    kp.b_sub = (uint32_t)(bro * rowb);
+    kp.tx_bytes = (uint32_t)((pair ? 2 : 1) * G * (BW * BH * BNI * rowb + bro * rowb));
   }
   kp.a_stage = kp.a_sub * G;
   kp.b_stage = kp.b_sub * G;
@@ -1321,26 +1413,46 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                      (size_t)kp.ngroups * kParamFloats * 4;
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
-  const int grid = (int)std::min<int64_t>(kp.num_units, sm_count_of_current_device());
+  const int sms = sm_count_of_current_device();
+  const int grid = pair ? (int)std::min<int64_t>(kp.num_groups, sms / 2) * 2
+                        : (int)std::min<int64_t>(kp.num_units, sms);
   // opt in to the large dynamic shared memory once per (device, kernel); the
   // attribute call is kept out of later launches so they can be graph-captured
-  static bool attr_set[64][2] = {};
+  static bool attr_set[64][4] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  bool& done = attr_set[dev & 63][tf32 ? 1 : 0];
+  bool& done = attr_set[dev & 63][(tf32 ? 1 : 0) + (pair ? 2 : 0)];
   if (!done) {
-    if (tf32)
-      NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-    else
-      NEO_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<false>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    const void* fn = tf32 ? (pair ? (const void*)conv_tc_kernel<true, true>
+                                  : (const void*)conv_tc_kernel<true, false>)
+                          : (pair ? (const void*)conv_tc_kernel<false, true>
+                                  : (const void*)conv_tc_kernel<false, false>);
+    NEO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemBudget));
     done = true;
   }
-  if (tf32)
-    neo_launch(conv_tc_kernel<true>, grid, kThreads, smem, stream, kp);
-  else
-    neo_launch(conv_tc_kernel<false>, grid, kThreads, smem, stream, kp);
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = neo_pdl_enabled() ? 2 : 1;
+    if (tf32) NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, true>, kp));
+    else NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, true>, kp));
+  } else if (tf32) {
+    neo_launch(conv_tc_kernel<true, false>, grid, kThreads, smem, stream, kp);
+  } else {
+    neo_launch(conv_tc_kernel<false, false>, grid, kThreads, smem, stream, kp);
+  }
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

@@ -335,3 +335,38 @@ def test_tc_conv_split_k_needs_workspace(cuda):
     # automatic split without a workspace silently runs unsplit
     got = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64)
     assert oracle.rel_err(got, oracle.conv2d(x, wt, 1, 1)) < 1e-4
+
+
+PAIR_CASES = [
+    # (n, c, h, w, k, r, s, stride, pad), tile
+    ((2, 64, 28, 28, 128, 1, 1, (1, 1), (0, 0)), {"cta_pair": 2}),
+    ((2, 128, 28, 28, 256, 1, 1, (1, 1), (0, 0)), {"cta_pair": 2, "tile_n": 256}),
+    ((3, 128, 14, 14, 256, 3, 3, (1, 1), (1, 1)), {"cta_pair": 2}),                     # halo
+    ((3, 128, 14, 14, 256, 3, 3, (1, 1), (1, 1)), {"cta_pair": 2, "tile_w": 14, "tile_h": 9,
+                                                    "tile_img": 1, "slices_per_stage": 2}),
+    ((1, 64, 29, 29, 96, 3, 3, (2, 2), (1, 1)), {"cta_pair": 2, "tile_n": 96}),         # odd M tiles
+    ((1, 3, 30, 30, 64, 3, 3, (1, 1), (1, 1)), {"cta_pair": 2}),                        # padded C
+]
+
+
+@pytest.mark.parametrize("case,tile", PAIR_CASES)
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+def test_tc_conv_cta_pair(cuda, case, tile, mode_name):
+    """cta_group::2 tiles: two CTAs hold the halves of a 256-row M tile and
+    of the weight rows; full epilogue with residual, dummy odd M tiles."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, r, s, st, pd = case
+    rng = np.random.default_rng(k + r + c)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32))
+    oh, ow = (h + 2 * pd[0] - r) // st[0] + 1, (w + 2 * pd[1] - s) // st[1] + 1
+    bias = rng.normal(0, 0.1, k).astype(np.float32)
+    res = rng.standard_normal((n, k, oh, ow)).astype(np.float32)
+    ref = oracle.conv2d(x, wt, st, pd, bias=bias, residual=res, relu=True)
+    lanes = 8 if mode_name == "bf16" else 4
+    x_bn = min(64 if mode_name == "bf16" else 32, c) if c >= lanes else lanes
+    got = run_conv(mode, x, wt, st, pd, x_bn, 32, bias=bias, residual=res, relu=True, tile=tile,
+                   pad_channels=c < lanes)
+    assert oracle.rel_err(got, ref) < 1e-4
