@@ -210,10 +210,20 @@ def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind
             traffic = json.load(open(tpath)).get("bytes_per_step")
         except Exception:
             traffic = None
+    # memory-bound launches (everything but the convs): algorithmic bytes over
+    # their graphed time, against the 8 TB/s nominal and the measured copy peak
+    mem_bytes = sum(b for i, b in enumerate(prog.launch_bytes) if i not in cset)
+    mem_ops = {"launches": len(prog.launches) - len(conv_idx), "time_us": rest_s * 1e6,
+               "algorithmic_bytes": mem_bytes,
+               "achieved_GBps": mem_bytes / max(rest_s, 1e-12) / 1e9,
+               "peak_nominal_GBps": 8000.0,
+               "peak_measured_GBps": float(peak.get("hbm_gbs", 6531.6))}
+    mem_ops["frac_of_measured"] = mem_ops["achieved_GBps"] / mem_ops["peak_measured_GBps"]
     roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
             "frac": achieved / pk, "traffic": traffic,
             "kernel": "conv_tc_kernel (all %d conv launches of one step)" % len(conv_idx),
             "conv_ms_per_step": conv_s * 1e3, "peak_source": f"{peak_kind} bf16 sustained"}
+    roof["memory_bound_ops"] = mem_ops
     return roof, conv_s / float(np.median(step_times))
 
 

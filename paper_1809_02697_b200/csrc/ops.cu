@@ -167,7 +167,33 @@ __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, in
       const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
       const T* base = src + gq * V;
       uint4 res;
-      if constexpr (IS_MAX && sizeof(T) == 2) {
+      if constexpr (IS_MAX && sizeof(T) == 2 && WIN > 0) {
+        // max pooling: an out-of-bounds tap is clamped to the nearest row /
+        // column, which always lies inside the same window (pad < win), so
+        // the maximum is unchanged and all WIN*WIN loads are issued
+        // unconditionally before the reduction
+        int rows[WIN], cols[WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r) rows[r] = min(max(ih0 + r, 0), H - 1) * W;
+#pragma unroll
+        for (int q = 0; q < WIN; ++q) cols[q] = min(max(iw0 + q, 0), W - 1);
+        uint4 raw[WIN * WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r)
+#pragma unroll
+          for (int q = 0; q < WIN; ++q)
+            raw[r * WIN + q] = __ldg(reinterpret_cast<const uint4*>(base + (rows[r] + cols[q]) * x));
+        __nv_bfloat162 m[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) m[k] = reinterpret_cast<const __nv_bfloat162*>(&raw[0])[k];
+#pragma unroll
+        for (int t2 = 1; t2 < WIN * WIN; ++t2)
+#pragma unroll
+          for (int k = 0; k < NP; ++k)
+            m[k] = __hmax2(m[k], reinterpret_cast<const __nv_bfloat162*>(&raw[t2])[k]);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) reinterpret_cast<__nv_bfloat162*>(&res)[k] = m[k];
+      } else if constexpr (IS_MAX && sizeof(T) == 2) {
         __nv_bfloat162 m[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) m[k] = __bfloat162bfloat162(__float2bfloat16(-INFINITY));

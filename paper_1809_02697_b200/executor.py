@@ -107,6 +107,17 @@ def _plan_arena(vals: list[_Val], align: int = 256) -> int:
     return max((p.offset + p.nbytes for p in placed), default=0)
 
 
+def _nb(t) -> int:
+    """Bytes of a device tensor."""
+    return int(t.numel()) * t.element_size()
+
+
+def _vb(v) -> int:
+    """Bytes of a value's own elements (its window, for concat windows)."""
+    import torch
+    return int(np.prod(v.shape)) * torch.empty((), dtype=v.dtype).element_size()
+
+
 class DeviceProgram:
     """One compiled forward of ``plan`` on ``device`` in ``mode``."""
 
@@ -127,6 +138,7 @@ class DeviceProgram:
         self.launches: list = []        # zero-arg callables, in order
         self.tc_params: list = []       # tensor-core conv params (split-K workspace)
         self.launch_names: list[str] = []
+        self.launch_bytes: list[int] = []
         self.vals: dict[int, _Val] = {}
         self.weights: list = []         # device tensors kept alive
         self.graph_exec = None
@@ -453,9 +465,12 @@ class DeviceProgram:
                 v.tensor = base.tensor.reshape(v.shape)
 
     # -- launches --------------------------------------------------------------
-    def _emit(self, name, fn):
+    def _emit(self, name, fn, nbytes: int = 0):
+        """Append a launch; ``nbytes`` = its algorithmic HBM bytes (memory-
+        bound operators: what the kernel must read and write once)."""
         self.launches.append(fn)
         self.launch_names.append(name)
+        self.launch_bytes.append(int(nbytes))
 
     def _upload(self, arr, dtype=None):
         import torch
@@ -636,7 +651,7 @@ class DeviceProgram:
         self._emit("convert", lambda: L.call(
             "neo_layout_transform", D.dtype_code(src), D.dtype_code(dst), src.data_ptr(),
             dst.data_ptr(), 1, numel, 1, 1, L.NCHW_TAG, 1, L.NCHW_TAG, 1, 0,
-            D.stream_handle(self.stream)))
+            D.stream_handle(self.stream)), _nb(src) + _nb(dst))
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
@@ -647,7 +662,7 @@ class DeviceProgram:
             s_t, d_t = src.tensor, out.tensor
             self._emit(f"stemfold{node.id}", lambda: D.stem_fold(
                 s_t, d_t, f["n"], f["C"], f["h"], f["w"], f["S"], f["sw"], f["pw"], f["ow"],
-                f["xf"], self.round_flag, self.stream))
+                f["xf"], self.round_flag, self.stream), _nb(s_t) + _nb(d_t))
             return
         n, c, h, w = self.specs[node.inputs[0][0]].logical_nchw
         src_layout = src.layout
@@ -661,7 +676,7 @@ class DeviceProgram:
             flags |= self.round_flag
         s_t, d_t = src.tensor, out.tensor
         self._emit(f"transform{node.id}", lambda: D.layout_transform(
-            s_t, d_t, n, c, h, w, s_tag, d_tag, flags, self.stream))
+            s_t, d_t, n, c, h, w, s_tag, d_tag, flags, self.stream), _nb(s_t) + _nb(d_t))
 
     def _geom(self, v: _Val):
         """(n, channel blocks, h, w, lanes) of a feature-map value."""
@@ -681,28 +696,30 @@ class DeviceProgram:
         win, st, pad = node.attrs["window"], node.attrs["stride"], node.attrs.get("pad", 0)
         flags = self.round_flag if src.layout.tag == "NCHWc" else 0
         s_t, d_t = src.tensor, out.tensor
+        nb = _vb(src) + _vb(out)
         if src.win is not None or out.win is not None:
             iw, ow = self._window(src), self._window(out)
             self._emit(f"{mode}pool{node.id}", lambda: D.pool2d_window(
-                s_t, d_t, n, cb, h, w, x, win, st, pad, mode, iw, ow, flags, self.stream))
+                s_t, d_t, n, cb, h, w, x, win, st, pad, mode, iw, ow, flags, self.stream), nb)
             return
         self._emit(f"{mode}pool{node.id}", lambda: D.pool2d(
-            s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream))
+            s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream), nb)
 
     def _bind_eltwise(self, op, a: _Val, b: _Val | None, out: _Val):
         from . import device as D
         n, cb, h, w, x = self._geom(a)
         flags = self.round_flag if a.layout.tag == "NCHWc" else 0
         a_t, b_t, o_t = a.tensor, (b.tensor if b is not None else None), out.tensor
+        nb = _vb(a) + _vb(out) + (_vb(b) if b is not None else 0)
         if b is None and (a.win is not None or out.win is not None):
             aw, ow = self._window(a), self._window(out)
             self._emit(f"eltwise{out.nid}", lambda: D.eltwise_window(
-                op, a_t, o_t, n, cb, h * w, x, aw, ow, None, None, flags, self.stream))
+                op, a_t, o_t, n, cb, h * w, x, aw, ow, None, None, flags, self.stream), nb)
             return
         if (b is not None and b.win is not None) or a.win is not None or out.win is not None:
             raise InputMismatch(f"eltwise {out.nid}: windowed add")
         self._emit(f"eltwise{out.nid}", lambda: D.eltwise(
-            op, a_t, b_t, o_t, n, cb, h * w, x, None, None, flags, self.stream))
+            op, a_t, b_t, o_t, n, cb, h * w, x, None, None, flags, self.stream), nb)
 
     def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
         from . import device as D
@@ -719,13 +736,14 @@ class DeviceProgram:
         op = L.ELT_SCALE_SHIFT_RELU if relu else L.ELT_SCALE_SHIFT
         flags = self.round_flag if src.layout.tag == "NCHWc" else 0
         a_t, o_t = src.tensor, out.tensor
+        nb = _vb(src) + _vb(out)
         if src.win is not None or out.win is not None:
             aw, ow = self._window(src), self._window(out)
             self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise_window(
-                op, a_t, o_t, n, cb, h * w, x, aw, ow, t_scale, t_shift, flags, self.stream))
+                op, a_t, o_t, n, cb, h * w, x, aw, ow, t_scale, t_shift, flags, self.stream), nb)
             return
         self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise(
-            op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream))
+            op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream), nb)
 
     def _bind_concat(self, node, ins, out: _Val):
         from . import device as D
@@ -749,7 +767,8 @@ class DeviceProgram:
                     raise InputMismatch(f"concat {node.id}: input {src} is a foreign window")
                 s_t, d_t = v.tensor, dst.tensor
                 self._emit(f"concat{node.id}", lambda s_t=s_t, d_t=d_t, chunk=chunk, off=off:
-                           D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream))
+                           D.concat_copy(s_t, d_t, outer, chunk, row, off, self.stream),
+                           2 * _nb(s_t))
             off += chunk
 
     def _bind_dense(self, node, src: _Val, out: _Val, relu: bool = False):
@@ -779,7 +798,8 @@ class DeviceProgram:
                               flags=self.round_flag if o_t.dtype == torch.float32 and
                               self._feeds_tc_dense(out.nid) else 0, tile=tile)
             self.tc_params.append(p)
-            self._emit(f"dense{node.id}_tc", lambda p=p: D.conv2d(p, self.stream))
+            self._emit(f"dense{node.id}_tc", lambda p=p: D.conv2d(p, self.stream),
+                       _nb(wd) + _nb(src.tensor) + _nb(o_t))
             return
         a_t = self._as_f32(src) if self.mode != "bf16" or src.tensor.dtype != torch.bfloat16 \
             else src.tensor
@@ -787,11 +807,13 @@ class DeviceProgram:
         o_t = out.tensor if out.tensor.dtype == torch.float32 else torch.empty(
             out.shape, dtype=torch.float32, device=self.device)
         self._emit(f"dense{node.id}", lambda: D.dense(a_t, w_t, b_t, o_t, n, width, units,
-                                                      self.stream))
+                                                      self.stream),
+                   _nb(w_t) + _nb(a_t) + _nb(o_t))
         if relu:
             from . import _lib as L2
             self._emit(f"relu{out.nid}", lambda: D.eltwise(
-                L2.ELT_RELU, o_t, None, o_t, 1, 1, 1, o_t.numel(), 1, 0, self.stream))
+                L2.ELT_RELU, o_t, None, o_t, 1, 1, 1, o_t.numel(), 1, 0, self.stream),
+                2 * _nb(o_t))
         if o_t is not out.tensor:
             self.weights.append(o_t)
             self._emit_convert(o_t, out.tensor)
@@ -802,7 +824,8 @@ class DeviceProgram:
         rows = int(np.prod(src.shape[:-1]))
         a_t = self._as_f32(src)
         o_t = out.tensor
-        self._emit(f"softmax{out.nid}", lambda: D.softmax(a_t, o_t, rows, cols, self.stream))
+        self._emit(f"softmax{out.nid}", lambda: D.softmax(a_t, o_t, rows, cols, self.stream),
+                   _nb(a_t) + _nb(o_t))
 
     # -- running -----------------------------------------------------------------
     def input_names(self) -> list[str]:
