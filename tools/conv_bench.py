@@ -23,6 +23,12 @@ def main():
     ap.add_argument("--k", type=int, default=256)
     ap.add_argument("--hw", type=int, default=56)
     ap.add_argument("--r", type=int, default=1)
+    ap.add_argument("--s", type=int, default=0, help="kernel width (default = r)")
+    ap.add_argument("--h", type=int, default=0, help="input height (default = hw)")
+    ap.add_argument("--w", type=int, default=0, help="input width (default = hw)")
+    ap.add_argument("--stride-w", type=int, default=0)
+    ap.add_argument("--pad-h", type=int, default=-1)
+    ap.add_argument("--pad-w", type=int, default=-1)
     ap.add_argument("--stride", type=int, default=1)
     ap.add_argument("--x", type=int, default=64)
     ap.add_argument("--y", type=int, default=64)
@@ -43,22 +49,29 @@ def main():
     act = torch.bfloat16 if args.mode == "bf16" else torch.float32
     lmode = L.MODE_BF16 if args.mode == "bf16" else L.MODE_TF32
     n, c, k, hw, r, st = args.n, args.c, args.k, args.hw, args.r, args.stride
-    pad = r // 2
-    oh = (hw + 2 * pad - r) // st + 1
-    x = torch.randn((n, c // args.x, hw, hw, args.x), device=dev).to(act)
-    w = torch.randn((k, c, r, r), device=dev) * 0.05
-    wd = D.pack_weights_umma(w, args.x, lmode)
-    out = torch.empty((n, k // args.y, oh, oh, args.y), dtype=act, device=dev)
+    s_ = args.s or r
+    H, W = args.h or hw, args.w or hw
+    sw = args.stride_w or st
+    ph = args.pad_h if args.pad_h >= 0 else r // 2
+    pw = args.pad_w if args.pad_w >= 0 else s_ // 2
+    oh = (H + 2 * ph - r) // st + 1
+    ow = (W + 2 * pw - s_) // sw + 1
+    x = torch.randn((n, -(-c // args.x), H, W, args.x), device=dev).to(act)
+    w = torch.randn((k, c, r, s_), device=dev) * 0.05
+    wd = D.pack_weights_umma(w, args.x, lmode, pad_channels=c % args.x != 0)
+    out = torch.empty((n, k // args.y, oh, ow, args.y), dtype=act, device=dev)
     res = torch.randn_like(out) if args.res else None
     bias = torch.randn(k, device=dev)
-    flops = 2 * n * k * c * r * r * oh * oh
+    flops = 2 * n * k * c * r * s_ * oh * ow
     byts = (x.numel() + out.numel() * (2 if args.res else 1)) * x.element_size()
 
-    hh, ww = (1, hw * hw) if args.flat else (hw, hw)
+    hh, ww = (1, H * W) if args.flat else (H, W)
 
     def run(tile):
-        p = D.conv_params(lmode, x, wd, out, n, c, hh, ww, k, r, r, (st, st), (pad, pad), args.x,
-                          args.y, bias=bias, residual=res, relu=True, tile=tile)
+        from paper_1809_02697_b200 import _lib as L2
+        p = D.conv_params(lmode, x, wd, out, n, c, hh, ww, k, r, s_, (st, sw), (ph, pw), args.x,
+                          args.y, bias=bias, residual=res, relu=True, tile=tile,
+                          flags=L2.FLAG_PAD_CHANNELS if c % args.x else 0)
         cfg = D.default_tiles(p)
         ws = torch.zeros(max(D.conv_workspace_bytes(p), 4) // 4, device=dev)
         D.set_workspace(p, ws)
@@ -83,11 +96,10 @@ def main():
 
     tiles = [json.loads(args.tile) if args.tile else None]
     if args.sweep:
-        tiles = [None]
-        for tn, g, stg in itertools.product((64, 128, 256), (1, 2), (2, 3, 4, 6)):
-            if tn > -(-k // 16) * 16:
-                continue
-            tiles.append({"tile_n": tn, "slices_per_stage": g, "stages": stg})
+        from paper_1809_02697_b200.kernels import ConvWorkload
+        from paper_1809_02697_b200.tuning import tile_variants
+        wl = ConvWorkload(c, k, H, W, r, s_, (st, sw), (ph, pw))
+        tiles = [None] + [t for t in tile_variants(wl, args.mode, n, pair=True) if t]
     for tile in tiles:
         try:
             us, cfg = run(tile)
