@@ -819,7 +819,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           else mbar_arrive(tempty_bar(acc));
         }
     }
-    if (leader) bulk_wait_all();
+    // the staging slots must outlive the stores' reads; the writes themselves
+    // complete with the grid (dependent kernels wait on grid completion)
+    if (leader) bulk_wait_read<0>();
     if (leader) TRACE(64, 0);
   }
 
