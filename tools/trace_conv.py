@@ -56,9 +56,11 @@ def main():
                 line.append(f"{NAMES[ev]}={by[(ev, t)][-1] / 1000:.2f}us")
         print(" ".join(line))
     mma = sorted(v for (ev, t), vs in by.items() if ev == 12 for v in vs)
-    print(f"mma full-waits: {len(mma)} first {mma[0] / 1000:.2f}us last {mma[-1] / 1000:.2f}us")
+    if mma:
+        print(f"mma full-waits: {len(mma)} first {mma[0] / 1000:.2f}us last {mma[-1] / 1000:.2f}us")
     prod = sorted(v for (ev, t), vs in by.items() if ev == 2 for v in vs)
-    print(f"producer stages: {len(prod)} first {prod[0] / 1000:.2f}us last {prod[-1] / 1000:.2f}us")
+    if prod:
+        print(f"producer stages: {len(prod)} first {prod[0] / 1000:.2f}us last {prod[-1] / 1000:.2f}us")
     chunk = sorted((ns, ev) for ev, tile, ns in recs if 43 <= ev < 56)
     print("chunk events (first 24):", [(ev, round((ns - t0) / 1000, 2)) for ns, ev in chunk[:24]])
     print("all events in time order:")
