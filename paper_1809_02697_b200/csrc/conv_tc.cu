@@ -506,7 +506,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const int ih0 = oh0 * p.stride_h - p.pad_h;
         if (p.halo) {
           for (int ks = ks0; ks < ks1; ++ks) {
+            TRACE(1, t);
             mbar_wait(empty_bar(stage), phase ^ 1u);
+            TRACE(2, t);
             const uint32_t fb = fbar_base + 8u * stage;
             if (leader_cta) mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
             const uint32_t a_dst = sA + stage * p.a_stage;

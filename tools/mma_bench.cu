@@ -31,12 +31,14 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n, int iters, int kstri
     const uint32_t idesc = umma_idesc(1u, 128, n);
     const uint64_t ad0 = umma_smem_desc(sA, 16, 1024, 2), bd0 = umma_smem_desc(sB, 16, 1024, 2);
     const long long t0 = clock64();
-    if (nacc == 0) {
-      // unrolled: constant descriptor offsets, no per-MMA register work
+    if (nacc <= 0) {
+      // unrolled: constant descriptor offsets, no per-MMA register work;
+      // nacc < 0: A view shifted by -nacc 128-byte rows (halo taps)
+      const uint64_t ash = ad0 + (uint64_t)(-nacc * 8);
       for (int i = 0; i < iters; i += 8) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          umma_ss<false>(tmem, ad0 + (uint64_t)((j & 3) * 2), bd0 + (uint64_t)((j & 3) * 2), idesc,
+          umma_ss<false>(tmem, ash + (uint64_t)((j & 3) * 2), bd0 + (uint64_t)((j & 3) * 2), idesc,
                          1u);
       }
     } else {
@@ -63,16 +65,16 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
   cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  for (int nacc : {0, 1}) {
+  for (int nacc : {0, -1, -2, -4, -8}) {
     for (int n : {32, 64, 128, 256}) {
-      if (n * nacc > 512) continue;
+      if (n > 256) continue;
       const int iters = 4096, grid = 1;
       mma_kernel<<<grid, 128, 170 * 1024>>>(n, iters, 4, nacc, d);
       mma_kernel<<<grid, 128, 170 * 1024>>>(n, iters, 4, nacc, d);
       cudaDeviceSynchronize();
       unsigned long long h[1];
       cudaMemcpy(h, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-      printf("accumulators %d N=%3d: %7.1f cycles/MMA (ideal %5.1f at 4096 MAC/clk)  %s\n", nacc,
+      printf("A row shift %d N=%3d: %7.1f cycles/MMA (ideal %5.1f at 4096 MAC/clk)  %s\n", -nacc,
              n, (double)h[0] / iters, 128.0 * n * 16 / 4096, cudaGetErrorString(cudaGetLastError()));
     }
   }

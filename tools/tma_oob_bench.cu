@@ -11,6 +11,8 @@
 
 struct Args {
   CUtensorMap map;
+  CUtensorMap mapB;     // conv-like weight box (x, K, Cb, taps)
+  int withB, b_bytes;
   int iters, stages, box_bytes, off, N, Cb;
   int rank, rows_per_box, total_rows;   // rank 2/3: flat views
 };
@@ -18,7 +20,7 @@ struct Args {
 __global__ void __launch_bounds__(64, 1) k5(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
-  const uint32_t stage_bytes = (a.box_bytes + 1023) & ~1023;
+  const uint32_t stage_bytes = ((a.box_bytes + 1023) & ~1023) + (a.withB ? ((a.b_bytes + 1023) & ~1023) : 0);
   const uint32_t bars = base + a.stages * stage_bytes;
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 128u + 8u * s; };
@@ -36,7 +38,10 @@ __global__ void __launch_bounds__(64, 1) k5(const __grid_constant__ Args a) {
     int cb = 0, n = blockIdx.x % a.N;
     for (int it = 0; it < a.iters; ++it) {
       mbar_wait(empty(stage), phase ^ 1u);
-      mbar_arrive_expect_tx(full(stage), a.box_bytes);
+      mbar_arrive_expect_tx(full(stage), a.box_bytes + (a.withB ? a.b_bytes : 0));
+      if (a.withB)
+        tma_load_4d(base + stage * stage_bytes + ((a.box_bytes + 1023) & ~1023), &a.mapB,
+                    full(stage), 0, 0, cb, 0);
       if (a.rank == 5) {
         tma_load_5d(base + stage * stage_bytes, &a.map, full(stage), 0, a.off, a.off, cb, n);
       } else if (a.rank == 3) {
@@ -172,6 +177,54 @@ int main() {
     printf("%-32s grid %3d: %7.1f ns per box, %6.1f GB/s per CTA  %s\n", c.name, c.grid,
            ms * 1e6 / a.iters, (double)a.box_bytes * a.iters / (ms * 1e-3) / 1e9,
            cudaGetErrorString(cudaGetLastError()));
+  }
+  // the conv's halo stage: one 5-D band box + one 4-D weight box (3 taps x
+  // 128 rows) per stage, issued by one thread, 2 or 4 stages in flight
+  void* wsrc = nullptr;
+  cudaMalloc(&wsrc, 9ull * 4 * 256 * 128);
+  for (int stages : {2, 4}) {
+    for (int grid : {1, 148}) {
+      Args a{};
+      a.iters = 2048;
+      a.stages = stages;
+      a.N = N;
+      a.Cb = Cb;
+      a.rank = 5;
+      a.off = -1;
+      a.withB = 1;
+      const int H = 14, W = 14, bh = 8, bw = 16;
+      a.box_bytes = bh * bw * x * 2;
+      a.b_bytes = 3 * 128 * 128;
+      cuuint64_t dims[5] = {(cuuint64_t)x, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)Cb,
+                            (cuuint64_t)N};
+      cuuint64_t strides[4] = {(cuuint64_t)x * 2, (cuuint64_t)W * x * 2,
+                               (cuuint64_t)H * W * x * 2, (cuuint64_t)Cb * H * W * x * 2};
+      cuuint32_t box[5] = {(cuuint32_t)x, (cuuint32_t)bw, (cuuint32_t)bh, 1, 1};
+      cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+      encode(&a.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, src, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      cuuint64_t bd[4] = {(cuuint64_t)x, 256, (cuuint64_t)Cb, 9};
+      cuuint64_t bs[3] = {(cuuint64_t)x * 2, 256ull * x * 2, 256ull * Cb * x * 2};
+      cuuint32_t bb[4] = {(cuuint32_t)x, 128, 1, 3};
+      cuuint32_t be[4] = {1, 1, 1, 1};
+      encode(&a.mapB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, wsrc, bd, bs, bb, be,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const size_t smem = a.stages * (((a.box_bytes + 1023) & ~1023) + ((a.b_bytes + 1023) & ~1023)) + 2048;
+      k5<<<grid, 64, smem>>>(a);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      k5<<<grid, 64, smem>>>(a);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("conv halo stage (A 16KB + B 48KB), %d stages, grid %3d: %7.1f ns per stage  %s\n",
+             stages, grid, ms * 1e6 / a.iters, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
