@@ -1150,7 +1150,12 @@ int neo_conv_default_tiles(neo_conv_params* p) {
       if (fit >= std::min<int64_t>(want, 3) || g <= gmin || p->slices_per_stage > 0) {
         p->slices_per_stage = g;
         if (p->stages <= 0) {
-          const int64_t room = fit >= 2 ? fit : budget / stage;   // else shrink staging
+          // else shrink the staging, but keep one slot per epilogue group so
+          // the TMA-store epilogue survives (the direct path is far slower)
+          const int rbo = epi_rowb_out(p, p->tile_n);
+          const int64_t min_staging =
+              rbo ? (int64_t)epi_groups(p, p->tile_n) * kTileM * rbo : 0;
+          const int64_t room = fit >= 2 ? fit : (budget - min_staging) / stage;
           p->stages = (int)std::max<int64_t>(2, std::min<int64_t>(want, room));
         }
         break;

@@ -24,13 +24,14 @@ def main():
     ap.add_argument("--db", default=None)
     ap.add_argument("--repeats", type=int, default=10)
     ap.add_argument("--refresh", action="store_true", help="re-measure existing entries")
+    ap.add_argument("--pair", action="store_true", help="also time CTA-pair (cta_group::2) tiles")
     args = ap.parse_args()
     from paper_1809_02697_b200 import ScheduleDb, build_model
     from paper_1809_02697_b200.tuning import DEFAULT_DB, tune_tiles
     db = ScheduleDb(args.db or DEFAULT_DB)
     g = build_model(args.model, batch=args.batch)
     t0 = time.time()
-    best = tune_tiles(g, db, args.mode, args.batch, repeats=args.repeats, refresh=args.refresh)
+    best = tune_tiles(g, db, args.mode, args.batch, repeats=args.repeats, refresh=args.refresh, pair=args.pair)
     print(f"tuned {len(best)} convs of {args.model} b{args.batch} {args.mode} in "
           f"{time.time() - t0:.1f}s -> {db.path}")
 
