@@ -155,6 +155,13 @@ typedef struct neo_conv_params {
    * tile, each holding half of the A rows and half of the weight rows, so a
    * weight byte serves 256 pixels (0 = automatic, 1 = off, 2 = on). */
   int cta_pair;
+  /* BN-ReLU prologue (DenseNet pre-activation, reference executor.py:174-181
+   * + ReLU): with pro_scale != NULL the conv consumes
+   * relu?(x * pro_scale[c] + pro_shift[c]) instead of x, computed on the
+   * tiles in shared memory (unpadded 1x1 convs, TF32/BF16 modes). */
+  const float* pro_scale;
+  const float* pro_shift;
+  int pro_relu;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);

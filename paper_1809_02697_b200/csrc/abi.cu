@@ -54,7 +54,10 @@ int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream) {
                 p->oc_bn, (long long)p->k);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (p->mode) {
-    case NEO_MODE_FP32: return neo_conv_simt_launch(p, st);
+    case NEO_MODE_FP32:
+      NEO_CHECK_ARG(p->pro_scale == nullptr, NEO_ERR_UNSUPPORTED,
+                    "the BN-ReLU prologue runs on the tensor-core path only");
+      return neo_conv_simt_launch(p, st);
     case NEO_MODE_TF32:
     case NEO_MODE_BF16: return neo_conv_tc_launch(p, st);
     default: neo_set_error("unknown conv mode %d", p->mode); return NEO_ERR_INVALID_ARG;

@@ -34,6 +34,7 @@ namespace {
 constexpr int kMaxStages = 8;
 constexpr int kThreads = 576;   // warp 0 TMA, warp 1 MMA, warps 2-17 epilogue (2 groups of 8)
 constexpr int kEpiWarps = 16;          // warps 2..17
+constexpr int kProWarps = 8;           // prologue mode: warps 10..17 rewrite A slices
 constexpr int kMaxGroups = 4;          // epilogue groups = TMEM accumulator stages
 constexpr int kTileM = 128;
 #ifdef NEO_TRACE
@@ -91,6 +92,13 @@ struct ConvTCParams {
   // g % tiles_k, M tiles 2 * (g / tiles_k) + rank (a missing odd tile is a
   // dummy: loads out of bounds, stores clipped).
   int pair, tiles_m, num_groups;
+  // BN-ReLU prologue (DenseNet pre-activation fused into a 1x1 conv): warps
+  // 10-17 rewrite every landed activation slice in shared memory as
+  // relu(x * pro_scale[c] + pro_shift[c]) before the MMA may read it (the
+  // MMA waits on xfull barriers); the epilogue keeps warps 2-9
+  const float* pro_scale;
+  const float* pro_shift;
+  int pro, pro_relu;
   float* ws;        // partials
   int* counters;    // per-tile arrival counters (zero between launches)
 };
@@ -432,11 +440,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   auto tempty_bar = [&](int a) { return sBar + 160u + 8u * a; };
   auto res_bar = [&](int g, int b) { return sBar + 192u + 16u * g + 8u * b; };
   const uint32_t tslot = sBar + 256u;
+  auto xfull_bar = [&](int i) { return sBar + 384u + 8u * i; };   // prologue: slice rewritten
   volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 256);
   float* par_gen = reinterpret_cast<float*>(bar_gen + 512);   // ngroups x kParamFloats
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int epi_warps = p.pro ? kEpiWarps - kProWarps : kEpiWarps;   // warps 2 .. 2+epi_warps-1
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const bool leader_cta = rank == 0;
 #ifdef NEO_TRACE
@@ -456,11 +466,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(full_bar(i), 1);
       mbar_init(empty_bar(i), 1);
+      mbar_init(xfull_bar(i), kProWarps);
     }
     for (int a = 0; a < p.ngroups; ++a) {
       mbar_init(tfull_bar(a), 1);
       // pair: the leader's MMA waits for both CTAs' epilogue warps
-      mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * (kEpiWarps / p.ngroups));
+      mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * (epi_warps / p.ngroups));
       mbar_init(res_bar(a, 0), 1);
       mbar_init(res_bar(a, 1), 1);
     }
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.BN;
         for (int ks = ks0; ks < ks1; ++ks) {
-          mbar_wait(full_bar(stage), phase);
+          mbar_wait(p.pro ? xfull_bar(stage) : full_bar(stage), phase);
           TRACE(12, t);
           tc_fence_after();
           const uint32_t a0 = sA + stage * p.a_stage;
@@ -659,11 +670,82 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         TRACE(13, t);
       }
     }
+  } else if (p.pro && warp >= 2 + epi_warps) {
+    // ---------------- prologue warps: walk the stage ring behind the
+    // producer; rewrite each landed slice in place, hand it to the MMA
+    const int ptid = (warp - 2 - epi_warps) * 32 + lane;
+    const int chunks_row = p.rowb / 16;               // 16-byte chunks per row
+    const int per_slice = kTileM * chunks_row;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+      const int u = cta_unit(p, it, rank);
+      if (u < 0) break;
+      const int t = u / p.splits;
+      const int ks0 = (u - t * p.splits) * p.kps;
+      const int ks1 = min(p.kstages, ks0 + p.kps);
+      for (int ks = ks0; ks < ks1; ++ks) {
+        mbar_wait(full_bar(stage), phase);
+        uint8_t* a_gen = gen_base + stage * p.a_stage;
+        for (int g = 0; g < p.G; ++g) {
+          const int sl = ks * p.G + g;                // 1x1: slice = channel block
+          if (sl >= p.nslices) continue;              // padding slice: zeros x zero weights
+          const int cbase = (sl % p.Cb) * (p.rowb / (TF32 ? 4 : 2));
+          uint8_t* slice = a_gen + g * p.a_sub;
+          for (int idx = ptid; idx < per_slice; idx += kProWarps * 32) {
+            const int row = idx / chunks_row, ch = idx - row * chunks_row;
+            uint4* ptr = reinterpret_cast<uint4*>(slice + swz_offset(row, ch, p.rowb));
+            uint4 v = *ptr;
+            if constexpr (TF32) {
+              float* f = reinterpret_cast<float*>(&v);
+              const int c0 = cbase + ch * 4;
+              const float4 sc = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
+              const float4 sh = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
+              const float scv[4] = {sc.x, sc.y, sc.z, sc.w}, shv[4] = {sh.x, sh.y, sh.z, sh.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float y = __fadd_rn(__fmul_rn(f[e], scv[e]), shv[e]);
+                if (p.pro_relu) y = fmaxf(y, 0.f);
+                f[e] = neo_round_tf32(y);
+              }
+            } else {
+              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+              const int c0 = cbase + ch * 8;
+              const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
+              const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0 + 4));
+              const float4 t0 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
+              const float4 t1 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0 + 4));
+              const float scv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              const float shv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x2 = __bfloat1622float2(h[e]);
+                float a = __fadd_rn(__fmul_rn(x2.x, scv[2 * e]), shv[2 * e]);
+                float b = __fadd_rn(__fmul_rn(x2.y, scv[2 * e + 1]), shv[2 * e + 1]);
+                if (p.pro_relu) {
+                  a = fmaxf(a, 0.f);
+                  b = fmaxf(b, 0.f);
+                }
+                h[e] = __floats2bfloat162_rn(a, b);
+              }
+            }
+            *ptr = v;
+          }
+        }
+        fence_proxy_async_smem();      // generic-proxy writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(xfull_bar(stage));
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
   } else {
     // ---------------- epilogue: two groups of 4 warps, group g takes the
     // tiles whose accumulator lives in TMEM stage g (alternate tiles), so
     // both groups drain in parallel with the MMA of the next tile.
-    const int gwarps = kEpiWarps / p.ngroups;      // 8 or 4
+    const int gwarps = epi_warps / p.ngroups;      // 8 or 4 (4 in prologue mode)
     const int gthreads = gwarps * 32;
     const int grp = (warp - 2) / gwarps;
     const int nsub = gwarps / 4;                    // warps per lane quarter: 2 or 1
@@ -995,6 +1077,7 @@ int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
 // parallel hide its latency) when four N tiles fit the 512 TMEM columns,
 // else two (long K loops want the shared memory for pipeline stages)
 static int epi_groups(const neo_conv_params* p, int tile_n) {
+  if (p->pro_scale) return 2;            // prologue mode: 8 epilogue warps, 2 groups
   static const int forced = getenv("NEOB200_EPI_GROUPS") ? atoi(getenv("NEOB200_EPI_GROUPS")) : 0;
   if (forced == 2 || (forced == 4 && tile_n <= 128)) return forced;
   const int64_t slices = p->r * p->s * neo_ceil_div(p->c, std::max(1, p->ic_bn));
@@ -1086,8 +1169,8 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     // short reductions are epilogue-bound: cap at 128 so four epilogue
     // groups (TMEM stages) can drain tiles in parallel
     const int64_t red_slices = p->r * p->s * neo_ceil_div(p->c, std::max(1, p->ic_bn));
-    const int widest = (halo || red_slices <= 8) ? std::min(128, pick_tile_n(p->k))
-                                                 : pick_tile_n(p->k);
+    const int widest = (halo || red_slices <= 8 || p->pro_scale) ? std::min(128, pick_tile_n(p->k))
+                                                                 : pick_tile_n(p->k);
     p->tile_n = widest;
     for (int bn : {256, 128, 64}) {
       if (bn > widest) continue;
@@ -1263,8 +1346,17 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const int64_t nslices = halo ? p->r * Cb : p->r * p->s * Cb;
   const int64_t kstages = neo_ceil_div(nslices, G);
 
+  if (p->pro_scale) {
+    // BN-ReLU prologue: 1x1, unpadded, whole channel blocks, N tile <= 128
+    NEO_CHECK_ARG(p->pro_shift != nullptr, NEO_ERR_INVALID_ARG, "prologue needs scale and shift");
+    NEO_CHECK_ARG(p->r == 1 && p->s == 1 && p->pad_h == 0 && p->pad_w == 0 && p->c % x == 0,
+                  NEO_ERR_UNSUPPORTED,
+                  "BN-ReLU prologue needs an unpadded 1x1 conv over whole channel blocks");
+    NEO_CHECK_ARG(BN <= 128 && p->cta_pair != 2, NEO_ERR_SCHEDULE_INVALID,
+                  "BN-ReLU prologue runs single-CTA tiles with tile_n <= 128 (tile_n=%d)", BN);
+  }
   const int64_t tiles_m_all = neo_ceil_div(OW, BW) * neo_ceil_div(OH, BH) * neo_ceil_div(p->n, BNI);
-  const bool pair = use_pair(p, BN, tiles_m_all);
+  const bool pair = !p->pro_scale && use_pair(p, BN, tiles_m_all);
   NEO_CHECK_ARG(!(p->cta_pair == 2 && !pair), NEO_ERR_SCHEDULE_INVALID,
                 "cta_pair not possible here (split_k=%d, tile_n=%d, %lld M tiles)", p->split_k,
                 BN, (long long)tiles_m_all);
@@ -1399,6 +1491,10 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.relu = p->relu;
   kp.out_f32 = p->out_dtype == NEO_F32;
   kp.round_tf32 = (p->flags & NEO_FLAG_ROUND_TF32) ? 1 : 0;
+  kp.pro = p->pro_scale != nullptr;
+  kp.pro_scale = p->pro_scale;
+  kp.pro_shift = p->pro_shift;
+  kp.pro_relu = p->pro_relu;
 
   // TMA-store epilogue: output / residual tensor maps over (y, OW, OH, Kb_total, N)
   const int rb_out = epi_rowb_out(p, BN);

@@ -95,7 +95,8 @@ def pack_weights_umma(w_kcrs: torch.Tensor, x: int, mode: int, pad_channels: boo
 
 def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 0), ic_bn=1,
                 oc_bn=1, scale=None, shift=None, bias=None, residual=None, relu=False,
-                x_cb=(0, 0), out_cb=(0, 0), res_cb=(0, 0), flags=0, tile=None) -> L.ConvParams:
+                x_cb=(0, 0), out_cb=(0, 0), res_cb=(0, 0), flags=0, tile=None,
+                prologue=None) -> L.ConvParams:
     p = L.ConvParams()
     p.mode = mode
     p.x, p.w, p.out = _ptr(x), _ptr(w), _ptr(out)
@@ -110,6 +111,9 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
     p.res_cb_offset, p.res_cb_total = res_cb
     p.out_dtype = dtype_code(out)
     p.flags = flags
+    if prologue is not None:        # (scale, shift, relu): BN-ReLU on the input
+        p.pro_scale, p.pro_shift = _ptr(prologue[0]), _ptr(prologue[1])
+        p.pro_relu = int(bool(prologue[2]))
     if tile:
         for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
                     "split_k", "cta_pair"):

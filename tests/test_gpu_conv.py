@@ -370,3 +370,53 @@ def test_tc_conv_cta_pair(cuda, case, tile, mode_name):
     got = run_conv(mode, x, wt, st, pd, x_bn, 32, bias=bias, residual=res, relu=True, tile=tile,
                    pad_channels=c < lanes)
     assert oracle.rel_err(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("shape", [(2, 128, 14, 14, 128, 32), (1, 256, 7, 7, 64, 64),
+                                   (3, 64, 9, 11, 48, 16)])
+def test_tc_conv_bn_relu_prologue(cuda, mode_name, shape):
+    """BN-ReLU fused into a 1x1 conv's shared-memory tiles equals the
+    unfused scale-shift-relu launch followed by the conv, bit for bit, and
+    the oracle within accumulation error."""
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    n, c, h, w, k, x_bn = shape
+    if mode_name == "tf32":
+        x_bn = min(x_bn, 32)
+    rng = np.random.default_rng(c + k)
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    act = torch.bfloat16 if mode_name == "bf16" else torch.float32
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, 1, 1)) * np.sqrt(2.0 / c)).astype(np.float32))
+    scale = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    shift = rng.normal(0, 0.3, c).astype(np.float32)
+    dev = torch.device("cuda")
+    xb = torch.from_numpy(pack_nchw(x, x_bn)).to(dev).to(act)
+    sc, sh = torch.from_numpy(scale).to(dev), torch.from_numpy(shift).to(dev)
+    flags = L.FLAG_ROUND_TF32 if mode_name == "tf32" else 0
+    tmp = torch.empty_like(xb)
+    D.eltwise(L.ELT_SCALE_SHIFT_RELU, xb, None, tmp, n, c // x_bn, h * w, x_bn, sc, sh, flags)
+    wd = D.pack_weights_umma(torch.from_numpy(wt).to(dev), x_bn, mode)
+    y = 16
+    out_a = torch.empty((n, k // y, h, w, y), device=dev)
+    out_b = torch.empty_like(out_a)
+    pa = D.conv_params(mode, tmp, wd, out_a, n, c, h, w, k, 1, 1, (1, 1), (0, 0), x_bn, y,
+                       relu=True)
+    pb = D.conv_params(mode, xb, wd, out_b, n, c, h, w, k, 1, 1, (1, 1), (0, 0), x_bn, y,
+                       relu=True, prologue=(sc, sh, True))
+    D.conv2d(pa)
+    D.conv2d(pb)
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, out_b)
+    pre = np.maximum(x * scale[None, :, None, None] + shift[None, :, None, None], 0)
+    ref = oracle.conv2d(rnd(pre.astype(np.float32)), wt, 1, 0, relu=True)
+    assert oracle.rel_err(unpack_nchw(out_b.cpu().numpy()), ref) < 1e-4
+    with pytest.raises(Exception):     # padded / wider kernels are rejected
+        bad = D.conv_params(mode, xb, D.pack_weights_umma(
+            torch.from_numpy(rnd(rng.standard_normal((k, c, 3, 3)).astype(np.float32))).to(dev),
+            x_bn, mode), out_b, n, c, h, w, k, 3, 3, (1, 1), (1, 1), x_bn, y,
+            prologue=(sc, sh, True))
+        D.conv2d(bad)
