@@ -168,6 +168,39 @@ class DeviceProgram:
                         and nid not in g.outputs and nid not in self.keep):
                     self.fused_bn_relu[us[0]] = nid
                     self.skip.add(nid)
+        # BN -> ReLU feeding only the data input of an unpadded 1x1 conv on the
+        # tensor cores can become the conv's shared-memory prologue (DenseNet
+        # pre-activation; neither the BN nor the ReLU value is materialised).
+        # Opt-in (NEOB200_PROLOGUE=1): on B200 the in-smem rewrite sits on the
+        # critical path of every pipeline stage and cost more (DenseNet-201
+        # b32 2.9 -> 5.2 ms) than the HBM-speed scale-shift-relu launches it
+        # removes.
+        self.prologue: dict[int, int] = {}       # conv id -> bn id
+        self.pro_src: dict[int, int] = {}        # relu id -> the BN's input value
+        import os
+        if self.mode in ("bf16", "tf32") and os.environ.get("NEOB200_PROLOGUE"):
+            for relu, bn in list(self.fused_bn_relu.items()):
+                us = self.users[relu]
+                if len(us) != 1 or relu in g.outputs or relu in self.keep:
+                    continue
+                cv = g.nodes[us[0]]
+                if cv.kind != OpKind.Conv2d or cv.inputs[0][0] != relu:
+                    continue
+                if any(s == relu for s, _ in cv.inputs[1:]):
+                    continue
+                wt = g.nodes[cv.inputs[1][0]].attrs["value"]
+                kh, kw = (wt.shape[2], wt.shape[3]) if wt.ndim == 4 else (wt.shape[2], wt.shape[3])
+                spec = self.specs[relu]
+                if (kh, kw) != (1, 1) or hw_pair(cv.attrs["pad"]) != (0, 0):
+                    continue
+                if spec.layout.tag != "NCHWc" or not tc_legal_block(spec.layout.x, self.mode):
+                    continue
+                if spec.logical_nchw[1] % spec.layout.x:
+                    continue
+                self.prologue[cv.id] = bn
+                self.pro_src[relu] = g.nodes[bn].inputs[0][0]
+                self.skip.add(relu)
+                del self.fused_bn_relu[relu]
         # Dense layers run as 1x1 tensor-core convs over their row-major input
         # ((N, F) == NCHW[x]c with H = W = 1); a Dense whose only consumer is a
         # ReLU writes the ReLU's value with the relu fused into the epilogue.
@@ -244,7 +277,7 @@ class DeviceProgram:
         for nid in order:
             node = self.g.nodes[nid]
             for src, _ in node.inputs:
-                tgt = self._storage(src)
+                tgt = self._storage(self.pro_src.get(src, src))
                 if tgt is not None:
                     tgt.last = max(tgt.last, self.step[nid])
             fused_src = self.fused_bn_relu.get(nid, self.fused_dense_relu.get(nid))
@@ -548,7 +581,8 @@ class DeviceProgram:
         from . import _lib as L
         from . import device as D
         g = self.g
-        data = self.vals[node.inputs[0][0]]
+        data_id = self.pro_src.get(node.inputs[0][0], node.inputs[0][0])
+        data = self.vals[data_id]
         wv = g.nodes[node.inputs[1][0]].attrs["value"]
         epi = dict(node.attrs.get("epilogue") or {})
         extra = 1 if epi.get("residual") else 0
@@ -559,7 +593,7 @@ class DeviceProgram:
             bias = b if bias is None else bias + b
         sh, sw = hw_pair(node.attrs["stride"])
         ph, pw = hw_pair(node.attrs["pad"])
-        dspec = self.specs[node.inputs[0][0]]
+        dspec = self.specs[data_id]
         n, c, h, w = dspec.logical_nchw
         if wv.ndim == 6:
             kcrs = host_unpack_kcrs(wv)
@@ -603,11 +637,17 @@ class DeviceProgram:
             if res is not None:
                 r_t = res.tensor if res.tensor.dtype == o_t.dtype else self._as_f32(res)
             flags = self.round_flag | (L.FLAG_PAD_CHANNELS if pad_c else 0)
+            pro = None
+            if node.id in self.prologue:      # BN -> ReLU applied on the smem tiles
+                ps, pt = self._bn_scale_shift(g.nodes[self.prologue[node.id]])
+                pro = (self._upload(ps), self._upload(pt), True)
+                tile["tile_n"] = min(tile.get("tile_n") or 0, 128)
+                tile["cta_pair"] = 0
             p = D.conv_params(mode, x_t, wd, o_t, n, c, h, w, k, r, s, (sh, sw), (ph, pw),
                               ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t,
                               bool(epi.get("relu")), x_cb=self._window(data),
                               out_cb=self._window(out), flags=flags,
-                              tile=tile if any(tile.values()) else None)
+                              tile=tile if any(tile.values()) else None, prologue=pro)
             self.tc_params.append(p)
             self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream))
             return
@@ -721,9 +761,8 @@ class DeviceProgram:
         self._emit(f"eltwise{out.nid}", lambda: D.eltwise(
             op, a_t, b_t, o_t, n, cb, h * w, x, None, None, flags, self.stream), nb)
 
-    def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
-        from . import device as D
-        from . import _lib as L
+    def _bn_scale_shift(self, node):
+        """Per-channel (scale, shift) of a standalone BatchNorm."""
         if len(node.inputs) == 5:   # unfolded BN (executor.py:174-178, f32 arithmetic)
             gamma, beta, mean, var = (np.asarray(self.g.nodes[s].attrs["value"], np.float32)
                                       for s, _ in node.inputs[1:])
@@ -731,6 +770,12 @@ class DeviceProgram:
             shift = beta - mean * scale
         else:
             scale, shift = node.attrs["scale"], node.attrs["shift"]
+        return np.asarray(scale, np.float32), np.asarray(shift, np.float32)
+
+    def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
+        from . import device as D
+        from . import _lib as L
+        scale, shift = self._bn_scale_shift(node)
         t_scale, t_shift = self._upload(scale), self._upload(shift)
         n, cb, h, w, x = self._geom(src)
         op = L.ELT_SCALE_SHIFT_RELU if relu else L.ELT_SCALE_SHIFT

@@ -149,3 +149,21 @@ def test_ssd_heads(cuda, mode, tol):
     for a, b in zip(got, ref):
         assert a.shape == b.shape
         assert oracle.rel_err(a, b) < tol
+
+
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_densenet_bn_relu_prologue_fusion(cuda, mode, monkeypatch):
+    """Opt-in executor fusion of DenseNet's pre-activation BN-ReLU into the
+    following 1x1 conv (NEOB200_PROLOGUE=1): fewer launches, same logits."""
+    from paper_1809_02697_b200 import DeviceProgram, ExecutablePlan, compile_graph, model_input
+    from paper_1809_02697_b200.models import densenet
+    g = densenet(blocks=(3, 4), growth=32, batch=2, image=64, num_classes=10, softmax=False)
+    feeds = model_input(g, seed=1)
+    ref = oracle.execute_reference(g, feeds)
+    plain = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode=mode)), 0, mode)
+    monkeypatch.setenv("NEOB200_PROLOGUE", "1")
+    fused = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode=mode)), 0, mode)
+    assert fused.prologue and len(fused.launches) < len(plain.launches)
+    a, b = plain.run(feeds)[0], fused.run(feeds)[0]
+    assert np.array_equal(a, b)
+    assert oracle.rel_err(b, ref[0]) < TOL[mode]
