@@ -162,6 +162,12 @@ typedef struct neo_conv_params {
   const float* pro_scale;
   const float* pro_shift;
   int pro_relu;
+  /* weight-stationary tiles: each CTA keeps the whole weight image of its N
+   * block in shared memory and streams only activations (stride-1 KxK convs
+   * then load one input band per channel block for all R*S taps)
+   * (0 = automatic: when it fits beside >= 3 activation stages, 1 = off,
+   * 2 = on). */
+  int weight_stationary;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);

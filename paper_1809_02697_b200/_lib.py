@@ -66,6 +66,7 @@ class ConvParams(ctypes.Structure):
         ("split_k", _c_int), ("workspace", _c_vp), ("workspace_bytes", _c_i64),
         ("cta_pair", _c_int),
         ("pro_scale", _c_vp), ("pro_shift", _c_vp), ("pro_relu", _c_int),
+        ("weight_stationary", _c_int),
     ]
 
 

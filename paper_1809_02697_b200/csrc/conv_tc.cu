@@ -99,6 +99,15 @@ struct ConvTCParams {
   const float* pro_scale;
   const float* pro_shift;
   int pro, pro_relu;
+  // weight-stationary: every CTA's tiles share one N block (grid % tiles_k
+  // == 0), whose whole weight image (b_region bytes) is loaded into shared
+  // memory once; the stage ring then carries only activations.  Halo tiles
+  // load one band per channel block covering all R rows (kernel row r = the
+  // band view shifted by r*BW rows), so a stage feeds R*S taps.
+  int wst;
+  uint32_t b_region;
+  int dbg;          // NEOB200_DBG timing experiments (1: no epilogue work, 2: no A loads,
+                    // 8: per-CTA MMA-loop clocks -> neo_dbg_clk)
   float* ws;        // partials
   int* counters;    // per-tile arrival counters (zero between launches)
 };
@@ -259,29 +268,42 @@ __device__ __forceinline__ void load_par16(const float* par, int col, float (&ds
 // One output channel block (y columns) of one pixel row: TMEM -> registers ->
 // epilogue -> swizzled smem row (which already holds the residual block when
 // HAS_RES).  OUT_F32 selects f32 vs bf16 storage.
-template <bool OUT_F32, bool HAS_RES>
+template <bool OUT_F32, bool HAS_RES, bool AFFINE>
 __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int col0,
                                               int m, uint8_t* sbuf_gen, const float* par,
                                               float relu_floor, bool round, int c_begin,
                                               int c_step) {
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
-#pragma unroll 1
-  for (int c = c_begin; c < nchunk; c += c_step) {
-    uint32_t v[16];
-    tmem_ld16(tcol + c * 16, v);
-    float sc[16], sh[16], bi[16];
+  // one chunk: 16 accumulator columns of row m -> scale/shift/bias
+  // (+ residual from the slot) -> relu -> the swizzled staging slot
+  auto finish = [&](const uint32_t (&v)[16], int c) {
     const int col = col0 + c * 16;
-    load_par16(par, col, sc);
-    load_par16(par + 256, col, sh);
-    load_par16(par + 512, col, bi);
-    tmem_ld_wait();
-    float f[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      f[j] = fmaf(__uint_as_float(v[j]), sc[j], sh[j]) + bi[j];
+    constexpr int kPer = 16 / kChunks16;   // values per 16-byte staging piece
 #pragma unroll
     for (int q = 0; q < kChunks16; ++q) {
+      // parameters of this piece only (keeps the live register set small)
+      float f[kPer];
+#pragma unroll
+      for (int j4 = 0; j4 < kPer / 4; ++j4) {
+        const int cc = col + q * kPer + 4 * j4;
+        const float4 bi = *reinterpret_cast<const float4*>(par + 512 + cc);
+        const float* vv = reinterpret_cast<const float*>(v) + q * kPer + 4 * j4;
+        if constexpr (AFFINE) {
+          const float4 sc = *reinterpret_cast<const float4*>(par + cc);
+          const float4 sh = *reinterpret_cast<const float4*>(par + 256 + cc);
+          f[4 * j4 + 0] = fmaf(vv[0], sc.x, sh.x) + bi.x;
+          f[4 * j4 + 1] = fmaf(vv[1], sc.y, sh.y) + bi.y;
+          f[4 * j4 + 2] = fmaf(vv[2], sc.z, sh.z) + bi.z;
+          f[4 * j4 + 3] = fmaf(vv[3], sc.w, sh.w) + bi.w;
+        } else {
+          // identity scale/shift: fma(v, 1, 0) == v, so this is the same value
+          f[4 * j4 + 0] = vv[0] + bi.x;
+          f[4 * j4 + 1] = vv[1] + bi.y;
+          f[4 * j4 + 2] = vv[2] + bi.z;
+          f[4 * j4 + 3] = vv[3] + bi.w;
+        }
+      }
       const uint32_t off = swz_offset(m, c * kChunks16 + q, p.rowb_out);
       uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
       if constexpr (OUT_F32) {
@@ -290,7 +312,7 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         const float r4[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float t = f[4 * q + j];
+          float t = f[j];
           if constexpr (HAS_RES) t += r4[j];
           t = fmaxf(t, relu_floor);
           o[j] = round ? neo_round_tf32(t) : t;
@@ -304,17 +326,31 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float a = f[8 * q + 2 * j], b = f[8 * q + 2 * j + 1];
+          float a = f[2 * j], b = f[2 * j + 1];
           if constexpr (HAS_RES) {
             const float2 t = __bfloat1622float2(r2[j]);
             a += t.x;
             b += t.y;
           }
-          h2[j] = __floats2bfloat162_rn(fmaxf(a, relu_floor), fmaxf(b, relu_floor));
+          // relu fused into the conversion (max(v, 0) then round == round
+          // then clamp: rounding keeps the sign)
+          uint32_t h;
+          if (relu_floor == 0.f)
+            asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+          else
+            asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+          reinterpret_cast<uint32_t*>(h2)[j] = h;
         }
         *slot = packed;
       }
     }
+  };
+#pragma unroll 1
+  for (int c = c_begin; c < nchunk; c += c_step) {
+    uint32_t v[16];
+    tmem_ld16(tcol + c * 16, v);
+    tmem_ld_wait_regs(v);
+    finish(v, c);
   }
 }
 
@@ -392,31 +428,167 @@ __device__ __forceinline__ void trace(int ev, int t, unsigned* cnt) {
 #define TRACE(ev, t)
 #endif
 
+// NEOB200_DBG & 8: per-CTA (MMA-loop cycles, ns) for clock checks
+__device__ unsigned long long g_dbg_clk[8 * 1024];
+
 // MMA issue: descriptors are formed by adding small offsets (in 16-byte
 // units) to per-stage bases, with the K steps of a slice unrolled at compile
 // time, so the single issuing thread spends a handful of uniform-datapath
 // instructions per tcgen05.mma instead of rebuilding descriptors (measured
 // on B200: ~175 cycles per MMA with per-MMA descriptor arithmetic, 64 cycles
 // -- the M=128 N=128 K=16 execution time -- with constant offsets).
+// Descriptor arithmetic stays on the low 32-bit word (14-bit start-address
+// field, byte offset >> 4; smem addresses never carry out of it); the high
+// word (SBO, swizzle, version) is fixed per launch.  The two halves are
+// joined inside the asm, so the issuing loop only does 32-bit uniform adds
+// (64-bit loop-carried descriptors were kept in vector registers and moved
+// to uniform registers before every MMA, stalling the issue).
 template <bool TF32, bool PAIR>
-__device__ __forceinline__ void mma_issue(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
-                                          uint32_t acc) {
-  if constexpr (PAIR) umma_ss2<TF32>(d, ad, bd, idesc, acc);
-  else umma_ss<TF32>(d, ad, bd, idesc, acc);
+__device__ __forceinline__ void mma_issue(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                          uint32_t bhi, uint32_t idesc, uint32_t acc) {
+#define NEO_MMA_LO(CG, KIND)                                                                 \
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 ad, bd;\n\t"                              \
+               "setp.ne.b32 p, %6, 0;\n\t"                                                  \
+               "mov.b64 ad, {%1, %2};\n\t"                                                  \
+               "mov.b64 bd, {%3, %4};\n\t"                                                  \
+               "tcgen05.mma.cta_group::" CG ".kind::" KIND " [%0], ad, bd, %5, p;\n\t}"      \
+               ::"r"(d), "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc)     \
+               : "memory")
+  if constexpr (PAIR) {
+    if constexpr (TF32) NEO_MMA_LO("2", "tf32");
+    else NEO_MMA_LO("2", "f16");
+  } else {
+    if constexpr (TF32) NEO_MMA_LO("1", "tf32");
+    else NEO_MMA_LO("1", "f16");
+  }
+#undef NEO_MMA_LO
 }
-// n slices (slice j at ad + j*ad_step, bd + j*bd_step), KPR K steps of 32
+// n slices (slice j at alo + j*a_step, blo + j*b_step), KPR K steps of 32
 // bytes (+2 in descriptor units) each; acc0 = accumulate flag of the first MMA
 template <bool TF32, bool PAIR, int KPR>
-__device__ __forceinline__ void mma_slices(uint32_t d, uint64_t ad, uint64_t bd, uint32_t ad_step,
-                                           uint32_t bd_step, int n, uint32_t idesc,
-                                           uint32_t acc0) {
+__device__ __forceinline__ void mma_slices(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                           uint32_t bhi, uint32_t a_step, uint32_t b_step, int n,
+                                           uint32_t idesc, uint32_t acc0) {
   for (int j = 0; j < n; ++j) {
 #pragma unroll
     for (int kk = 0; kk < KPR; ++kk)
-      mma_issue<TF32, PAIR>(d, ad + 2u * kk, bd + 2u * kk, idesc, kk == 0 ? acc0 : 1u);
+      mma_issue<TF32, PAIR>(d, alo + 2u * kk, ahi, blo + 2u * kk, bhi, idesc, kk == 0 ? acc0 : 1u);
     acc0 = 1u;
-    ad += ad_step;
-    bd += bd_step;
+    alo += a_step;
+    blo += b_step;
+  }
+}
+
+// MMA issue modes of mma_tiles
+enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst };
+
+// The MMA issuer's tile loop.  Barrier map as in conv_tc_kernel.  Stage and
+// accumulator indices advance by counters; MODE fixes the operand layout:
+//   K4/K2/K1  SWIZZLE_128/64/32 K-major slices (4/2/1 K steps of 16 per slice)
+//   Narrow    16-byte rows, no swizzle, one K step spans two slices (LBO)
+//   Halo      one band per (r, channel block), S taps = shifted views
+//   HaloWst   weight-stationary halo: one band per channel block, R*S taps,
+//             weights at b_sub * (cb*R + r) in the resident image
+template <bool TF32, bool PAIR, int MODE>
+__device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint32_t tmem_base,
+                                          uint32_t sA, uint32_t sB, uint32_t sBar) {
+  const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, PAIR ? 2 * kTileM : kTileM, p.BN);
+  const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst;
+  const uint64_t adesc0 = MODE == kMmaNarrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
+                          : halo_mode        ? umma_smem_desc(sA, 16, 1024, 2)
+                                             : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
+  const uint64_t bdesc0 = MODE == kMmaNarrow ? umma_smem_desc(sB, p.b_sub, 128, 0)
+                          : halo_mode        ? umma_smem_desc(sB, 16, 1024, 2)
+                                             : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
+  const uint32_t a0lo = (uint32_t)adesc0, ahi = (uint32_t)(adesc0 >> 32);
+  const uint32_t b0lo = (uint32_t)bdesc0, bhi = (uint32_t)(bdesc0 >> 32);
+  const uint32_t a_stage_u = p.a_stage >> 4, b_stage_u = p.b_stage >> 4;
+  const uint32_t a_sub_u = p.a_sub >> 4, b_sub_u = p.b_sub >> 4;
+  const uint32_t b_tap_u = (uint32_t)(PAIR ? p.BN / 2 : p.BN) * 8u;   // halo: weight tap stride
+  const uint32_t band_r_u = (uint32_t)p.BW * 8u;                      // wst halo: kernel row stride
+  const uint32_t full0 = p.pro ? sBar + 384u : sBar;                 // xfull (prologue) or full
+  const int nst = p.stages, ng = p.ngroups, G = p.G, S = p.S, R = p.R;
+  const int kst = p.kstages;
+  const bool split = p.splits > 1;
+  const bool wst = p.wst != 0;
+  int stage = 0, acc = 0;
+  uint32_t phase = 0, acc_phase = 0;
+  const bool prof = (p.dbg & 16) != 0;
+  long long c_te = 0, c_fu = 0, c_mma = 0, c_com = 0, c_x;
+  for (int it = 0;; ++it) {
+    const int u = cta_unit(p, it, rank);
+    if (u < 0) break;
+    int ks0 = 0, ks1 = kst;
+    if (split) {
+      const int t = u / p.splits;
+      ks0 = (u - t * p.splits) * p.kps;
+      ks1 = min(kst, ks0 + p.kps);
+    }
+    if (prof) c_x = clock64();
+    mbar_wait(sBar + 160u + 8u * acc, acc_phase ^ 1u);     // accumulator drained
+    tc_fence_after();
+    if (prof) c_te += clock64() - c_x;
+    const uint32_t d_tmem = tmem_base + acc * p.BN;
+    uint32_t ad = a0lo + (uint32_t)stage * a_stage_u;
+    uint32_t bd = b0lo + (uint32_t)(wst && !halo_mode ? ks0 : stage) * b_stage_u;
+    for (int ks = ks0; ks < ks1; ++ks) {
+      if (prof) c_x = clock64();
+      mbar_wait(full0 + 8u * stage, phase);
+      tc_fence_after();
+      if (prof) {
+        const long long c = clock64();
+        c_fu += c - c_x;
+        c_x = c;
+      }
+      const uint32_t acc0 = ks != ks0 ? 1u : 0u;
+      if constexpr (MODE == kMmaHaloWst) {
+        const uint32_t bw = b0lo + (uint32_t)ks * R * b_sub_u;
+        for (int r = 0; r < R; ++r)
+          mma_slices<TF32, PAIR, 4>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi, 8u,
+                                    b_tap_u, S, idesc, (acc0 | (uint32_t)r) ? 1u : 0u);
+      } else if constexpr (MODE == kMmaHalo) {
+        for (int g = 0; g < G; ++g)
+          mma_slices<TF32, PAIR, 4>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi, 8u,
+                                    b_tap_u, S, idesc, (acc0 | (uint32_t)g) ? 1u : 0u);
+      } else if constexpr (MODE == kMmaNarrow) {
+        const int ksteps = G / 2;
+        for (int k = 0; k < ksteps; ++k)
+          mma_issue<TF32, PAIR>(d_tmem, ad + 2u * k * a_sub_u, ahi, bd + 2u * k * b_sub_u, bhi,
+                                idesc, k == 0 ? acc0 : 1u);
+      } else {
+        constexpr int KPR = MODE == kMmaK4 ? 4 : MODE == kMmaK2 ? 2 : 1;
+        mma_slices<TF32, PAIR, KPR>(d_tmem, ad, ahi, bd, bhi, a_sub_u, b_sub_u, G, idesc, acc0);
+      }
+      if (prof) {
+        const long long c = clock64();
+        c_mma += c - c_x;
+        c_x = c;
+      }
+      if constexpr (PAIR) umma_commit2_mc(sBar + 64u + 8u * stage, 3);
+      else umma_commit(sBar + 64u + 8u * stage);
+      if (prof) c_com += clock64() - c_x;
+      if (++stage == nst) {
+        stage = 0;
+        phase ^= 1u;
+        ad = a0lo;
+        bd = wst && !halo_mode ? bd + b_stage_u : b0lo;
+      } else {
+        ad += a_stage_u;
+        bd += b_stage_u;
+      }
+    }
+    if constexpr (PAIR) umma_commit2_mc(sBar + 128u + 8u * acc, 3);
+    else umma_commit(sBar + 128u + 8u * acc);
+    if (++acc == ng) {
+      acc = 0;
+      acc_phase ^= 1u;
+    }
+  }
+  if (prof) {
+    g_dbg_clk[2048 + 4 * blockIdx.x] = c_te;
+    g_dbg_clk[2048 + 4 * blockIdx.x + 1] = c_fu;
+    g_dbg_clk[2048 + 4 * blockIdx.x + 2] = c_mma;
+    g_dbg_clk[2048 + 4 * blockIdx.x + 3] = c_com;
   }
 }
 
@@ -430,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   const uint32_t sA = sraw + pad;
   const uint32_t sB = sA + p.stages * p.a_stage;
-  const uint32_t sO = sB + p.stages * p.b_stage;                // 2 groups x nslot staging slots
+  const uint32_t sO = sB + p.b_region;   // ngroups x nslot staging slots
   const uint32_t sBar = sO + p.ngroups * p.nslot * p.stage_out;
   uint8_t* gen_base = smem_raw + pad;
   uint8_t* bar_gen = gen_base + (sBar - sA);
@@ -441,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   auto res_bar = [&](int g, int b) { return sBar + 192u + 16u * g + 8u * b; };
   const uint32_t tslot = sBar + 256u;
   auto xfull_bar = [&](int i) { return sBar + 384u + 8u * i; };   // prologue: slice rewritten
+  const uint32_t wbar = sBar + 320u;                                // weight-stationary image
   volatile uint32_t* tslot_gen = reinterpret_cast<volatile uint32_t*>(bar_gen + 256);
   float* par_gen = reinterpret_cast<float*>(bar_gen + 512);   // ngroups x kParamFloats
 
@@ -468,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       mbar_init(empty_bar(i), 1);
       mbar_init(xfull_bar(i), kProWarps);
     }
+    mbar_init(wbar, 1);
     for (int a = 0; a < p.ngroups; ++a) {
       mbar_init(tfull_bar(a), 1);
       // pair: the leader's MMA waits for both CTAs' epilogue warps
@@ -505,6 +679,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // pair: the peer's loads complete on the leader's full barriers
       const uint32_t fbar_base = PAIR ? mapa_shared(full_bar(0), 0) : full_bar(0);
       const int bofs = PAIR ? rank * (p.BN / 2) : 0;   // weight rows this CTA fetches
+      if (p.wst) {
+        // the CTA's N block (grid % tiles_k == 0) -> its whole weight image
+        const int wk0 = ((int)blockIdx.x % p.tiles_k) * p.BN;
+        mbar_arrive_expect_tx(wbar, p.b_region);
+        if (p.halo) {
+          for (int co = 0; co < p.Cb; ++co)
+            for (int r = 0; r < p.R; ++r)
+              tma_load_4d(sB + (uint32_t)(co * p.R + r) * p.b_sub, &p.tmB, wbar, 0, wk0, co,
+                          r * p.S);
+        } else {
+          for (int ks = 0; ks < p.kstages; ++ks)
+            tma_load_3d(sB + (uint32_t)ks * p.b_stage, &p.tmB, wbar, 0, wk0, ks * p.G);
+        }
+      }
       for (int i = 0;; ++i) {
         const int u = cta_unit(p, i, rank);
         if (u < 0) break;
@@ -515,6 +703,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         decode_tile(p, t, n0, oh0, ow0, k0);
         const int iw0 = ow0 * p.stride_w - p.pad_w;
         const int ih0 = oh0 * p.stride_h - p.pad_h;
+        if (p.halo && p.wst) {
+          // one band per channel block: rows ih0 .. ih0 + BH + R - 2
+          for (int ks = ks0; ks < ks1; ++ks) {
+            TRACE(1, t);
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            TRACE(2, t);
+            if (p.dbg & 2) {
+              mbar_arrive(full_bar(stage));
+            } else {
+              mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
+              tma_load_5d(sA + stage * p.a_stage, &p.tmA, full_bar(stage), 0, iw0, ih0, ks, n0);
+            }
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          continue;
+        }
         if (p.halo) {
           for (int ks = ks0; ks < ks1; ++ks) {
             TRACE(1, t);
@@ -573,8 +780,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               }
             }
           }
-          if (!PAIR || leader_cta) tma_load_3d(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
-          else if constexpr (PAIR) tma_load_3d_pair(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
+          if (p.wst) {
+          } else if (!PAIR || leader_cta) {
+            tma_load_3d(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
+          } else if constexpr (PAIR) {
+            tma_load_3d_pair(sB + stage * p.b_stage, &p.tmB, fb, 0, k0 + bofs, ks * p.G);
+          }
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1u;
@@ -585,89 +796,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   } else if (warp == 1) {
     if (lane == 0 && leader_cta) {
       // ---------------- MMA issuer (pair: the leader issues M=256) ----------
-      const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, PAIR ? 2 * kTileM : kTileM, p.BN);
-      const int ksteps = p.G * p.rowb / 32;
-      // descriptors of stage 0; other stages / K steps only move the 14-bit
-      // start-address field (byte offset >> 4), so they are formed by adds
-      const bool narrow = p.rowb == 16;
-      const uint64_t adesc0 = narrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
-                                     : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
-      const uint64_t bdesc0 = narrow ? umma_smem_desc(sB, p.b_sub, 128, 0)
-                                     : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
-      const int kpr_shift = p.rowb >= 128 ? 2 : p.rowb == 64 ? 1 : 0;  // log2 K steps per row
-      const uint32_t a_sub_u = p.a_sub >> 4, b_sub_u = p.b_sub >> 4;   // slice strides
-      // halo: SW128 descriptors at the ring bases (the band view of tap s
-      // starts s 128-byte rows further; base offset 0, see halo_baseoff)
-      const uint64_t hdesc_a = umma_smem_desc(sA, 16, 1024, 2);
-      const uint64_t hdesc_b = umma_smem_desc(sB, 16, 1024, 2);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int it = 0;; ++it) {
-        const int u = cta_unit(p, it, rank);
-        if (u < 0) break;
-        const int t = u / p.splits;
-        const int ks0 = (u - t * p.splits) * p.kps;
-        const int ks1 = min(p.kstages, ks0 + p.kps);
-        const int acc = it % p.ngroups;
-        const uint32_t acc_phase = (it / p.ngroups) & 1;
-        TRACE(10, t);
-        mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
-        TRACE(11, t);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * p.BN;
-        for (int ks = ks0; ks < ks1; ++ks) {
-          mbar_wait(p.pro ? xfull_bar(stage) : full_bar(stage), phase);
-          TRACE(12, t);
-          tc_fence_after();
-          const uint32_t a0 = sA + stage * p.a_stage;
-          const uint32_t b0 = sB + stage * p.b_stage;
-          if (p.halo) {
-            // 128-byte rows (SW128): tap s = A view shifted by s rows
-            // (+8 descriptor units), weight tap s = +b_tap bytes
-            const uint32_t b_tap_u = (uint32_t)(PAIR ? p.BN / 2 : p.BN) * 8u;
-            for (int g = 0; g < p.G; ++g) {
-              const uint64_t ad = hdesc_a + ((a0 + g * p.a_sub - sA) >> 4);
-              const uint64_t bd = hdesc_b + ((b0 + g * p.b_sub - sB) >> 4);
-              mma_slices<TF32, PAIR, 4>(d_tmem, ad, bd, 8u, b_tap_u, p.S, idesc,
-                                        (ks != ks0 || g != 0) ? 1u : 0u);
-            }
-            if constexpr (PAIR) umma_commit2_mc(empty_bar(stage), 3);
-            else umma_commit(empty_bar(stage));
-            if (++stage == p.stages) {
-              stage = 0;
-              phase ^= 1u;
-            }
-            continue;
-          }
-          const uint64_t ad_stage = adesc0 + ((uint64_t)(stage * p.a_stage) >> 4);
-          const uint64_t bd_stage = bdesc0 + ((uint64_t)(stage * p.b_stage) >> 4);
-          const uint32_t acc0 = ks != ks0 ? 1u : 0u;
-          if (narrow) {
-            // 16-byte rows: no swizzle; one K step spans two slices (LBO)
-            for (int k = 0; k < ksteps; ++k)
-              mma_issue<TF32, PAIR>(d_tmem, ad_stage + ((2u * k * p.a_sub) >> 4),
-                                    bd_stage + ((2u * k * p.b_sub) >> 4), idesc,
-                                    k == 0 ? acc0 : 1u);
-          } else if (kpr_shift == 2) {
-            mma_slices<TF32, PAIR, 4>(d_tmem, ad_stage, bd_stage, a_sub_u, b_sub_u, p.G, idesc,
-                                      acc0);
-          } else if (kpr_shift == 1) {
-            mma_slices<TF32, PAIR, 2>(d_tmem, ad_stage, bd_stage, a_sub_u, b_sub_u, p.G, idesc,
-                                      acc0);
-          } else {
-            mma_slices<TF32, PAIR, 1>(d_tmem, ad_stage, bd_stage, a_sub_u, b_sub_u, p.G, idesc,
-                                      acc0);
-          }
-          if constexpr (PAIR) umma_commit2_mc(empty_bar(stage), 3);
-          else umma_commit(empty_bar(stage));
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-        if constexpr (PAIR) umma_commit2_mc(tfull_bar(acc), 3);
-        else umma_commit(tfull_bar(acc));
-        TRACE(13, t);
+      // one tile-loop instantiation per operand layout: the single issuing
+      // thread must keep the tensor pipe's short queue (~2 MMAs) fed, so the
+      // loop carries no per-stage mode branches and no integer divisions
+      long long dbg_c0 = 0, dbg_t0 = 0;
+      if (p.wst) mbar_wait(wbar, 0);
+      if (p.dbg & 8) {
+        dbg_c0 = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+      }
+      const int mode = p.halo ? (p.wst ? kMmaHaloWst : kMmaHalo)
+                       : p.rowb == 16 ? kMmaNarrow
+                       : p.rowb >= 128 ? kMmaK4
+                       : p.rowb == 64 ? kMmaK2 : kMmaK1;
+      switch (mode) {
+        case kMmaK4: mma_tiles<TF32, PAIR, kMmaK4>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaK2: mma_tiles<TF32, PAIR, kMmaK2>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaK1: mma_tiles<TF32, PAIR, kMmaK1>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaNarrow: mma_tiles<TF32, PAIR, kMmaNarrow>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHalo: mma_tiles<TF32, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
+        default: mma_tiles<TF32, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
+      }
+      if (p.dbg & 8) {
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        g_dbg_clk[2 * blockIdx.x] = (unsigned long long)(clock64() - dbg_c0);
+        g_dbg_clk[2 * blockIdx.x + 1] = (unsigned long long)(t1 - dbg_t0);
       }
     }
   } else if (p.pro && warp >= 2 + epi_warps) {
@@ -756,6 +910,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const uint32_t bar_id = 1 + grp;
     const size_t plane = (size_t)p.OH * p.OW * p.y;
     uint32_t res_phase = 0u;                // phase of this group's residual barrier
+    int par_k0 = -1;                        // N block whose parameters are staged
+    const bool affine = p.scale != nullptr || p.shift != nullptr;
+    const bool eprof = (p.dbg & 32) != 0 && (warp == 2 + gwarps * grp) && lane == 0;
+    long long e_pre = 0, e_tf = 0, e_res = 0, e_cmp = 0, e_st = 0, e_x = 0;
+    auto etick = [&](long long& acc_c) {
+      if (eprof) {
+        const long long c = clock64();
+        acc_c += c - e_x;
+        e_x = c;
+      }
+    };
     // pair: accumulator releases go to the leader CTA's tempty barriers
     const uint32_t tempty_base = PAIR ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
     for (int it = grp;; it += p.ngroups) {
@@ -834,9 +999,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
         };
         if (leader) TRACE(20 + grp, t);
+        if (eprof) e_x = clock64();
         issue_res(0, min(nblk, p.nslot));
-        {
-          // stage this tile's channel vectors (identity where absent)
+        if (k0 != par_k0) {
+          // stage this tile's channel vectors (identity where absent); a
+          // group keeps them while its tiles stay in one N block
+          par_k0 = k0;
           float* par = par_gen + grp * kParamFloats;
           const int j = ((warp - 2) % gwarps) * 32 + lane;
           const int k = k0 + j;
@@ -848,9 +1016,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         if (leader) TRACE(22 + grp, t);
         named_bar_sync(bar_id, gthreads);
         if (leader) TRACE(24 + grp, t);
+        etick(e_pre);
         mbar_wait(tfull_bar(acc), acc_phase);
         if (leader) TRACE(26 + grp, t);
         tc_fence_after();
+        etick(e_tf);
+        if (p.dbg & 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty_bar(acc));
+          continue;
+        }
         for (int b0 = 0; b0 < nblk; b0 += p.nslot) {
           const int cnt = min(p.nslot, nblk - b0);
           if (b0 > 0) {
@@ -861,6 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             mbar_wait(res_bar(grp, 0), res_phase & 1u);
             res_phase ^= 1u;
           }
+          etick(e_res);
           if (leader) TRACE(28 + grp, t);
           const float floor_v = p.relu ? 0.f : -INFINITY;
           const bool rnd = p.round_tf32 != 0;
@@ -874,13 +1051,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const uint32_t tcol = trow + (b0 + i) * p.y;
             const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
-            if (p.out_f32) {
-              if (has_res) epi_block_tma<true, true>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
-              else epi_block_tma<true, false>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
+#define NEO_EPI(F32, RES, AFF) \
+  epi_block_tma<F32, RES, AFF>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep)
+            if (affine) {
+              if (p.out_f32) {
+                if (has_res) NEO_EPI(true, true, true);
+                else NEO_EPI(true, false, true);
+              } else {
+                if (has_res) NEO_EPI(false, true, true);
+                else NEO_EPI(false, false, true);
+              }
             } else {
-              if (has_res) epi_block_tma<false, true>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
-              else epi_block_tma<false, false>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep);
+              if (p.out_f32) {
+                if (has_res) NEO_EPI(true, true, false);
+                else NEO_EPI(true, false, false);
+              } else {
+                if (has_res) NEO_EPI(false, true, false);
+                else NEO_EPI(false, false, false);
+              }
             }
+#undef NEO_EPI
           }
           if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
             tc_fence_before();
@@ -890,6 +1080,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           else mbar_arrive(tempty_bar(acc));
         }
           }
+          etick(e_cmp);
           if (leader) TRACE(30 + grp, t);
           fence_proxy_async_smem();
           named_bar_sync(bar_id, gthreads);
@@ -900,6 +1091,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                            p.out_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
             bulk_commit();
           }
+          etick(e_st);
         }
         continue;
       } else {
@@ -931,6 +1123,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     // complete with the grid (dependent kernels wait on grid completion)
     if (leader) bulk_wait_read<0>();
     if (leader) TRACE(64, 0);
+    if (eprof) {
+      unsigned long long* d = g_dbg_clk + 4096 + (blockIdx.x * 4 + grp) * 5;
+      d[0] = e_pre;
+      d[1] = e_tf;
+      d[2] = e_res;
+      d[3] = e_cmp;
+      d[4] = e_st;
+    }
   }
 
   __syncthreads();
@@ -1122,6 +1322,22 @@ static int64_t halo_pair_bytes(const neo_conv_params* p, int rowb, int64_t m_til
   return (int64_t)halo_a_rows(p) * rowb + (int64_t)p->s * b_rows(p, p->tile_n, m_tiles) * rowb;
 }
 
+// weight-stationary (see ConvTCParams::wst): single-CTA tiles, unsplit
+// reduction, no prologue; the resident image and the activation stage sizes
+static bool wst_allowed(const neo_conv_params* p, int tile_n, int64_t m_tiles) {
+  static const bool disabled = getenv("NEOB200_NO_WST") != nullptr;
+  return !disabled && !p->pro_scale && p->split_k <= 1 && !use_pair(p, tile_n, m_tiles);
+}
+static int64_t wst_w_bytes(const neo_conv_params* p, bool halo, int rowb, int G, int tile_n) {
+  const int64_t Cb = neo_ceil_div(p->c, p->ic_bn);
+  if (halo) return p->r * p->s * Cb * (int64_t)tile_n * rowb;
+  return neo_ceil_div(p->r * p->s * Cb, G) * G * (int64_t)tile_n * rowb;
+}
+// halo band: 128 rows read from the largest shift (R-1)*BW + S-1
+static int wst_band_rows(const neo_conv_params* p, int BW) {
+  return (int)neo_ceil_div(kTileM + (p->r - 1) * BW + p->s - 1, 8) * 8;
+}
+
 int neo_conv_default_tiles(neo_conv_params* p) {
   NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
   if (p->mode == NEO_MODE_FP32) return NEO_OK;
@@ -1220,7 +1436,26 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   static const bool auto_split = getenv("NEOB200_AUTO_SPLITK") != nullptr;
   const bool underfilled = p->split_k <= 0 && base_units * 2 <= sms && auto_split;
   if (underfilled && p->slices_per_stage <= 0) p->slices_per_stage = rowb == 16 ? 2 : 1;
-  if (p->slices_per_stage <= 0 || p->stages <= 0) {
+  // weight-stationary when the whole N block's weights fit beside the
+  // staging and >= 3 activation stages (2 when explicitly asked for)
+  bool wst = false;
+  if (p->weight_stationary != 1 && !underfilled && wst_allowed(p, p->tile_n, m_tiles)) {
+    const int g = p->slices_per_stage > 0 ? p->slices_per_stage
+                                          : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
+    const int64_t wb = wst_w_bytes(p, halo, rowb, g, p->tile_n);
+    const int64_t ast = halo ? (int64_t)wst_band_rows(p, p->tile_w) * rowb : (int64_t)g * kTileM * rowb;
+    const int64_t kst = halo ? neo_ceil_div(p->c, p->ic_bn) : neo_ceil_div(nslices, g);
+    const int64_t want = std::min<int64_t>(6, std::max<int64_t>(3, kst + 2));
+    const int64_t fit = (budget - staging - wb) / ast;
+    if ((!halo || g == 1) && fit >= std::max(p->stages, p->weight_stationary == 2 ? 2 : 3)) {
+      wst = true;
+      p->slices_per_stage = g;
+      if (p->stages <= 0) p->stages = (int)std::min<int64_t>({want, fit, kMaxStages});
+      p->split_k = 1;
+    }
+  }
+  p->weight_stationary = wst ? 2 : 1;
+  if (!wst && (p->slices_per_stage <= 0 || p->stages <= 0)) {
     int g = p->slices_per_stage > 0 ? p->slices_per_stage
                                     : (halo ? 1 : pick_slices_per_stage(nslices, rowb, p->tile_n));
     const int gmin = rowb == 16 ? 2 : 1;
@@ -1339,11 +1574,14 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const int64_t Cb = neo_ceil_div(p->c, x);
   const int64_t cbt = p->x_cb_total > 0 ? p->x_cb_total : Cb;
   const bool halo = BW > OW;
+  const bool wst = p->weight_stationary == 2;
   NEO_CHECK_ARG(!halo || halo_eligible(p, rowb, OW), NEO_ERR_SCHEDULE_INVALID,
                 "tile_w=%d wider than the output needs a stride-1, 128-byte-row conv", BW);
   NEO_CHECK_ARG(!halo || (BW == OW + p->s - 1 && BNI == 1), NEO_ERR_SCHEDULE_INVALID,
                 "halo tiles must span the padded width OW+S-1 of one image");
-  const int64_t nslices = halo ? p->r * Cb : p->r * p->s * Cb;
+  const int64_t nslices = halo ? (wst ? Cb : p->r * Cb) : p->r * p->s * Cb;
+  NEO_CHECK_ARG(!(wst && halo && G != 1), NEO_ERR_SCHEDULE_INVALID,
+                "weight-stationary halo tiles take one channel block per stage");
   const int64_t kstages = neo_ceil_div(nslices, G);
 
   if (p->pro_scale) {
@@ -1357,6 +1595,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   }
   const int64_t tiles_m_all = neo_ceil_div(OW, BW) * neo_ceil_div(OH, BH) * neo_ceil_div(p->n, BNI);
   const bool pair = !p->pro_scale && use_pair(p, BN, tiles_m_all);
+  NEO_CHECK_ARG(!wst || wst_allowed(p, BN, tiles_m_all), NEO_ERR_SCHEDULE_INVALID,
+                "weight-stationary tiles need single-CTA tiles, no split-K, no prologue");
   NEO_CHECK_ARG(!(p->cta_pair == 2 && !pair), NEO_ERR_SCHEDULE_INVALID,
                 "cta_pair not possible here (split_k=%d, tile_n=%d, %lld M tiles)", p->split_k,
                 BN, (long long)tiles_m_all);
@@ -1376,7 +1616,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                              (cuuint64_t)p->h * p->w_in * rowb,
                              (cuuint64_t)cbt * p->h * p->w_in * rowb};
     cuuint32_t box[5] = {(cuuint32_t)x, (cuuint32_t)(BW * p->stride_w),
-                         (cuuint32_t)(BH * p->stride_h), 1u, (cuuint32_t)BNI};
+                         (cuuint32_t)(BH * p->stride_h + (halo && wst ? p->r - 1 : 0)), 1u,
+                         (cuuint32_t)BNI};
     // halo: box = BH rows of the padded width (stride 1), i.e. BH*BW pixels
     cuuint32_t estr[5] = {1u, (cuuint32_t)p->stride_w, (cuuint32_t)p->stride_h, 1u, 1u};
     CUresult r = encode(&kp.tmA, dt, 5, const_cast<char*>(base), dims, strides, box, estr,
@@ -1438,6 +1679,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                           : nullptr;
     NEO_CHECK_ARG(num_tiles * sp.splits < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many units");
     kp.num_units = (int)(num_tiles * sp.splits);
+    NEO_CHECK_ARG(!wst || sp.splits == 1, NEO_ERR_SCHEDULE_INVALID,
+                  "weight-stationary tiles need an unsplit reduction");
     NEO_CHECK_ARG(!pair || sp.splits == 1, NEO_ERR_SCHEDULE_INVALID,
                   "CTA-pair tiles need an unsplit reduction");
     kp.pair = pair ? 1 : 0;
@@ -1462,17 +1705,28 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     static const char* bo = getenv("NEOB200_HALO_BASEOFF");
     kp.halo_baseoff = bo ? atoi(bo) : 0;  // swizzle follows absolute address bits
   }
-  if (halo) {
+  if (halo && wst) {
+    kp.a_sub = (uint32_t)(wst_band_rows(p, BW) * rowb);
+    kp.b_sub = (uint32_t)(p->s * BN * rowb);
+    kp.tx_bytes = (uint32_t)((BH + p->r - 1) * BW * rowb);
+  } else if (halo) {
     kp.a_sub = (uint32_t)(halo_a_rows(p) * rowb);
     kp.b_sub = (uint32_t)(p->s * bro * rowb);
     kp.tx_bytes = (uint32_t)((pair ? 2 : 1) * G * (BW * BH * rowb + p->s * bro * rowb));
   } else {
     kp.a_sub = (uint32_t)(kTileM * rowb);
     kp.b_sub = (uint32_t)(bro * rowb);
-    kp.tx_bytes = (uint32_t)((pair ? 2 : 1) * G * (BW * BH * BNI * rowb + bro * rowb));
+    kp.tx_bytes = (uint32_t)((pair ? 2 : 1) * G * (BW * BH * BNI * rowb + (wst ? 0 : bro * rowb)));
   }
   kp.a_stage = kp.a_sub * G;
   kp.b_stage = kp.b_sub * G;
+  kp.wst = wst ? 1 : 0;
+  {
+    static const char* dbg = getenv("NEOB200_DBG");
+    kp.dbg = dbg ? atoi(dbg) : 0;
+  }
+  kp.b_region = wst ? (halo ? (uint32_t)(p->r * Cb) * kp.b_sub : (uint32_t)kstages * kp.b_stage)
+                    : (uint32_t)p->stages * kp.b_stage;
   kp.ngroups = epi_groups(p, BN);
   uint32_t cols = 32;
   while (cols < (uint32_t)(kp.ngroups * BN)) cols <<= 1;
@@ -1500,7 +1754,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const int rb_out = epi_rowb_out(p, BN);
   {
     const int64_t left = (int64_t)kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4 -
-                         (int64_t)p->stages * (kp.a_stage + kp.b_stage);
+                         (int64_t)p->stages * kp.a_stage - kp.b_region;
     const int64_t slots = rb_out ? left / ((int64_t)kp.ngroups * kTileM * rb_out) : 0;
     kp.nslot = (int)std::min<int64_t>(slots, BN / std::max(1, p->oc_bn));
   }
@@ -1537,14 +1791,16 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.out_box_bytes = 0;
   }
 
-  const size_t smem = 1024 + (size_t)p->stages * (kp.a_stage + kp.b_stage) +
+  const size_t smem = 1024 + (size_t)p->stages * kp.a_stage + kp.b_region +
                      (size_t)kp.ngroups * kp.nslot * kp.stage_out + 512 +
                      (size_t)kp.ngroups * kParamFloats * 4;
   NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
   const int sms = sm_count_of_current_device();
-  const int grid = pair ? (int)std::min<int64_t>(kp.num_groups, sms / 2) * 2
-                        : (int)std::min<int64_t>(kp.num_units, sms);
+  // weight-stationary: grid % tiles_k == 0 keeps each CTA on one N block
+  const int grid = pair  ? (int)std::min<int64_t>(kp.num_groups, sms / 2) * 2
+                   : wst ? (int)(std::min<int64_t>(kp.num_units, sms) / kp.tiles_k * kp.tiles_k)
+                         : (int)std::min<int64_t>(kp.num_units, sms);
   // opt in to the large dynamic shared memory once per (device, kernel); the
   // attribute call is kept out of later launches so they can be graph-captured
   static bool attr_set[64][4] = {};
@@ -1604,3 +1860,8 @@ extern "C" int neo_trace_dump(unsigned long long* host, int max_n) {
   return n;
 }
 #endif
+
+// debug: per-CTA (MMA-loop cycles, ns) of the last NEOB200_DBG&8 launch
+extern "C" __attribute__((visibility("default"))) int neo_dbg_clk(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_dbg_clk, n * sizeof(unsigned long long));
+}

@@ -166,6 +166,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// waiters that are not on the critical issue path (epilogue warps): back
+// off with nanosleep so their polling does not compete with the MMA/TMA
+// threads for issue slots and barrier-unit bandwidth
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, int ns) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    if ((++spins & 1023u) == 0 && clock64() - t0 > 20000000000ll) __trap();
+  }
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }

@@ -116,7 +116,7 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
         p.pro_relu = int(bool(prologue[2]))
     if tile:
         for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
-                    "split_k", "cta_pair"):
+                    "split_k", "cta_pair", "weight_stationary"):
             setattr(p, key, int(tile.get(key, 0) or 0))
     return p
 
@@ -141,7 +141,8 @@ def default_tiles(p: L.ConvParams) -> dict:
     q = L.ConvParams.from_buffer_copy(p)
     L.check(L.load().neo_conv_default_tiles(ctypes.byref(q)), "neo_conv_default_tiles")
     return {k: getattr(q, k) for k in ("tile_w", "tile_h", "tile_img", "tile_n",
-                                        "slices_per_stage", "stages", "split_k", "cta_pair")}
+                                        "slices_per_stage", "stages", "split_k", "cta_pair",
+                                        "weight_stationary")}
 
 
 def pool2d(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, flags=0, stream=None):

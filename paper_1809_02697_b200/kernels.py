@@ -33,7 +33,7 @@ from .layout import NCHW, Tensor, kcrsck, nchwc
 UNROLL_LIMIT = 25  # kept for API compatibility (CPU window-flattening limit)
 
 TILE_FIELDS = ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
-               "split_k", "cta_pair")
+               "split_k", "cta_pair", "weight_stationary")
 
 
 @dataclass(frozen=True)
@@ -97,6 +97,7 @@ class ConvSchedule:
     stages: int = 0
     split_k: int = 0
     cta_pair: int = 0
+    weight_stationary: int = 0
 
     def check(self, wl: ConvWorkload) -> None:
         """Divisibility rules of the reference (kernels.py:56-63)."""

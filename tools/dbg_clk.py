@@ -1,0 +1,26 @@
+import ctypes, os, sys, subprocess
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tools')
+os.environ['NEOB200_DBG'] = os.environ.get('NEOB200_DBG', '8')
+sys.argv = ['conv_bench'] + sys.argv[1:]
+import conv_bench
+conv_bench.main()
+from paper_1809_02697_b200 import _lib as L
+lib = L.load()
+buf = (ctypes.c_ulonglong * 8192)()
+lib.neo_dbg_clk(buf, 8192)
+cyc = [buf[2*i] for i in range(148)]; ns = [buf[2*i+1] for i in range(148)]
+import statistics
+print("cycles median", statistics.median(cyc), "ns median", statistics.median(ns), "GHz", statistics.median(c/n for c, n in zip(cyc, ns) if n))
+
+if int(os.environ['NEOB200_DBG']) & 16:
+    names = ["tempty wait", "full wait", "mma issue", "commit"]
+    for j, nm in enumerate(names):
+        print(nm, statistics.median(buf[2048 + 4 * i + j] for i in range(148)))
+
+if int(os.environ['NEOB200_DBG']) & 32:
+    names = ["pre (res issue, params, bar)", "tfull wait", "res wait", "compute", "store"]
+    for j, nm in enumerate(names):
+        vals = [buf[4096 + (i * 4 + g) * 5 + j] for i in range(148) for g in range(4)]
+        vals = [v for v in vals if v]
+        print(nm, statistics.median(vals) if vals else 0)

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(96, 1) tma_stream(const __grid_constant__ Args
 
 int main(int argc, char** argv) {
   const long long src_mb = argc > 1 ? atoll(argv[1]) : 512;
+  const int grid = argc > 2 ? atoi(argv[2]) : 1;   // CTAs (one per SM), e.g. 148
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q);
@@ -139,10 +140,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&gmap, sizeof(CUtensorMap));
   for (int mode : {1, 3, 4})
     for (int boxes : {2, 4, 8})
-      cfgs.push_back({128, 32, boxes, 4, 1, mode});
+      cfgs.push_back({128, 32, boxes, 4, grid, mode});
   for (int mode : {1, 3, 4})
     for (int rows : {64, 128, 256})
-      cfgs.push_back({128, rows, 2, 3, 1, mode});
+      for (int stages : {3, 6})
+        cfgs.push_back({128, rows, 2, stages, grid, mode});
   for (auto c : cfgs) {
     Args a{};
     a.mode = c.mode;
@@ -154,7 +156,7 @@ int main(int argc, char** argv) {
     a.total_rows = bytes / c.rowb;
     const long long stage_bytes = (long long)c.rows * c.rowb * c.boxes;
     if (c.stages * stage_bytes + 2048 > 227 * 1024) continue;
-    a.iters = (int)std::max<long long>(64, (64ll << 20) / stage_bytes / c.grid);
+    a.iters = (int)std::max<long long>(64, (64ll << 20) / stage_bytes / std::min(c.grid, 8));
     cuuint64_t dims[2] = {(cuuint64_t)(c.rowb / 2), (cuuint64_t)a.total_rows};
     cuuint64_t strides[1] = {(cuuint64_t)c.rowb};
     cuuint32_t box[2] = {(cuuint32_t)(c.rowb / 2), (cuuint32_t)c.rows};

@@ -16,7 +16,7 @@ NAMES = {1: "prod:wait_empty>", 2: "prod:got_empty", 10: "mma:wait_tempty>", 11:
          12: "mma:got_full", 20: "epi0:start", 21: "epi1:start", 22: "epi0:res_issued",
          23: "epi1:res_issued", 24: "epi0:bar1", 25: "epi1:bar1", 26: "epi0:got_tfull",
          27: "epi1:got_tfull", 28: "epi0:got_res", 29: "epi1:got_res", 30: "epi0:computed",
-         31: "epi1:computed", 32: "epi0:bar2", 33: "epi1:bar2", 13: "mma:committed",
+         31: "epi1:computed", 32: "epi0:bar2", 33: "epi1:bar2", 13: "mma:committed", 14: "mma:wait_full>", 15: "mma:issued",
          40: "split:partial_stored", 41: "split:all_arrived", 42: "split:fixup_done",
          60: "kernel:entry", 61: "kernel:setup_done", 62: "kernel:final_sync", 64: "epi:bulk_done"}
 
@@ -64,7 +64,7 @@ def main():
     chunk = sorted((ns, ev) for ev, tile, ns in recs if 43 <= ev < 56)
     print("chunk events (first 24):", [(ev, round((ns - t0) / 1000, 2)) for ns, ev in chunk[:24]])
     print("all events in time order:")
-    for ev, tile, ns in sorted(recs, key=lambda r: r[2])[:80]:
+    for ev, tile, ns in sorted(recs, key=lambda r: r[2])[:160]:
         print(f"  {(ns - t0) / 1000:8.3f} us  {NAMES.get(ev, ev)}  tile {tile}")
     total = max(r[2] for r in recs) - t0
     print(f"CTA0 span {total / 1000:.2f} us, records {n}")
