@@ -319,27 +319,29 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         }
         *reinterpret_cast<float4*>(slot) = make_float4(o[0], o[1], o[2], o[3]);
       } else {
+        // bf16 output: the conv result (after scale/shift/bias) is rounded
+        // to bf16 once, the residual is added in packed bf16 (one rounding,
+        // as a separate bf16 add of the rounded conv output would do) and
+        // relu clamps the packed pair; without a residual the relu is fused
+        // into the conversion (rounding keeps the sign)
         uint4 packed;
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&packed);
-        uint4 rv;
-        if constexpr (HAS_RES) rv = *slot;
-        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+        uint32_t* h = reinterpret_cast<uint32_t*>(&packed);
+        const bool relu = relu_floor == 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float a = f[2 * j], b = f[2 * j + 1];
-          if constexpr (HAS_RES) {
-            const float2 t = __bfloat1622float2(r2[j]);
-            a += t.x;
-            b += t.y;
-          }
-          // relu fused into the conversion (max(v, 0) then round == round
-          // then clamp: rounding keeps the sign)
-          uint32_t h;
-          if (relu_floor == 0.f)
-            asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+          if (!HAS_RES && relu)
+            asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
           else
-            asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
-          reinterpret_cast<uint32_t*>(h2)[j] = h;
+            asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
+        }
+        if constexpr (HAS_RES) {
+          const uint4 rv = *slot;
+          const uint32_t* r = reinterpret_cast<const uint32_t*>(&rv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(r[j]));
+            if (relu) asm("max.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(0u));
+          }
         }
         *slot = packed;
       }
