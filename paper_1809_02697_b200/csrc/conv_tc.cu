@@ -600,6 +600,8 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
 template <bool TF32, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  long long dbg_t_entry = 0;
+  if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_entry));
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   const uint32_t sA = sraw + pad;
@@ -672,6 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   // the previous kernel's tail; nothing global is touched before this wait
   neo_pdl_trigger();
   neo_pdl_wait();
+  long long dbg_t_pdl = 0;
+  if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_pdl));
 
   if (warp == 0) {
     if (lane == 0) {
@@ -824,6 +828,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         g_dbg_clk[2 * blockIdx.x] = (unsigned long long)(clock64() - dbg_c0);
         g_dbg_clk[2 * blockIdx.x + 1] = (unsigned long long)(t1 - dbg_t0);
+        g_dbg_clk[7000 + 2 * blockIdx.x] = dbg_t0;
+        g_dbg_clk[7000 + 2 * blockIdx.x + 1] = t1;
       }
     }
   } else if (p.pro && warp >= 2 + epi_warps) {
@@ -1137,6 +1143,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
   __syncthreads();
   if (threadIdx.x == 0) TRACE(62, 0);
+  if ((p.dbg & 64) && threadIdx.x == 0) {
+    // per-CTA timeline: entry, past griddepcontrol.wait, all roles done
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dbg_clk[6144 + 3 * blockIdx.x] = dbg_t_entry;
+    g_dbg_clk[6144 + 3 * blockIdx.x + 1] = dbg_t_pdl;
+    g_dbg_clk[6144 + 3 * blockIdx.x + 2] = t;
+  }
 #ifdef NEO_TRACE
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x < kTraceWarps)
@@ -1448,7 +1462,10 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     const int64_t ast = halo ? (int64_t)wst_band_rows(p, p->tile_w) * rowb : (int64_t)g * kTileM * rowb;
     const int64_t kst = halo ? neo_ceil_div(p->c, p->ic_bn) : neo_ceil_div(nslices, g);
     const int64_t want = std::min<int64_t>(6, std::max<int64_t>(3, kst + 2));
-    const int64_t fit = (budget - staging - wb) / ast;
+    // an explicit depth may squeeze the epilogue staging to one slot per group
+    const int rbo = epi_rowb_out(p, p->tile_n);
+    const int64_t min_staging = rbo ? (int64_t)epi_groups(p, p->tile_n) * kTileM * rbo : 0;
+    const int64_t fit = (budget - (p->stages > 0 ? min_staging : staging) - wb) / ast;
     if ((!halo || g == 1) && fit >= std::max(p->stages, p->weight_stationary == 2 ? 2 : 3)) {
       wst = true;
       p->slices_per_stage = g;

@@ -24,3 +24,19 @@ if int(os.environ['NEOB200_DBG']) & 32:
         vals = [buf[4096 + (i * 4 + g) * 5 + j] for i in range(148) for g in range(4)]
         vals = [v for v in vals if v]
         print(nm, statistics.median(vals) if vals else 0)
+
+if int(os.environ['NEOB200_DBG']) & 64:
+    ent = [buf[6144 + 3 * i] for i in range(148)]
+    pdl = [buf[6144 + 3 * i + 1] for i in range(148)]
+    ex = [buf[6144 + 3 * i + 2] for i in range(148)]
+    t0 = min(ent)
+    rel = lambda v: [(x - t0) / 1000 for x in v]
+    import numpy as np
+    for nm, v in (("entry", ent), ("pdl-wait done", pdl), ("exit", ex)):
+        r = np.array(rel(v))
+        print(f"{nm:14s} min {r.min():6.2f} med {np.median(r):6.2f} max {r.max():6.2f} us")
+    if int(os.environ['NEOB200_DBG']) & 8:
+        ms = np.array(rel([buf[7000 + 2 * i] for i in range(148)]))
+        me = np.array(rel([buf[7000 + 2 * i + 1] for i in range(148)]))
+        print(f"mma loop start min {ms.min():6.2f} med {np.median(ms):6.2f} max {ms.max():6.2f}")
+        print(f"mma loop end   min {me.min():6.2f} med {np.median(me):6.2f} max {me.max():6.2f}")

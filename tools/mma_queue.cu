@@ -94,9 +94,17 @@ __global__ void __launch_bounds__(128, 1) grouped(int n, int groups, int mode, i
       if (mode >= 3) tc_fence_after();
       if (mode >= 4) acc += g / divisor;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_ss<false>(tmem + (acc & 1) * 0, ad0 + (uint64_t)(2 * kk), bd0 + (uint64_t)(2 * kk), idesc, 1u);
+      for (int kk = 0; kk < 4; ++kk) {
+        // 32-bit low-word descriptor arithmetic (as in conv_tc.cu mma_issue)
+        const uint32_t alo = (uint32_t)ad0 + 2u * kk, blo = (uint32_t)bd0 + 2u * kk;
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 ad, bd;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+                     "mov.b64 ad, {%1, %2};\n\tmov.b64 bd, {%3, %4};\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %5, p;\n\t}"
+                     ::"r"(tmem), "r"(alo), "r"((uint32_t)(ad0 >> 32)), "r"(blo),
+                     "r"((uint32_t)(bd0 >> 32)), "r"(idesc), "r"(1u) : "memory");
+      }
       if (mode >= 1) umma_commit(cbar);
+      if (mode >= 5) umma_commit(cbar);
     }
     umma_commit(bar);
     mbar_wait(bar, 0);
@@ -126,7 +134,7 @@ int main() {
   }
   cudaFuncSetAttribute(grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int n : {64, 128, 256})
-    for (int mode = 0; mode <= 4; ++mode) {
+    for (int mode = 0; mode <= 5; ++mode) {
       grouped<<<1, 128, 170 * 1024>>>(n, 256, mode, 7, d);
       grouped<<<1, 128, 170 * 1024>>>(n, 256, mode, 7, d);
       long long h[2];
