@@ -11,7 +11,8 @@ buf = (ctypes.c_ulonglong * 8192)()
 lib.neo_dbg_clk(buf, 8192)
 cyc = [buf[2*i] for i in range(148)]; ns = [buf[2*i+1] for i in range(148)]
 import statistics
-print("cycles median", statistics.median(cyc), "ns median", statistics.median(ns), "GHz", statistics.median(c/n for c, n in zip(cyc, ns) if n))
+if any(ns):
+    print("cycles median", statistics.median(cyc), "ns median", statistics.median(ns), "GHz", statistics.median(c/n for c, n in zip(cyc, ns) if n))
 
 if int(os.environ['NEOB200_DBG']) & 16:
     names = ["tempty wait", "full wait", "mma issue", "commit"]
@@ -40,3 +41,9 @@ if int(os.environ['NEOB200_DBG']) & 64:
         me = np.array(rel([buf[7000 + 2 * i + 1] for i in range(148)]))
         print(f"mma loop start min {ms.min():6.2f} med {np.median(ms):6.2f} max {ms.max():6.2f}")
         print(f"mma loop end   min {me.min():6.2f} med {np.median(me):6.2f} max {me.max():6.2f}")
+
+if int(os.environ['NEOB200_DBG']) & 128:
+    for w in range(2, 18):
+        n = buf[7680 + w]
+        if n:
+            print(f"warp {w:2d}: {n} chunks, tmem ld+wait {buf[7600 + w] / n:6.0f} cyc, finish {buf[7640 + w] / n:6.0f} cyc")
