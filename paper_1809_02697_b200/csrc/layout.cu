@@ -419,6 +419,57 @@ __global__ void stem_fold_kernel(const float* __restrict__ src, Td* __restrict__
     for (int v = 0; v < kVec; ++v) d4[v] = r4[v];
   }
 }
+
+// Row-tiled fold: one CTA per (n, h) input row (many small CTAs per SM hide
+// the load latency); the C input rows are staged in shared memory with
+// coalesced 16-byte loads, then every thread builds 16-byte pieces of the
+// folded output row (consecutive threads -> consecutive pieces: coalesced
+// stores).  CC = C (compile-time: no divisions).  Same values as
+// stem_fold_kernel.
+template <typename Td, int XF, int CC>
+__global__ void stem_fold_rows_kernel(const float* __restrict__ src, Td* __restrict__ dst,
+                                      int H, int W, int S, int sw, int pw, int OW, bool round) {
+  extern __shared__ float rows[];   // CC x W
+  neo_pdl_enter();
+  constexpr int kLanes = 16 / (int)sizeof(Td);   // lanes per 16-byte piece
+  constexpr int kPieces = XF / kLanes;
+  const int F = S * CC;
+  const int Cb = (F + XF - 1) / XF;
+  const int64_t row = blockIdx.x;
+  const int64_t n = row / H;
+  const int h = (int)(row - n * H);
+#pragma unroll
+  for (int c = 0; c < CC; ++c) {
+    const float* plane = src + ((n * CC + c) * H + h) * (int64_t)W;
+    if ((W & 3) == 0) {
+      for (int i = threadIdx.x; i < W / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(rows + c * W)[i] = __ldg(reinterpret_cast<const float4*>(plane) + i);
+    } else {
+      for (int i = threadIdx.x; i < W; i += blockDim.x) rows[c * W + i] = __ldg(plane + i);
+    }
+  }
+  __syncthreads();
+  const int per_cb = OW * kPieces;
+  for (int it = threadIdx.x; it < Cb * per_cb; it += blockDim.x) {
+    const int cb = it / per_cb;
+    const int rem = it - cb * per_cb;
+    const int wq = rem / kPieces, pc = rem - wq * kPieces;
+    const int iw0 = sw * wq - pw;
+    Td vals[kLanes];
+#pragma unroll
+    for (int j = 0; j < kLanes; ++j) {
+      const int f = cb * XF + pc * kLanes + j;   // folded channel = s*CC + c
+      const int ss = f / CC, c = f - ss * CC;
+      const int iw = iw0 + ss;
+      float v = 0.f;
+      if (f < F && iw >= 0 && iw < W) v = rows[c * W + iw];
+      if constexpr (sizeof(Td) == 4) vals[j] = round ? neo_round_tf32(v) : v;
+      else vals[j] = Elem<Td>::from_f(v);
+    }
+    Td* out = dst + (((n * Cb + cb) * H + h) * (int64_t)OW + wq) * XF + pc * kLanes;
+    *reinterpret_cast<uint4*>(out) = *reinterpret_cast<const uint4*>(vals);
+  }
+}
 }  // namespace
 
 extern "C" int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t n, int64_t c,
@@ -431,9 +482,25 @@ extern "C" int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool round = (flags & NEO_FLAG_ROUND_TF32) != 0;
+  // row-tiled kernel when the C input rows fit in shared memory
+  const size_t row_smem = (size_t)c * w * sizeof(float);
+  const bool rows_ok = row_smem <= 48 * 1024 && c <= 4 && n * h < (1ll << 31) &&
+                       !getenv("NEOB200_FOLD_PIXEL");
+#define NEO_FOLD_ROWS(T, X, CC)                                                               \
+  neo_launch(stem_fold_rows_kernel<T, X, CC>, (unsigned)(n * h), 128, row_smem, st, src,     \
+             static_cast<T*>(dst), (int)h, (int)w, s, stride_w, pad_w, (int)ow, round)
 #define NEO_FOLD(T, X)                                                                      \
-  neo_launch(stem_fold_kernel<T, X>, grid, 256, 0, st, src, static_cast<T*>(dst), n, (int)c, (int)h, \
-                                               (int)w, s, stride_w, pad_w, (int)ow, round)
+  do {                                                                                      \
+    if (rows_ok) {                                                                          \
+      if (c == 1) NEO_FOLD_ROWS(T, X, 1);                                                   \
+      else if (c == 2) NEO_FOLD_ROWS(T, X, 2);                                              \
+      else if (c == 3) NEO_FOLD_ROWS(T, X, 3);                                              \
+      else NEO_FOLD_ROWS(T, X, 4);                                                          \
+    } else {                                                                                \
+      neo_launch(stem_fold_kernel<T, X>, grid, 256, 0, st, src, static_cast<T*>(dst), n, (int)c, \
+                 (int)h, (int)w, s, stride_w, pad_w, (int)ow, round);                       \
+    }                                                                                       \
+  } while (0)
   if (dst_dtype == NEO_BF16) {
     if (xf == 8) NEO_FOLD(__nv_bfloat16, 8);
     else if (xf == 16) NEO_FOLD(__nv_bfloat16, 16);
@@ -448,6 +515,7 @@ extern "C" int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t
     else NEO_CHECK_ARG(false, NEO_ERR_UNSUPPORTED, "stem fold block %d", xf);
   }
 #undef NEO_FOLD
+#undef NEO_FOLD_ROWS
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
