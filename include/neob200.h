@@ -66,6 +66,10 @@ typedef enum {
 /* flag bits */
 #define NEO_FLAG_ROUND_TF32 0x1   /* round fp32 results to tf32 (RN)        */
 #define NEO_FLAG_PAD_CHANNELS 0x2 /* allow C % x != 0: zero-filled pad lanes */
+/* conv: the weight buffer is not written by any kernel that may still be
+ * running (e.g. packed at load time), so a programmatically launched conv may
+ * fetch its resident weight image before griddepcontrol.wait */
+#define NEO_FLAG_STATIC_WEIGHTS 0x4
 
 const char* neo_last_error(void);
 int neo_abi_version(void);

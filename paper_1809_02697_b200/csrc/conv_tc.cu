@@ -106,6 +106,7 @@ struct ConvTCParams {
   // band view shifted by r*BW rows), so a stage feeds R*S taps.
   int wst;
   uint32_t b_region;
+  int static_w;     // NEO_FLAG_STATIC_WEIGHTS: weight image fetched before griddepcontrol.wait
   int dbg;          // NEOB200_DBG timing experiments (1: no epilogue work, 2: no A loads,
                     // 8: per-CTA MMA-loop clocks -> neo_dbg_clk)
   float* ws;        // partials
@@ -671,9 +672,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t tmem_base = *tslot_gen;
   if (threadIdx.x == 0) TRACE(61, 0);
   // PDL: barrier init, TMEM allocation and descriptor prefetch above overlap
-  // the previous kernel's tail; nothing global is touched before this wait
+  // the previous kernel's tail.  Each role waits for the previous kernel
+  // before it touches global memory the previous kernels may write; the
+  // producer first issues a static resident weight image (weights are not
+  // written by the step), and the MMA warp never touches global memory.
   neo_pdl_trigger();
-  neo_pdl_wait();
+  if (warp != 0 && warp != 1) neo_pdl_wait();
   long long dbg_t_pdl = 0;
   if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_pdl));
 
@@ -685,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // pair: the peer's loads complete on the leader's full barriers
       const uint32_t fbar_base = PAIR ? mapa_shared(full_bar(0), 0) : full_bar(0);
       const int bofs = PAIR ? rank * (p.BN / 2) : 0;   // weight rows this CTA fetches
+      if (!(p.wst && p.static_w)) neo_pdl_wait();
       if (p.wst) {
         // the CTA's N block (grid % tiles_k == 0) -> its whole weight image
         const int wk0 = ((int)blockIdx.x % p.tiles_k) * p.BN;
@@ -698,6 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           for (int ks = 0; ks < p.kstages; ++ks)
             tma_load_3d(sB + (uint32_t)ks * p.b_stage, &p.tmB, wbar, 0, wk0, ks * p.G);
         }
+        if (p.static_w) neo_pdl_wait();   // activations come from the previous kernel
       }
       for (int i = 0;; ++i) {
         const int u = cta_unit(p, i, rank);
@@ -1740,6 +1746,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.a_stage = kp.a_sub * G;
   kp.b_stage = kp.b_sub * G;
   kp.wst = wst ? 1 : 0;
+  kp.static_w = (p->flags & NEO_FLAG_STATIC_WEIGHTS) ? 1 : 0;
   {
     static const char* dbg = getenv("NEOB200_DBG");
     kp.dbg = dbg ? atoi(dbg) : 0;

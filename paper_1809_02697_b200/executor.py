@@ -636,7 +636,9 @@ class DeviceProgram:
             r_t = None
             if res is not None:
                 r_t = res.tensor if res.tensor.dtype == o_t.dtype else self._as_f32(res)
-            flags = self.round_flag | (L.FLAG_PAD_CHANNELS if pad_c else 0)
+            # weights are packed here, at load time: the conv may prefetch its
+            # resident weight image before waiting on the previous kernel
+            flags = self.round_flag | (L.FLAG_PAD_CHANNELS if pad_c else 0) | L.FLAG_STATIC_WEIGHTS
             pro = None
             if node.id in self.prologue:      # BN -> ReLU applied on the smem tiles
                 ps, pt = self._bn_scale_shift(g.nodes[self.prologue[node.id]])
