@@ -1,0 +1,477 @@
+// K-STEM: the image stem of ResNet / DenseNet / SSD-ResNet as ONE kernel:
+//   conv 7x7 stride 2 pad 3 over a C<=4 channel NCHW f32 image, K = 64
+//   -> scale/shift -> bias -> relu      (Epilogue, reference kernels.py:185-197)
+//   -> max pool 3x3 stride 2 pad 1      (reference executor.py:103-128, -inf pad)
+//   -> NCHW[y]c bf16 (optionally a channel-block window of a concat buffer).
+// In the reference these are three operators (conv_blocked on the packed
+// 3-channel input, kernels.py:250-303, then _pool2d); here neither the packed
+// input nor the 112x112 conv map ever reaches HBM.
+//
+// Work unit = one 7x7 tile of pooled outputs of one image.  Its 3x3/2 pool
+// windows cover a 15x15 conv tile, computed as two M=128 tcgen05 MMA tiles of
+// 16 conv rows x 8 conv columns (16 x 16, row 15 / column 15 unused).
+//
+// No im2col: the input patch sits in shared memory as bf16 [row][col][4
+// channels] (8 bytes per pixel, channel 3 zero).  For kernel row r and a pair
+// of horizontal taps (s, s+1), the 8 K-elements (2 taps x 4 channels) of conv
+// pixel (g, i) are the 16 contiguous bytes at input (2g + r, 2i + s), and conv
+// pixel (g, i+1) starts exactly 16 bytes later (stride 2).  So eight conv
+// columns form an 8-row x 16-byte no-swizzle UMMA core matrix in place:
+//   A(step r, q) = patch + r*pitch + 32*q,  LBO = 16 B (next tap pair),
+//                  SBO = 2*pitch (next conv row = two input rows down).
+// K per step = 16 = taps {4q..4q+3} x 4 channels; 7 kernel rows x 2 steps =
+// 14 MMAs (M=128, N=64) per 16x8 conv tile.  Tap 7 and channel 3 carry zero
+// weights.  The weights are a resident 28 KB image [step][chunk][64 k][8].
+//
+// Warp roles (384 threads, persistent over units, one CTA per SM):
+//   warp 0      TMA producer: f32 patch box (44 cols x 37 rows x C planes,
+//               zero fill outside the image) into a 4-deep ring
+//   warp 1      TMEM allocator + single-thread MMA issuer (4 accumulators of
+//               2 x 64 columns)
+//   warps 2-3   converters: f32 planar box -> bf16 [row][col][4] patch
+//               (2-deep ring), then fence.proxy.async for the tensor core
+//   warps 4-11  epilogue: tcgen05.ld -> scale/shift/bias/relu -> bf16 conv
+//               tile in shared memory (double buffered, XOR-swizzled 16-byte
+//               chunks) -> 3x3/2 max pool -> 16-byte global stores
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "neo_common.cuh"
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kRawStages = 4;
+// f32 input box per unit: 37 rows x 44 columns starting 8 columns left of
+// the conv tile's first tap (a TMA box must start on a 16-byte boundary of
+// its innermost dimension; a negative, unaligned start column faults), so
+// patch column j is box column j + kColOff
+constexpr int kBoxW = 44, kBoxH = 37, kColOff = 3;
+constexpr int kPatchCols = 38;                 // input columns the MMAs read
+constexpr int kPitch = kPatchCols * 8;         // bytes per bf16x4 patch row
+constexpr int kPatchBytes = kBoxH * kPitch;    // 11248
+constexpr int kPatchSlot = 11264;              // patch slot (16-byte multiple)
+static_assert(kPatchBytes <= kPatchSlot, "patch slot too small");
+constexpr int kSteps = 14;                     // (r, q) K steps per conv tile
+constexpr int kWBytes = kSteps * 2 * 64 * 16;  // 28672
+constexpr int kCtileBytes = 16 * 16 * 128;     // 16x16 conv px x 64 bf16
+constexpr int kPool = 7;                       // pooled tile edge
+
+struct StemParams {
+  CUtensorMap tmX;          // 3-D f32 (W, H, N*C), box (44, 37, C)
+  const void* wimg;         // bf16 [14][2][64][8]
+  const float* scale;
+  const float* shift;
+  const float* bias;
+  __nv_bfloat16* out;
+  int N, C, OH, OW, PH, PW;
+  int tiles_h, tiles_w, num_units;
+  int y, out_cb_off, out_cb_total;
+  int relu;
+  uint32_t raw_bytes;       // 44*37*C*4
+  int dbg;                  // NEOB200_STEM_DBG: 1 no MMAs, 2 no TMEM loads, 4 no TMA
+};
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+__device__ __forceinline__ void unit_origin(const StemParams& p, int u, int& n, int& p0, int& q0) {
+  const int tw = u % p.tiles_w;
+  const int t = u / p.tiles_w;
+  const int th = t % p.tiles_h;
+  n = t / p.tiles_h;
+  p0 = th * kPool;
+  q0 = tw * kPool;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __grid_constant__ StemParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (sbase - smem_u32(smem_raw));
+  // layout: weights | ctile x2 | raw ring | patch x2 | params | barriers
+  const uint32_t sW = sbase;
+  const uint32_t sCt = sW + kWBytes;
+  const uint32_t sRaw = sCt + 2 * kCtileBytes;
+  const uint32_t raw_slot = (p.raw_bytes + 127u) & ~127u;
+  const uint32_t sPatch = sRaw + kRawStages * raw_slot;
+  const uint32_t sPar = sPatch + 2 * kPatchSlot;
+  const uint32_t sBar = sPar + 3 * 64 * 4;
+  auto raw_full = [&](int i) { return sBar + 8u * i; };
+  auto raw_empty = [&](int i) { return sBar + 32u + 8u * i; };
+  auto patch_full = [&](int i) { return sBar + 64u + 8u * i; };
+  auto patch_empty = [&](int i) { return sBar + 80u + 8u * i; };
+  auto tfull = [&](int i) { return sBar + 96u + 8u * i; };
+  auto tempty = [&](int i) { return sBar + 128u + 8u * i; };
+  const uint32_t wbar = sBar + 160u;
+  const uint32_t tslot = sBar + 168u;
+  float* par = reinterpret_cast<float*>(gbase + (sPar - sbase));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&p.tmX);
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(raw_full(i), 1);
+      mbar_init(raw_empty(i), 2);       // two converter warps
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(patch_full(i), 2);
+      mbar_init(patch_empty(i), 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(tfull(i), 1);
+      mbar_init(tempty(i), 8);          // eight epilogue warps
+    }
+    mbar_init(wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tslot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tslot - sbase));
+  neo_pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights are static (packed at load time): fetch before the PDL wait
+      mbar_arrive_expect_tx(wbar, kWBytes);
+      bulk_load(sW, p.wimg, kWBytes, wbar);
+      neo_pdl_wait();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        int n, p0, q0;
+        unit_origin(p, u, n, p0, q0);
+        mbar_wait(raw_empty(s), ph ^ 1u);
+        if (p.dbg & 4) {
+          mbar_arrive(raw_full(s));
+        } else {
+        mbar_arrive_expect_tx(raw_full(s), p.raw_bytes);
+        // input origin: conv row 2*p0 - 1 -> input row 2*(2*p0 - 1) - 3;
+        // columns from 4*q0 - 5 - kColOff (16-byte aligned)
+        tma_load_3d(sRaw + s * raw_slot, &p.tmX, raw_full(s), 4 * q0 - 8, 4 * p0 - 5, n * p.C);
+        }
+        if (++s == kRawStages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(1u, 128, 64);
+      // descriptors: A no-swizzle K-major, LBO 16 B, SBO two patch rows;
+      // B [step][chunk][k][8]: LBO 1024 B (chunk), SBO 128 B (8 k rows)
+      const uint64_t a0 = umma_smem_desc(sPatch, 16, 2 * kPitch, 0);
+      const uint64_t b0 = umma_smem_desc(sW, 1024, 128, 0);
+      const uint32_t alo0 = (uint32_t)a0, ahi = (uint32_t)(a0 >> 32);
+      const uint32_t blo0 = (uint32_t)b0, bhi = (uint32_t)(b0 >> 32);
+      mbar_wait(wbar, 0);
+      int it = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+        const int pb = it & 1, a = it & 3;
+        mbar_wait(patch_full(pb), (uint32_t)(it >> 1) & 1u);
+        mbar_wait(tempty(a), ((uint32_t)(it >> 2) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t abase = alo0 + (uint32_t)(pb * kPatchSlot) / 16u;
+#pragma unroll
+        for (int j = 0; j < 2 && !(p.dbg & 1); ++j) {
+          const uint32_t d = tmem_base + (uint32_t)(a * 128 + j * 64);
+#pragma unroll
+          for (int t = 0; t < kSteps; ++t) {
+            const int r = t >> 1, q = t & 1;
+            const uint32_t alo = abase + (uint32_t)(r * kPitch + 32 * q + 128 * j) / 16u;
+            const uint32_t blo = blo0 + (uint32_t)(t * 2048) / 16u;
+            asm volatile(
+                "{\n\t.reg .pred pa;\n\t.reg .b64 ad, bd;\n\t"
+                "setp.ne.b32 pa, %6, 0;\n\t"
+                "mov.b64 ad, {%1, %2};\n\t"
+                "mov.b64 bd, {%3, %4};\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %5, pa;\n\t}" ::"r"(d),
+                "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(t == 0 ? 0u : 1u)
+                : "memory");
+          }
+        }
+        umma_commit(patch_empty(pb));
+        umma_commit(tfull(a));
+      }
+    }
+  } else if (warp < 4) {
+    // ---- converters: f32 [c][37][44] -> bf16 [37][38][4] ----
+    const int ctid = threadIdx.x - 64;
+    const int C = p.C;
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      const int pb = it & 1;
+      mbar_wait(raw_full(s), ph);
+      mbar_wait(patch_empty(pb), ((uint32_t)(it >> 1) & 1u) ^ 1u);
+      const float* raw = reinterpret_cast<const float*>(gbase + (sRaw + s * raw_slot - sbase));
+      uint8_t* patch = gbase + (sPatch + pb * kPatchSlot - sbase);
+      constexpr int plane = kBoxW * kBoxH;
+      for (int idx = ctid; idx < kBoxH * kPatchCols; idx += 64) {
+        const int row = idx / kPatchCols, col = idx - row * kPatchCols;
+        const float* rp = raw + row * kBoxW + col + kColOff;
+        const float v0 = rp[0];
+        const float v1 = C > 1 ? rp[plane] : 0.f;
+        const float v2 = C > 2 ? rp[2 * plane] : 0.f;
+        const float v3 = C > 3 ? rp[3 * plane] : 0.f;
+        *reinterpret_cast<uint2*>(patch + row * kPitch + col * 8) =
+            make_uint2(pack_bf16x2(v0, v1), pack_bf16x2(v2, v3));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(patch_full(pb));
+        mbar_arrive(raw_empty(s));
+      }
+      if (++s == kRawStages) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  } else {
+    // ---- epilogue: 8 warps; warp covers TMEM lane quarter q of M tile j ----
+    const int ew = warp - 4;
+    const int q = warp & 3;
+    const int j = ew >> 2;
+    const int etid = threadIdx.x - 128;
+    neo_pdl_wait();
+    if (etid < 64) {
+      par[etid] = p.scale ? p.scale[etid] : 1.f;
+      par[64 + etid] = p.shift ? p.shift[etid] : 0.f;
+      par[128 + etid] = p.bias ? p.bias[etid] : 0.f;
+    }
+    named_bar_sync(1, 256);
+    const int m = q * 32 + lane;            // accumulator row = conv pixel (g, i)
+    const int g = m >> 3;
+    const int i = (m & 7) + 8 * j;
+    const uint32_t relu_bits = p.relu ? 1u : 0u;
+    int it = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      int n, p0, q0;
+      unit_origin(p, u, n, p0, q0);
+      const int a = it & 3;
+      mbar_wait(tfull(a), (uint32_t)(it >> 2) & 1u);
+      tc_fence_after();
+      uint8_t* ct = gbase + (sCt + (it & 1) * kCtileBytes - sbase);
+      uint8_t* row_base = ct + (g * 16 + i) * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 128 + j * 64);
+#pragma unroll
+      for (int c16 = 0; c16 < 4; ++c16) {
+        uint32_t v[16];
+        if (p.dbg & 2) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0u;
+        } else {
+          tmem_ld16(taddr + c16 * 16, v);
+          tmem_ld_wait_regs(v);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = c16 * 16 + h * 8 + 2 * e;
+            const float f0 = fmaf(__uint_as_float(v[h * 8 + 2 * e]), par[k], par[64 + k]) + par[128 + k];
+            const float f1 =
+                fmaf(__uint_as_float(v[h * 8 + 2 * e + 1]), par[k + 1], par[64 + k + 1]) + par[128 + k + 1];
+            if (relu_bits)
+              asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f0), "f"(f1));
+            else
+              asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f0), "f"(f1));
+          }
+          const int chunk = c16 * 2 + h;
+          *reinterpret_cast<uint4*>(row_base + ((chunk ^ (i & 7)) << 4)) =
+              make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(a));
+      named_bar_sync(1, 256);               // conv tile complete
+      // 3x3/2 max pool over the conv tile: item = (pooled row, col, 8-ch chunk)
+      const int cr0 = 2 * p0 - 1, cc0 = 2 * q0 - 1;
+      for (int item = etid; item < kPool * kPool * 8; item += 256) {
+        const int pp = item / 56, rem = item - pp * 56;
+        const int pq = rem >> 3, chunk = rem & 7;
+        const int P = p0 + pp, Q = q0 + pq;
+        if (P >= p.PH || Q >= p.PW) continue;
+        uint32_t b0 = 0xFF80FF80u, b1 = b0, b2 = b0, b3 = b0;   // -inf pairs
+#pragma unroll
+        for (int dg = 0; dg < 3; ++dg) {
+          const int gg = 2 * pp + dg;
+          const int crow = cr0 + gg;
+          if (crow < 0 || crow >= p.OH) continue;
+#pragma unroll
+          for (int di = 0; di < 3; ++di) {
+            const int ii = 2 * pq + di;
+            const int ccol = cc0 + ii;
+            if (ccol < 0 || ccol >= p.OW) continue;
+            const uint4 v = *reinterpret_cast<const uint4*>(ct + (gg * 16 + ii) * 128 +
+                                                            ((chunk ^ (ii & 7)) << 4));
+            b0 = bmax2(b0, v.x);
+            b1 = bmax2(b1, v.y);
+            b2 = bmax2(b2, v.z);
+            b3 = bmax2(b3, v.w);
+          }
+        }
+        const int k = chunk * 8;
+        const int kb = k / p.y, j0 = k - kb * p.y;
+        const size_t off =
+            ((((size_t)n * p.out_cb_total + p.out_cb_off + kb) * p.PH + P) * p.PW + Q) * p.y + j0;
+        *reinterpret_cast<uint4*>(p.out + off) = make_uint4(b0, b1, b2, b3);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+__global__ void stem_pack_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ img,
+                                 int C) {
+  // img[t][h][k][e]: step t = (r, q), chunk h, element e -> tap s = 4q + 2h + e/4, channel e%4
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= kSteps * 2 * 64 * 8) return;
+  const int e = idx & 7, k = (idx >> 3) & 63, h = (idx >> 9) & 1, t = idx >> 10;
+  const int r = t >> 1, q = t & 1;
+  const int s = 4 * q + 2 * h + (e >> 2), c = e & 3;
+  const float v = (s < 7 && c < C) ? w[((k * C + c) * 7 + r) * 7 + s] : 0.f;
+  img[idx] = __float2bfloat16_rn(v);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+}  // namespace
+
+extern "C" int neo_stem_pack_weights(const float* w_kcrs, void* img, int64_t k, int64_t c,
+                                     int64_t r, int64_t s, neo_stream_t stream) {
+  NEO_CHECK_ARG(w_kcrs && img, NEO_ERR_INVALID_ARG, "null pointer");
+  NEO_CHECK_ARG(k == 64 && r == 7 && s == 7 && c >= 1 && c <= 4, NEO_ERR_UNSUPPORTED,
+                "stem image needs K=64, 7x7, C<=4 (got K=%lld C=%lld %lldx%lld)", (long long)k,
+                (long long)c, (long long)r, (long long)s);
+  const int total = kSteps * 2 * 64 * 8;
+  neo_launch(stem_pack_kernel, dim3((total + 255) / 256), dim3(256), 0,
+             static_cast<cudaStream_t>(stream), w_kcrs, static_cast<__nv_bfloat16*>(img), (int)c);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int64_t neo_stem_weight_bytes(void) { return kWBytes; }
+
+extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
+                                  const float* scale, const float* shift, const float* bias,
+                                  int relu, int64_t n, int64_t c, int64_t h, int64_t w, int y,
+                                  int out_cb_offset, int out_cb_total, neo_stream_t stream) {
+  NEO_CHECK_ARG(x && wimg && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(n >= 1 && c >= 1 && c <= 4 && h >= 1 && w >= 1, NEO_ERR_SHAPE_MISMATCH,
+                "stem needs 1..4 input channels (C=%lld)", (long long)c);
+  NEO_CHECK_ARG(w % 4 == 0, NEO_ERR_UNSUPPORTED, "stem input width %lld must be a multiple of 4",
+                (long long)w);
+  NEO_CHECK_ARG(y == 8 || y == 16 || y == 32 || y == 64, NEO_ERR_UNSUPPORTED,
+                "stem output block %d not in {8,16,32,64}", y);
+  const int64_t OH = (h + 6 - 7) / 2 + 1, OW = (w + 6 - 7) / 2 + 1;
+  const int64_t PH = (OH + 2 - 3) / 2 + 1, PW = (OW + 2 - 3) / 2 + 1;
+  NEO_CHECK_ARG(OH >= 1 && OW >= 1 && PH >= 1 && PW >= 1, NEO_ERR_SHAPE_MISMATCH, "empty stem output");
+  const int cbt = out_cb_total > 0 ? out_cb_total : 64 / y;
+  NEO_CHECK_ARG(out_cb_offset >= 0 && out_cb_offset + 64 / y <= cbt, NEO_ERR_SHAPE_MISMATCH,
+                "output window [%d, %d) outside %d blocks", out_cb_offset, out_cb_offset + 64 / y,
+                cbt);
+  auto encode = encode_fn();
+  NEO_CHECK_ARG(encode != nullptr, NEO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  StemParams kp;
+  memset(&kp, 0, sizeof(kp));
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)(n * c)};
+    cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)h * w * 4};
+    cuuint32_t box[3] = {(cuuint32_t)kBoxW, (cuuint32_t)kBoxH, (cuuint32_t)c};
+
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = encode(&kp.tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "stem tensor map encode failed (%d)", (int)r);
+  }
+  kp.wimg = wimg;
+  kp.scale = scale;
+  kp.shift = shift;
+  kp.bias = bias;
+  kp.out = static_cast<__nv_bfloat16*>(out);
+  kp.N = (int)n;
+  kp.C = (int)c;
+  kp.OH = (int)OH;
+  kp.OW = (int)OW;
+  kp.PH = (int)PH;
+  kp.PW = (int)PW;
+  kp.tiles_h = (int)neo_ceil_div(PH, kPool);
+  kp.tiles_w = (int)neo_ceil_div(PW, kPool);
+  const int64_t units = n * kp.tiles_h * kp.tiles_w;
+  NEO_CHECK_ARG(units < (1ll << 31), NEO_ERR_UNSUPPORTED, "too many stem tiles");
+  kp.num_units = (int)units;
+  kp.y = y;
+  kp.out_cb_off = out_cb_offset;
+  kp.out_cb_total = cbt;
+  kp.relu = relu;
+  kp.raw_bytes = (uint32_t)(kBoxW * kBoxH * c * 4);
+  {
+    static const char* dbg = getenv("NEOB200_STEM_DBG");
+    kp.dbg = dbg ? atoi(dbg) : 0;
+  }
+  const uint32_t raw_slot = (kp.raw_bytes + 127u) & ~127u;
+  const size_t smem = 1024 + kWBytes + 2 * kCtileBytes + kRawStages * raw_slot + 2 * kPatchSlot +
+                      3 * 64 * 4 + 256;
+  static bool attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    NEO_CUDA_TRY(cudaFuncSetAttribute(stem_conv_pool_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_done[dev & 63] = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(units, sms);
+  neo_launch(stem_conv_pool_kernel, dim3(grid), dim3(kThreads), smem,
+             static_cast<cudaStream_t>(stream), kp);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}

@@ -234,3 +234,27 @@ def stem_fold(src: torch.Tensor, dst: torch.Tensor, n, c, h, w, s, stride_w, pad
     """NCHW f32 -> horizontally folded NCHW[xf]c (see neo_stem_fold)."""
     L.call("neo_stem_fold", _ptr(src), _ptr(dst), dtype_code(dst), n, c, h, w, s, stride_w,
            pad_w, ow, xf, flags, stream_handle(stream))
+
+
+def pack_stem_weights(w_kcrs: torch.Tensor, stream=None) -> torch.Tensor:
+    """KCRS f32 (64, C<=4, 7, 7) device weights -> the fused stem's bf16
+    tensor-core image (neo_stem_pack_weights)."""
+    w = w_kcrs.contiguous().float()
+    k, c, r, s = w.shape
+    img = torch.empty(L.load().neo_stem_weight_bytes() // 2, dtype=torch.bfloat16,
+                      device=w.device)
+    L.call("neo_stem_pack_weights", _ptr(w), _ptr(img), k, c, r, s, stream_handle(stream))
+    return img
+
+
+def stem_conv_pool(x: torch.Tensor, wimg: torch.Tensor, out: torch.Tensor, n, c, h, w, y,
+                   scale=None, shift=None, bias=None, relu=True, out_cb=(0, 0),
+                   stream=None) -> None:
+    """Fused stem: maxpool3x3/2(relu(conv7x7/2(x) * scale + shift + bias))
+    from NCHW f32 straight into bf16 NCHW[y]c (neo_stem_conv_pool)."""
+    if x.dtype != torch.float32 or out.dtype != torch.bfloat16:
+        raise E.InputMismatch("stem_conv_pool takes f32 input and writes bf16")
+    opt = lambda t: _ptr(t) if t is not None else None
+    L.call("neo_stem_conv_pool", _ptr(x), _ptr(wimg), _ptr(out), opt(scale), opt(shift),
+           opt(bias), int(bool(relu)), n, c, h, w, y, out_cb[0], out_cb[1],
+           stream_handle(stream))

@@ -29,6 +29,7 @@ raises.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -227,6 +228,18 @@ class DeviceProgram:
                 info = self._stem_fold_info(nid)
                 if info:
                     self.stem_fold[nid] = info
+        # image stem (7x7/2 conv + relu + 3x3/2 max pool over a <=4-channel
+        # input) as one fused launch in bf16 mode: neither the packed input
+        # nor the conv map is materialised (neo_stem_conv_pool)
+        self.fused_stem: dict[int, tuple[int, int]] = {}   # pool id -> (conv, input)
+        if self.mode == "bf16" and not os.environ.get("NEOB200_NO_FUSED_STEM"):
+            for t, info in list(self.stem_fold.items()):
+                found = self._fused_stem_info(t, info)
+                if found:
+                    cv, mp, src = found
+                    self.fused_stem[mp] = (cv, src)
+                    self.skip.update((t, cv))
+                    del self.stem_fold[t]
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -278,6 +291,10 @@ class DeviceProgram:
             node = self.g.nodes[nid]
             for src, _ in node.inputs:
                 tgt = self._storage(self.pro_src.get(src, src))
+                if tgt is not None:
+                    tgt.last = max(tgt.last, self.step[nid])
+            if nid in self.fused_stem:      # the fused stem reads the graph input
+                tgt = self._storage(self.fused_stem[nid][1])
                 if tgt is not None:
                     tgt.last = max(tgt.last, self.step[nid])
             fused_src = self.fused_bn_relu.get(nid, self.fused_dense_relu.get(nid))
@@ -373,6 +390,38 @@ class DeviceProgram:
         if v.win is None:
             return 0, v.shape[1]
         return v.win[1], self.vals[v.win[0]].shape[1]
+
+    def _fused_stem_info(self, t: int, info: dict):
+        """(conv, pool, input) if stem transform ``t`` feeds exactly one
+        7x7/2 pad-3 conv with 64 outputs and no residual whose only consumer
+        is a 3x3/2 pad-1 max pool writing NCHW[y]c."""
+        g = self.g
+        if info["S"] != 7 or info["sw"] != 2 or info["pw"] != 3 or info["w"] % 4:
+            return None
+        us = self.users[t]
+        if len(us) != 1:
+            return None
+        cv = g.nodes[us[0]]
+        wt = g.nodes[cv.inputs[1][0]].attrs["value"]
+        if wt.ndim == 6:                    # pre-packed KCRS[x]c[y]k
+            wt = host_unpack_kcrs(wt)
+        epi = cv.attrs.get("epilogue") or {}
+        if (wt.ndim != 4 or tuple(wt.shape) != (64, info["C"], 7, 7) or epi.get("residual")
+                or len(cv.inputs) > 3 or hw_pair(cv.attrs["stride"]) != (2, 2)
+                or hw_pair(cv.attrs["pad"]) != (3, 3)):
+            return None
+        cus = self.users[cv.id]
+        if len(cus) != 1 or cv.id in g.outputs or cv.id in self.keep:
+            return None
+        mp = g.nodes[cus[0]]
+        if (mp.kind != OpKind.MaxPool or hw_pair(mp.attrs["window"]) != (3, 3)
+                or hw_pair(mp.attrs["stride"]) != (2, 2)
+                or hw_pair(mp.attrs.get("pad", 0)) != (1, 1)):
+            return None
+        lay = self.specs[mp.id].layout
+        if lay.tag != "NCHWc" or lay.x not in (8, 16, 32, 64):
+            return None
+        return cv.id, mp.id, g.nodes[t].inputs[0][0]
 
     def _stem_fold_info(self, nid) -> dict | None:
         """Fold parameters if ``nid`` packs a few-channel graph input that
@@ -528,6 +577,8 @@ class DeviceProgram:
             elif kind == OpKind.LayoutTransform:
                 if out.alias is None:
                     self._bind_transform(node, ins[0], out)
+            elif nid in self.fused_stem:
+                self._bind_stem(node, out)
             elif kind in (OpKind.MaxPool, OpKind.AvgPool):
                 self._bind_pool(node, ins[0], out)
             elif kind == OpKind.ReLU and nid in self.fused_dense_relu:
@@ -694,6 +745,37 @@ class DeviceProgram:
             "neo_layout_transform", D.dtype_code(src), D.dtype_code(dst), src.data_ptr(),
             dst.data_ptr(), 1, numel, 1, 1, L.NCHW_TAG, 1, L.NCHW_TAG, 1, 0,
             D.stream_handle(self.stream)), _nb(src) + _nb(dst))
+
+    def _bind_stem(self, pool_node, out: _Val):
+        """conv 7x7/2 (+ epilogue) -> max pool 3x3/2 of a <=4-channel image as
+        one neo_stem_conv_pool launch (reference: conv_blocked + _pool2d)."""
+        from . import device as D
+        g = self.g
+        cv_id, src_id = self.fused_stem[pool_node.id]
+        node = g.nodes[cv_id]
+        src = self.vals[src_id]
+        epi = dict(node.attrs.get("epilogue") or {})
+        bias = epi.get("bias")
+        if len(node.inputs) >= 3:           # executor.py:63-66: explicit bias input
+            b = g.nodes[node.inputs[2][0]].attrs["value"]
+            bias = b if bias is None else bias + b
+        scale, shift = epi.get("scale"), epi.get("shift")
+        if scale is None and shift is not None:
+            scale = np.ones(64, np.float32)
+        vec = lambda v: None if v is None else self._upload(np.asarray(v, np.float32))
+        t_scale, t_shift, t_bias = vec(scale), vec(shift), vec(bias)
+        w = g.nodes[node.inputs[1][0]].attrs["value"]
+        w = np.asarray(host_unpack_kcrs(w) if w.ndim == 6 else w, np.float32)
+        wimg = D.pack_stem_weights(self._upload(w))
+        self.weights.append(wimg)
+        n, c, h, wd = src.shape
+        x_t, o_t = src.tensor, out.tensor
+        y = out.layout.x
+        cb = self._window(out)
+        relu = bool(epi.get("relu"))
+        self._emit(f"stem{cv_id}_pool{pool_node.id}", lambda: D.stem_conv_pool(
+            x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream),
+            _nb(x_t) + _vb(out))
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
