@@ -23,16 +23,17 @@
 // 14 MMAs (M=128, N=64) per 16x8 conv tile.  Tap 7 and channel 3 carry zero
 // weights.  The weights are a resident 28 KB image [step][chunk][64 k][8].
 //
-// Warp roles (384 threads, persistent over units, one CTA per SM):
+// Warp roles (768 threads, persistent over units, one CTA per SM):
 //   warp 0      TMA producer: f32 patch box (44 cols x 37 rows x C planes,
 //               zero fill outside the image) into a 4-deep ring
 //   warp 1      TMEM allocator + single-thread MMA issuer (4 accumulators of
 //               2 x 64 columns)
-//   warps 2-3   converters: f32 planar box -> bf16 [row][col][4] patch
-//               (2-deep ring), then fence.proxy.async for the tensor core
-//   warps 4-11  epilogue: tcgen05.ld -> scale/shift/bias/relu -> bf16 conv
+//   warps 2-7   converters: f32 planar box -> bf16 [row][col][4] patch
+//               (4-deep ring), then fence.proxy.async for the tensor core
+//   warps 8-23  epilogue: tcgen05.ld -> scale/shift/bias/relu -> bf16 conv
 //               tile in shared memory (double buffered, XOR-swizzled 16-byte
-//               chunks) -> 3x3/2 max pool -> 16-byte global stores
+//               chunks; pixels outside the conv map stored as -inf) -> 3x3/2
+//               max pool -> 16-byte global stores
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -41,8 +42,11 @@
 
 namespace {
 
-constexpr int kThreads = 384;
-constexpr int kRawStages = 4;
+constexpr int kConvWarps = 6;                 // warps 2..7
+constexpr int kEpiThreads = 512;               // warps 8..23
+constexpr int kThreads = 64 + kConvWarps * 32 + kEpiThreads;
+constexpr int kRawStages = 4;                  // max f32 box ring depth
+constexpr int kPatchStages = 4;                // converted patches in flight
 // f32 input box per unit: 37 rows x 44 columns starting 8 columns left of
 // the conv tile's first tap (a TMA box must start on a 16-byte boundary of
 // its innermost dimension; a negative, unaligned start column faults), so
@@ -70,7 +74,9 @@ struct StemParams {
   int y, out_cb_off, out_cb_total;
   int relu;
   uint32_t raw_bytes;       // 44*37*C*4
-  int dbg;                  // NEOB200_STEM_DBG: 1 no MMAs, 2 no TMEM loads, 4 no TMA
+  int raw_stages;           // f32 box ring depth (4, 3 for C = 4)
+  int dbg;                  // NEOB200_STEM_DBG: 1 no MMAs, 2 no TMEM loads, 4 no TMA,
+                            // 8 no pooling, 16 no conversion, 32 phase clocks
 };
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
@@ -94,6 +100,10 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
   return r;
 }
 
+// NEOB200_STEM_DBG & 32: per-CTA phase clocks of the MMA thread and of
+// epilogue warp 8 (lane 0) -> neo_stem_dbg_clk
+__device__ unsigned long long g_stem_clk[148 * 8];
+
 __device__ __forceinline__ void unit_origin(const StemParams& p, int u, int& n, int& p0, int& q0) {
   const int tw = u % p.tiles_w;
   const int t = u / p.tiles_w;
@@ -112,17 +122,17 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
   const uint32_t sCt = sW + kWBytes;
   const uint32_t sRaw = sCt + 2 * kCtileBytes;
   const uint32_t raw_slot = (p.raw_bytes + 127u) & ~127u;
-  const uint32_t sPatch = sRaw + kRawStages * raw_slot;
-  const uint32_t sPar = sPatch + 2 * kPatchSlot;
+  const uint32_t sPatch = sRaw + p.raw_stages * raw_slot;
+  const uint32_t sPar = sPatch + kPatchStages * kPatchSlot;
   const uint32_t sBar = sPar + 3 * 64 * 4;
   auto raw_full = [&](int i) { return sBar + 8u * i; };
   auto raw_empty = [&](int i) { return sBar + 32u + 8u * i; };
   auto patch_full = [&](int i) { return sBar + 64u + 8u * i; };
-  auto patch_empty = [&](int i) { return sBar + 80u + 8u * i; };
-  auto tfull = [&](int i) { return sBar + 96u + 8u * i; };
-  auto tempty = [&](int i) { return sBar + 128u + 8u * i; };
-  const uint32_t wbar = sBar + 160u;
-  const uint32_t tslot = sBar + 168u;
+  auto patch_empty = [&](int i) { return sBar + 96u + 8u * i; };
+  auto tfull = [&](int i) { return sBar + 128u + 8u * i; };
+  auto tempty = [&](int i) { return sBar + 160u + 8u * i; };
+  const uint32_t wbar = sBar + 192u;
+  const uint32_t tslot = sBar + 200u;
   float* par = reinterpret_cast<float*>(gbase + (sPar - sbase));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -130,15 +140,15 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
     tma_prefetch_desc(&p.tmX);
     for (int i = 0; i < kRawStages; ++i) {
       mbar_init(raw_full(i), 1);
-      mbar_init(raw_empty(i), 2);       // two converter warps
+      mbar_init(raw_empty(i), kConvWarps);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(patch_full(i), 2);
+    for (int i = 0; i < kPatchStages; ++i) {
+      mbar_init(patch_full(i), kConvWarps);
       mbar_init(patch_empty(i), 1);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(tfull(i), 1);
-      mbar_init(tempty(i), 8);          // eight epilogue warps
+      mbar_init(tempty(i), kEpiThreads / 32);
     }
     mbar_init(wbar, 1);
     fence_mbar_init();
@@ -173,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         // columns from 4*q0 - 5 - kColOff (16-byte aligned)
         tma_load_3d(sRaw + s * raw_slot, &p.tmX, raw_full(s), 4 * q0 - 8, 4 * p0 - 5, n * p.C);
         }
-        if (++s == kRawStages) {
+        if (++s == p.raw_stages) {
           s = 0;
           ph ^= 1u;
         }
@@ -189,11 +199,16 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
       const uint32_t alo0 = (uint32_t)a0, ahi = (uint32_t)(a0 >> 32);
       const uint32_t blo0 = (uint32_t)b0, bhi = (uint32_t)(b0 >> 32);
       mbar_wait(wbar, 0);
+      const bool prof = (p.dbg & 32) != 0;
+      long long m_pf = 0, m_te = 0, m_is = 0;
       int it = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
-        const int pb = it & 1, a = it & 3;
-        mbar_wait(patch_full(pb), (uint32_t)(it >> 1) & 1u);
+        const int pb = it % kPatchStages, a = it & 3;
+        long long t0 = prof ? clock64() : 0;
+        mbar_wait(patch_full(pb), (uint32_t)(it / kPatchStages) & 1u);
+        if (prof) { const long long t = clock64(); m_pf += t - t0; t0 = t; }
         mbar_wait(tempty(a), ((uint32_t)(it >> 2) & 1u) ^ 1u);
+        if (prof) { const long long t = clock64(); m_te += t - t0; t0 = t; }
         tc_fence_after();
         const uint32_t abase = alo0 + (uint32_t)(pb * kPatchSlot) / 16u;
 #pragma unroll
@@ -216,23 +231,31 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         }
         umma_commit(patch_empty(pb));
         umma_commit(tfull(a));
+        if (prof) m_is += clock64() - t0;
+      }
+      if (prof) {
+        g_stem_clk[blockIdx.x * 8 + 0] = m_pf;
+        g_stem_clk[blockIdx.x * 8 + 1] = m_te;
+        g_stem_clk[blockIdx.x * 8 + 2] = m_is;
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 2 + kConvWarps) {
     // ---- converters: f32 [c][37][44] -> bf16 [37][38][4] ----
     const int ctid = threadIdx.x - 64;
     const int C = p.C;
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
+    const int nconv = (p.dbg & 16) ? 0 : kBoxH * kPatchCols;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
-      const int pb = it & 1;
+      const int pb = it % kPatchStages;
       mbar_wait(raw_full(s), ph);
-      mbar_wait(patch_empty(pb), ((uint32_t)(it >> 1) & 1u) ^ 1u);
+      mbar_wait(patch_empty(pb), ((uint32_t)(it / kPatchStages) & 1u) ^ 1u);
       const float* raw = reinterpret_cast<const float*>(gbase + (sRaw + s * raw_slot - sbase));
       uint8_t* patch = gbase + (sPatch + pb * kPatchSlot - sbase);
       constexpr int plane = kBoxW * kBoxH;
-      for (int idx = ctid; idx < kBoxH * kPatchCols; idx += 64) {
+#pragma unroll 4
+      for (int idx = ctid; idx < nconv; idx += kConvWarps * 32) {
         const int row = idx / kPatchCols, col = idx - row * kPatchCols;
         const float* rp = raw + row * kBoxW + col + kColOff;
         const float v0 = rp[0];
@@ -248,40 +271,52 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         mbar_arrive(patch_full(pb));
         mbar_arrive(raw_empty(s));
       }
-      if (++s == kRawStages) {
+      if (++s == p.raw_stages) {
         s = 0;
         ph ^= 1u;
       }
     }
   } else {
-    // ---- epilogue: 8 warps; warp covers TMEM lane quarter q of M tile j ----
-    const int ew = warp - 4;
+    // ---- epilogue: 16 warps; warp = (TMEM lane quarter q, M tile j, column
+    // half) drains 32 accumulator columns of 32 conv pixels ----
+    const int ew = warp - 2 - kConvWarps;
     const int q = warp & 3;
-    const int j = ew >> 2;
-    const int etid = threadIdx.x - 128;
+    const int j = (ew >> 2) & 1;
+    const int half = ew >> 3;
+    const int etid = threadIdx.x - 64 - kConvWarps * 32;
     neo_pdl_wait();
     if (etid < 64) {
       par[etid] = p.scale ? p.scale[etid] : 1.f;
       par[64 + etid] = p.shift ? p.shift[etid] : 0.f;
       par[128 + etid] = p.bias ? p.bias[etid] : 0.f;
     }
-    named_bar_sync(1, 256);
+    named_bar_sync(1, kEpiThreads);
+    const bool affine = p.scale != nullptr || p.shift != nullptr;
     const int m = q * 32 + lane;            // accumulator row = conv pixel (g, i)
     const int g = m >> 3;
     const int i = (m & 7) + 8 * j;
     const uint32_t relu_bits = p.relu ? 1u : 0u;
+    const bool prof = (p.dbg & 32) != 0 && warp == 2 + kConvWarps && lane == 0;
+    long long t0 = 0, c_wait = 0, c_math = 0, c_bar = 0, c_pool = 0;
     int it = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
       int n, p0, q0;
       unit_origin(p, u, n, p0, q0);
+      const int cr0 = 2 * p0 - 1, cc0 = 2 * q0 - 1;
+      // conv pixels outside the conv map hold -inf: the pool below then needs
+      // no bounds checks (reference -inf padding, executor.py:103-128)
+      const bool valid = cr0 + g >= 0 && cr0 + g < p.OH && cc0 + i >= 0 && cc0 + i < p.OW;
       const int a = it & 3;
+      if (prof) t0 = clock64();
       mbar_wait(tfull(a), (uint32_t)(it >> 2) & 1u);
+      if (prof) { const long long t = clock64(); c_wait += t - t0; t0 = t; }
       tc_fence_after();
       uint8_t* ct = gbase + (sCt + (it & 1) * kCtileBytes - sbase);
       uint8_t* row_base = ct + (g * 16 + i) * 128;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 128 + j * 64);
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) +
+                             (uint32_t)(a * 128 + j * 64 + half * 32);
 #pragma unroll
-      for (int c16 = 0; c16 < 4; ++c16) {
+      for (int c16 = 0; c16 < 2; ++c16) {
         uint32_t v[16];
         if (p.dbg & 2) {
 #pragma unroll
@@ -292,19 +327,35 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+          const int k0 = half * 32 + c16 * 16 + h * 8;
+          float f[8];
+          const float4 b0 = *reinterpret_cast<const float4*>(par + 128 + k0);
+          const float4 b1 = *reinterpret_cast<const float4*>(par + 128 + k0 + 4);
+          const float bi[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          if (affine) {
+            const float4 s0 = *reinterpret_cast<const float4*>(par + k0);
+            const float4 s1 = *reinterpret_cast<const float4*>(par + k0 + 4);
+            const float4 t0 = *reinterpret_cast<const float4*>(par + 64 + k0);
+            const float4 t1 = *reinterpret_cast<const float4*>(par + 64 + k0 + 4);
+            const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const float sh[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = fmaf(__uint_as_float(v[h * 8 + e]), sc[e], sh[e]) + bi[e];
+          } else {
+            // identity scale/shift: fma(v, 1, 0) == v
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[h * 8 + e]) + bi[e];
+          }
           uint32_t o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int k = c16 * 16 + h * 8 + 2 * e;
-            const float f0 = fmaf(__uint_as_float(v[h * 8 + 2 * e]), par[k], par[64 + k]) + par[128 + k];
-            const float f1 =
-                fmaf(__uint_as_float(v[h * 8 + 2 * e + 1]), par[k + 1], par[64 + k + 1]) + par[128 + k + 1];
             if (relu_bits)
-              asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f0), "f"(f1));
+              asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f[2 * e]), "f"(f[2 * e + 1]));
             else
-              asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f0), "f"(f1));
+              asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(o[e]) : "f"(f[2 * e]), "f"(f[2 * e + 1]));
+            if (!valid) o[e] = 0xFF80FF80u;
           }
-          const int chunk = c16 * 2 + h;
+          const int chunk = k0 >> 3;
           *reinterpret_cast<uint4*>(row_base + ((chunk ^ (i & 7)) << 4)) =
               make_uint4(o[0], o[1], o[2], o[3]);
         }
@@ -312,10 +363,11 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(a));
-      named_bar_sync(1, 256);               // conv tile complete
+      if (prof) { const long long t = clock64(); c_math += t - t0; t0 = t; }
+      named_bar_sync(1, kEpiThreads);       // conv tile complete
+      if (prof) { const long long t = clock64(); c_bar += t - t0; t0 = t; }
       // 3x3/2 max pool over the conv tile: item = (pooled row, col, 8-ch chunk)
-      const int cr0 = 2 * p0 - 1, cc0 = 2 * q0 - 1;
-      for (int item = etid; item < kPool * kPool * 8; item += 256) {
+      for (int item = etid; item < ((p.dbg & 8) ? 0 : kPool * kPool * 8); item += kEpiThreads) {
         const int pp = item / 56, rem = item - pp * 56;
         const int pq = rem >> 3, chunk = rem & 7;
         const int P = p0 + pp, Q = q0 + pq;
@@ -323,14 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         uint32_t b0 = 0xFF80FF80u, b1 = b0, b2 = b0, b3 = b0;   // -inf pairs
 #pragma unroll
         for (int dg = 0; dg < 3; ++dg) {
-          const int gg = 2 * pp + dg;
-          const int crow = cr0 + gg;
-          if (crow < 0 || crow >= p.OH) continue;
 #pragma unroll
           for (int di = 0; di < 3; ++di) {
-            const int ii = 2 * pq + di;
-            const int ccol = cc0 + ii;
-            if (ccol < 0 || ccol >= p.OW) continue;
+            const int gg = 2 * pp + dg, ii = 2 * pq + di;
             const uint4 v = *reinterpret_cast<const uint4*>(ct + (gg * 16 + ii) * 128 +
                                                             ((chunk ^ (ii & 7)) << 4));
             b0 = bmax2(b0, v.x);
@@ -345,6 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
             ((((size_t)n * p.out_cb_total + p.out_cb_off + kb) * p.PH + P) * p.PW + Q) * p.y + j0;
         *reinterpret_cast<uint4*>(p.out + off) = make_uint4(b0, b1, b2, b3);
       }
+      if (prof) { const long long t = clock64(); c_pool += t - t0; t0 = t; }
+    }
+    if (prof) {
+      g_stem_clk[blockIdx.x * 8 + 3] = c_wait;
+      g_stem_clk[blockIdx.x * 8 + 4] = c_math;
+      g_stem_clk[blockIdx.x * 8 + 5] = c_bar;
+      g_stem_clk[blockIdx.x * 8 + 6] = c_pool;
     }
   }
   __syncthreads();
@@ -457,8 +511,10 @@ extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
     kp.dbg = dbg ? atoi(dbg) : 0;
   }
   const uint32_t raw_slot = (kp.raw_bytes + 127u) & ~127u;
-  const size_t smem = 1024 + kWBytes + 2 * kCtileBytes + kRawStages * raw_slot + 2 * kPatchSlot +
-                      3 * 64 * 4 + 256;
+  const size_t fixed = 1024 + kWBytes + 2 * kCtileBytes + kPatchStages * kPatchSlot + 3 * 64 * 4 + 256;
+  kp.raw_stages = (int)std::min<size_t>(kRawStages, (227 * 1024 - fixed) / raw_slot);
+  NEO_CHECK_ARG(kp.raw_stages >= 2, NEO_ERR_UNSUPPORTED, "stem input ring does not fit");
+  const size_t smem = fixed + (size_t)kp.raw_stages * raw_slot;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -474,4 +530,8 @@ extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
              static_cast<cudaStream_t>(stream), kp);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int neo_stem_dbg_clk(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_stem_clk, n * sizeof(unsigned long long));
 }
