@@ -194,7 +194,10 @@ def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind
     events on the executor stream; returns (roofline dict, conv share of
     the step)."""
     from paper_1809_02697_b200.timing import graph_time
-    conv_idx = [i for i, n in enumerate(prog.launch_names) if n.startswith("conv")]
+    # conv launches: the tensor-core convs and the fused image stem (its conv
+    # FLOPs are part of flops_per_step; it also runs the stem's max pool)
+    conv_idx = [i for i, n in enumerate(prog.launch_names)
+                if n.startswith("conv") or (n.startswith("stem") and "_pool" in n)]
     cset = set(conv_idx)
     step_s = graph_time(prog, lambda i: True, steps, flush)
     rest_s = graph_time(prog, lambda i: i not in cset, steps, flush)
@@ -221,7 +224,8 @@ def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind
     mem_ops["frac_of_measured"] = mem_ops["achieved_GBps"] / mem_ops["peak_measured_GBps"]
     roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
             "frac": achieved / pk, "traffic": traffic,
-            "kernel": "conv_tc_kernel (all %d conv launches of one step)" % len(conv_idx),
+            "kernel": "conv_tc_kernel + stem_conv_pool_kernel (all %d conv launches of one step)"
+                      % len(conv_idx),
             "conv_ms_per_step": conv_s * 1e3, "peak_source": f"{peak_kind} bf16 sustained"}
     roof["memory_bound_ops"] = mem_ops
     return roof, conv_s / float(np.median(step_times))

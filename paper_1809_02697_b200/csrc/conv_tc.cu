@@ -73,6 +73,12 @@ struct ConvTCParams {
   uint32_t stage_out; // bytes of one staging buffer (128 rows * rowb_out)
   uint32_t out_box_bytes;
   int nslot;          // staging slots per epilogue group (tma_epi)
+  // residual prefetch (tma_epi with a residual, nslot >= 2 * blocks per
+  // tile): a group's slots form two sets used by alternate tiles; right
+  // after a tile's store is committed the group issues the residual loads of
+  // its next tile into the other set, so their HBM latency overlaps this
+  // tile's store drain and the next accumulator wait
+  int res_pf;
   // halo mode (stride-1 convs): tiles span the padded output width
   // BW = OW + S - 1; a pipeline slice is one (kernel row r, channel block)
   // input band, loaded once; the S horizontal taps read it through
@@ -348,8 +354,19 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
       }
     }
   };
+  // two 16-column TMEM loads in flight per wait (hides the load latency)
+  int c = c_begin;
 #pragma unroll 1
-  for (int c = c_begin; c < nchunk; c += c_step) {
+  for (; c + c_step < nchunk; c += 2 * c_step) {
+    uint32_t v[16], w[16];
+    tmem_ld16(tcol + c * 16, v);
+    tmem_ld16(tcol + (c + c_step) * 16, w);
+    tmem_ld_wait_regs(v);
+    tmem_ld_wait_regs(w);
+    finish(v, c);
+    finish(w, c + c_step);
+  }
+  if (c < nchunk) {
     uint32_t v[16];
     tmem_ld16(tcol + c * 16, v);
     tmem_ld_wait_regs(v);
@@ -1000,21 +1017,28 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         // results overwrite them and leave with TMA bulk stores.
         const bool has_res = p.res != nullptr;
         const int nblk = ncols / p.y;
-        const uint32_t sgrp = sO + grp * p.nslot * p.stage_out;
+        const bool pf = p.res_pf != 0;
+        const int lt = it / p.ngroups;            // this group's tile counter
+        const int set = pf ? (lt & 1) : 0;        // prefetch: alternate slot sets
+        const uint32_t sgrp = sO + (grp * p.nslot + set * (p.nslot / 2)) * p.stage_out;
         uint8_t* sgrp_gen = gen_base + (sgrp - sA);
+        const uint32_t rbar = res_bar(grp, set);
+        auto load_res = [&](uint32_t dst, uint32_t bar, int b0, int cnt, int tow0, int toh0, int tk0,
+                            int tn0) {
+          mbar_arrive_expect_tx(bar, cnt * p.out_box_bytes);
+          for (int i = 0; i < cnt; ++i)
+            tma_load_5d(dst + i * p.stage_out, &p.tmR, bar, 0, tow0, toh0,
+                        p.res_cb_off + (tk0 + (b0 + i) * p.y) / p.y, tn0);
+        };
         auto issue_res = [&](int b0, int cnt) {
           if (!leader) return;
           bulk_wait_read<0>();              // previous stores left the slots
-          if (has_res) {
-            mbar_arrive_expect_tx(res_bar(grp, 0), cnt * p.out_box_bytes);
-            for (int i = 0; i < cnt; ++i)
-              tma_load_5d(sgrp + i * p.stage_out, &p.tmR, res_bar(grp, 0), 0, ow0, oh0,
-                          p.res_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
-          }
+          if (has_res) load_res(sgrp, rbar, b0, cnt, ow0, oh0, k0, n0);
         };
         if (leader) TRACE(20 + grp, t);
         if (eprof) e_x = clock64();
-        issue_res(0, min(nblk, p.nslot));
+        if (!pf) issue_res(0, min(nblk, p.nslot));
+        else if (lt == 0 && leader) load_res(sgrp, rbar, 0, nblk, ow0, oh0, k0, n0);
         if (k0 != par_k0) {
           // stage this tile's channel vectors (identity where absent); a
           // group keeps them while its tiles stay in one N block
@@ -1041,14 +1065,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           if (lane == 0) mbar_arrive(tempty_bar(acc));
           continue;
         }
-        for (int b0 = 0; b0 < nblk; b0 += p.nslot) {
-          const int cnt = min(p.nslot, nblk - b0);
+        const int slots = pf ? p.nslot / 2 : p.nslot;
+        for (int b0 = 0; b0 < nblk; b0 += slots) {
+          const int cnt = min(slots, nblk - b0);
           if (b0 > 0) {
             issue_res(b0, cnt);
             named_bar_sync(bar_id, gthreads);
           }
           if (has_res) {
-            mbar_wait(res_bar(grp, 0), res_phase & 1u);
+            mbar_wait(rbar, pf ? ((uint32_t)(lt >> 1) & 1u) : (res_phase & 1u));
             res_phase ^= 1u;
           }
           etick(e_res);
@@ -1090,9 +1115,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-          if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
-          else mbar_arrive(tempty_bar(acc));
-        }
+              if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
+              else mbar_arrive(tempty_bar(acc));
+            }
           }
           etick(e_cmp);
           if (leader) TRACE(30 + grp, t);
@@ -1104,6 +1129,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               tma_store_5d(&p.tmO, sgrp + i * p.stage_out, 0, ow0, oh0,
                            p.out_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
             bulk_commit();
+            if (pf) {
+              // the group's next tile: its residual goes into the other set
+              // once the store issued from that set one tile ago has read it
+              const int un = cta_unit(p, it + p.ngroups, rank);
+              if (un >= 0) {
+                int nn0, noh0, now0, nk0;
+                decode_tile(p, un / p.splits, nn0, noh0, now0, nk0);
+                bulk_wait_read<1>();
+                const int nset = set ^ 1;
+                load_res(sO + (grp * p.nslot + nset * (p.nslot / 2)) * p.stage_out,
+                         res_bar(grp, nset), 0, min(p.K - nk0, p.BN) / p.y, now0, noh0, nk0,
+                         nn0);
+              }
+            }
           }
           etick(e_st);
         }
@@ -1782,7 +1821,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     const int64_t left = (int64_t)kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4 -
                          (int64_t)p->stages * kp.a_stage - kp.b_region;
     const int64_t slots = rb_out ? left / ((int64_t)kp.ngroups * kTileM * rb_out) : 0;
-    kp.nslot = (int)std::min<int64_t>(slots, BN / std::max(1, p->oc_bn));
+    const int64_t per_tile = BN / std::max(1, p->oc_bn);
+    static const bool no_pf = getenv("NEOB200_NO_RES_PREFETCH") != nullptr;
+    kp.res_pf = (!no_pf && p->residual && !pair && kp.splits == 1 && slots >= 2 * per_tile && per_tile >= 1 &&
+                 p->k % BN == 0) ? 1 : 0;
+    kp.nslot = (int)std::min<int64_t>(slots, (kp.res_pf ? 2 : 1) * per_tile);
   }
   kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
   if (kp.tma_epi) {

@@ -44,7 +44,7 @@ def main(csv_path, names_path, md_path, json_path):
     for i, (lid, e) in enumerate(launches.items()):
         name = names[i] if i < len(names) else "?"
         rd, wr = e.get("read", 0.0), e.get("write", 0.0)
-        if "conv_tc_kernel" in e["kernel"]:
+        if "conv_tc_kernel" in e["kernel"] or "stem_conv_pool" in e["kernel"]:
             conv_bytes += rd + wr
             conv_us += e.get("us", 0)
         kern = e["kernel"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
@@ -56,9 +56,9 @@ def main(csv_path, names_path, md_path, json_path):
             "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none python tools/one_step.py`"
             " (cold-cache, serialised launches: compare shares, not absolutes).",
             "",
-            f"* total kernel time {total:.1f} us; conv_tc_kernel share "
+            f"* total kernel time {total:.1f} us; conv share (conv_tc_kernel + stem_conv_pool_kernel) "
             f"{100 * conv_us / total:.1f}% ({conv_us:.1f} us)",
-            f"* conv_tc_kernel DRAM traffic per step: {conv_bytes / 1e6:.1f} MB",
+            f"* conv DRAM traffic per step (conv_tc_kernel + stem_conv_pool_kernel): {conv_bytes / 1e6:.1f} MB",
             ""]
     open(md_path, "w").write("\n".join(head + lines) + "\n")
     json.dump({"bytes_per_step": conv_bytes, "conv_us_ncu": conv_us, "total_us_ncu": total,
