@@ -354,19 +354,8 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
       }
     }
   };
-  // two 16-column TMEM loads in flight per wait (hides the load latency)
-  int c = c_begin;
 #pragma unroll 1
-  for (; c + c_step < nchunk; c += 2 * c_step) {
-    uint32_t v[16], w[16];
-    tmem_ld16(tcol + c * 16, v);
-    tmem_ld16(tcol + (c + c_step) * 16, w);
-    tmem_ld_wait_regs(v);
-    tmem_ld_wait_regs(w);
-    finish(v, c);
-    finish(w, c + c_step);
-  }
-  if (c < nchunk) {
+  for (int c = c_begin; c < nchunk; c += c_step) {
     uint32_t v[16];
     tmem_ld16(tcol + c * 16, v);
     tmem_ld_wait_regs(v);

@@ -359,3 +359,79 @@ def conv_flops(g: Graph, batch: int | None = None) -> int:
         _, _, oh, ow = specs[node.id].logical_nchw
         total += 2 * (batch or n) * k * c * r * s * oh * ow
     return total
+
+
+# ---------------------------------------------------------------------------
+# The reference's four seeded toy families (models.py:10-95), kept so a user
+# of ``neoplan gen`` / ``gen_model`` gets the same graphs and weights here:
+# the random draws happen in the same order, so a given (kind, depth,
+# channels, hw, seed) yields bit-identical constants (pinned against the
+# reference in tests/test_modelio.py).
+
+KINDS = ("chain", "vgg-ish", "resnet-block", "diamond-concat")
+
+
+class _Toy:
+    """Seeded builder for the toy families: He-like scaled convs without
+    bias and BatchNorms with random statistics."""
+
+    def __init__(self, g: Graph, seed: int):
+        self.g = g
+        self.rng = np.random.default_rng(seed)
+
+    def conv(self, x, c_in, c_out, k, stride=1, pad=None, gain=0.2):
+        w = self.rng.standard_normal((c_out, c_in, k, k)) * gain / np.sqrt(c_in * k * k)
+        wid = self.g.constant(w.astype(np.float32))
+        return self.g.add(OpKind.Conv2d, inputs=[x, wid], stride=stride,
+                          pad=k // 2 if pad is None else pad)
+
+    def bn(self, x, c):
+        draws = [(0.5, 1.5), (-0.2, 0.2), (-0.1, 0.1), (0.5, 1.5)]   # gamma beta mean var
+        stats = [self.g.constant(self.rng.uniform(lo, hi, c).astype(np.float32))
+                 for lo, hi in draws]
+        return self.g.add(OpKind.BatchNorm, inputs=[x, *stats], eps=1e-5)
+
+    def relu(self, x):
+        return self.g.add(OpKind.ReLU, inputs=[x])
+
+
+def gen_model(kind: str, depth: int = 3, channels: int = 16, hw: int = 16,
+              seed: int = 0) -> Graph:
+    """Toy CNN of one of ``KINDS`` (reference models.py:29-95)."""
+    if kind not in KINDS:
+        raise ValueError(f"unknown model kind {kind!r}; choose from {KINDS}")
+    if min(depth, channels, hw) < 1:
+        raise ValueError("depth, channels and hw must be positive")
+    g = Graph(f"{kind}-d{depth}-c{channels}")
+    t = _Toy(g, seed)
+    x = g.add(OpKind.Input, shape=(1, channels, hw, hw), layout="NCHW", name="data")
+    c = channels
+    if kind == "chain":
+        for _ in range(depth):
+            x = t.relu(t.bn(t.conv(x, c, c, 3), c))
+    elif kind == "vgg-ish":
+        size = hw
+        for _ in range(depth):
+            x = t.relu(t.conv(x, c, 2 * c, 3))
+            c *= 2
+            if size >= 4:
+                x = g.add(OpKind.MaxPool, inputs=[x], window=2, stride=2)
+                size //= 2
+        x = g.add(OpKind.Flatten, inputs=[x])
+        w = g.constant((t.rng.standard_normal((10, c * size * size)) * 0.05).astype(np.float32))
+        x = g.add(OpKind.Softmax, inputs=[g.add(OpKind.Dense, inputs=[x, w])])
+    elif kind == "resnet-block":
+        for _ in range(depth):
+            y = t.relu(t.bn(t.conv(x, c, c, 3), c))
+            y = t.bn(t.conv(y, c, c, 3), c)
+            x = t.relu(g.add(OpKind.ElementwiseAdd, inputs=[y, x]))
+    else:   # diamond-concat: a 3x3 and a 1x1 branch joined on the channel axis
+        for _ in range(depth):
+            half = max(1, c // 2)
+            a = t.relu(t.conv(x, c, half, 3))
+            b = t.relu(t.conv(x, c, half, 1))
+            x = g.add(OpKind.Concat, inputs=[a, b], axis=1)
+            c = 2 * half
+        x = t.conv(x, c, c, 1)
+    g.outputs = [x]
+    return g

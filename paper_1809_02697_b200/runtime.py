@@ -96,3 +96,44 @@ def resolve_pool(pool) -> DevicePool:
     if isinstance(pool, str):
         return DevicePool(mode=pool)
     raise TypeError(f"expected DevicePool, mode string or None, got {type(pool).__name__}")
+
+
+class ThreadPool(DevicePool):
+    """Reference name (runtime.py:36-126) so ``with ThreadPool(n) as pool:
+    execute(g, inputs, pool)`` keeps working: on a B200 the intra-op split
+    is the CUDA grid, so the thread count is recorded but the pool runs on
+    ``devices`` (default GPU 0) in ``mode``.  Host-side ``parallel_for``
+    still uses ``num_threads`` worker threads."""
+
+    def __init__(self, num_threads: int | None = None, devices=None, mode: str | None = None):
+        super().__init__(devices if devices is not None else [0], mode or default_mode())
+        self.num_threads = num_threads or default_num_threads()
+
+
+def default_num_threads() -> int:
+    """NEOPLAN_NUM_THREADS or the physical core count (runtime.py:29-33)."""
+    env = os.environ.get("NEOPLAN_NUM_THREADS")
+    if env:
+        try:
+            return max(1, int(env))
+        except ValueError:
+            pass
+    return physical_cores()
+
+
+def parallel_for(pool, n_items: int, body) -> None:
+    """Host-side static-partition loop (runtime.py:140-149): ``body(lo, hi)``
+    over ``split_ranges(n_items, threads)`` on worker threads, joined before
+    returning; the first exception is re-raised.  Device work never goes
+    through here (kernels own their grids)."""
+    from concurrent.futures import ThreadPoolExecutor
+    threads = getattr(pool, "num_threads", None) or default_num_threads()
+    chunks = split_ranges(n_items, threads)
+    if len(chunks) <= 1:
+        for lo, hi in chunks:
+            body(lo, hi)
+        return
+    with ThreadPoolExecutor(max_workers=len(chunks)) as ex:
+        futures = [ex.submit(body, lo, hi) for lo, hi in chunks]
+    for f in futures:
+        f.result()

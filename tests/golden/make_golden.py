@@ -238,17 +238,26 @@ def planner(neo):
                  arrays)
 
 
-def main():
+def modelfiles(neo):
+    """Model container files written by the reference (modelio.py): a raw
+    toy graph and an optimized one (packed weights, epilogue dicts), to pin
+    byte compatibility of save_model / load_model / read_weights."""
+    g = neo.gen_model("resnet-block", depth=2, channels=8, hw=8, seed=4)
+    neo.save_model(g, os.path.join(HERE, "model_toy.json"), os.path.join(HERE, "model_toy.npwt"))
+    s = neo.simplify(neo.gen_model("diamond-concat", depth=2, channels=16, hw=8, seed=5))
+    opt = neo.pretransform_weights(neo.alter_and_insert_transforms(s, neo.uniform_assignment(s, 8)))
+    neo.save_model(opt, os.path.join(HERE, "model_opt.json"), os.path.join(HERE, "model_opt.npwt"))
+
+
+def main(only=None):
     neo = import_reference()
     print("reference:", neo.__file__)
-    layouts(neo)
-    conv(neo)
-    pool(neo)
-    graphs(neo)
-    models(neo)
-    planner(neo)
+    steps = [layouts, conv, pool, graphs, models, planner, modelfiles]
+    for step in steps:
+        if only is None or step.__name__ in only:
+            step(neo)
     print("fixtures written to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    main(set(sys.argv[1:]) or None)
