@@ -137,6 +137,18 @@ int neo_stem_conv_pool(const float* x, const void* wimg, void* out, const float*
                        int64_t h, int64_t w, int y, int out_cb_offset, int out_cb_total,
                        neo_stream_t stream);
 
+/* Fused classifier head (B200 lowering of the reference's global average
+ * pool executor.py:103-128, Flatten, Dense executor.py:197-203 and Softmax
+ * executor.py:167-170):
+ *   pooled[n, c] = bf16(sum_t x[n, c, t] / hw)      (x: bf16 NCHW[y]c, H*W = hw)
+ *   logits[n, u] = sum_c pooled[n, c] * w[u, c] + bias[u]   (w: bf16 (units, c))
+ *   out = softmax ? softmax_rows(logits) : logits          (f32 (n, units))
+ * C % 256 == 0.  pooled (n*c bf16), logits (2*n*units f32) and bar (3 ints,
+ * zero-initialised once; the kernel re-arms them) are caller scratch. */
+int neo_classifier_head(const void* x, const void* w_bf16, const float* bias, void* pooled,
+                        float* logits, float* out, int* bar, int64_t n, int64_t c, int64_t hw,
+                        int y, int64_t units, int softmax, neo_stream_t stream);
+
 /* ---- fused blocked convolution (kernels.py:250-303 conv_blocked, with the
  * Epilogue kernels.py:74-87 applied in the order scale/shift -> bias ->
  * residual -> relu, kernels.py:185-197) --------------------------------- */

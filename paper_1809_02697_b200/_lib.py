@@ -90,6 +90,8 @@ SIGNATURES = {
     "neo_stem_weight_bytes": (_c_i64, []),
     "neo_stem_conv_pool": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
                                     _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_vp]),
+    "neo_classifier_head": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
+                                     _c_i64, _c_i64, _c_int, _c_i64, _c_int, _c_vp]),
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
     "neo_conv2d_nchwc_fused": (_c_int, [ctypes.POINTER(ConvParams), _c_vp]),
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),

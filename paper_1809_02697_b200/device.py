@@ -258,3 +258,24 @@ def stem_conv_pool(x: torch.Tensor, wimg: torch.Tensor, out: torch.Tensor, n, c,
     L.call("neo_stem_conv_pool", _ptr(x), _ptr(wimg), _ptr(out), opt(scale), opt(shift),
            opt(bias), int(bool(relu)), n, c, h, w, y, out_cb[0], out_cb[1],
            stream_handle(stream))
+
+
+class HeadScratch:
+    """Device scratch of one fused classifier head (pooled features, logits,
+    barrier counters)."""
+
+    def __init__(self, n: int, c: int, units: int, device):
+        self.pooled = torch.empty(n * c, dtype=torch.bfloat16, device=device)
+        self.logits = torch.empty(2 * n * units, dtype=torch.float32, device=device)
+        self.bar = torch.zeros(4, dtype=torch.int32, device=device)
+
+
+def classifier_head(x: torch.Tensor, w_bf16: torch.Tensor, bias, out: torch.Tensor, n, c, hw, y,
+                    units, softmax: bool, scratch: HeadScratch, stream=None) -> None:
+    """Global avg pool -> dense (+bias) -> optional softmax in one launch
+    (neo_classifier_head)."""
+    if x.dtype != torch.bfloat16 or w_bf16.dtype != torch.bfloat16 or out.dtype != torch.float32:
+        raise E.InputMismatch("classifier_head takes bf16 features / weights and writes f32")
+    L.call("neo_classifier_head", _ptr(x), _ptr(w_bf16), _ptr(bias) if bias is not None else None,
+           _ptr(scratch.pooled), _ptr(scratch.logits), _ptr(out), _ptr(scratch.bar), n, c, hw, y,
+           units, int(bool(softmax)), stream_handle(stream))

@@ -240,6 +240,15 @@ class DeviceProgram:
                     self.fused_stem[mp] = (cv, src)
                     self.skip.update((t, cv))
                     del self.stem_fold[t]
+        # classifier head (global avg pool -> flatten -> dense -> softmax) as
+        # one fused launch in bf16 mode (neo_classifier_head)
+        self.fused_head: dict[int, dict] = {}    # anchor (softmax or dense) id -> info
+        if self.mode == "bf16" and not os.environ.get("NEOB200_NO_FUSED_HEAD"):
+            for nid in order:
+                info = self._fused_head_info(nid)
+                if info:
+                    self.fused_head[info["anchor"]] = info
+                    self.skip.update(info["skip"])
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -291,6 +300,10 @@ class DeviceProgram:
             node = self.g.nodes[nid]
             for src, _ in node.inputs:
                 tgt = self._storage(self.pro_src.get(src, src))
+                if tgt is not None:
+                    tgt.last = max(tgt.last, self.step[nid])
+            if nid in self.fused_head:      # the fused head reads the pool's input
+                tgt = self._storage(self.fused_head[nid]["src"])
                 if tgt is not None:
                     tgt.last = max(tgt.last, self.step[nid])
             if nid in self.fused_stem:      # the fused stem reads the graph input
@@ -422,6 +435,52 @@ class DeviceProgram:
         if lay.tag != "NCHWc" or lay.x not in (8, 16, 32, 64):
             return None
         return cv.id, mp.id, g.nodes[t].inputs[0][0]
+
+    def _fused_head_info(self, nid: int) -> dict | None:
+        """Chain global AvgPool -> (NCHW transform) -> Flatten -> Dense ->
+        (Softmax) with single consumers, over a bf16 NCHW[y]c map."""
+        g = self.g
+        node = g.nodes[nid]
+        if node.kind != OpKind.AvgPool or hw_pair(node.attrs.get("pad", 0)) != (0, 0):
+            return None
+        src = node.inputs[0][0]
+        sspec = self.specs[src]
+        n, c, h, w = sspec.logical_nchw
+        if hw_pair(node.attrs["window"]) != (h, w) or sspec.layout.tag != "NCHWc":
+            return None
+        if sspec.layout.x % 8 or c % 256 or c % sspec.layout.x:
+            return None
+        chain, cur = [nid], nid
+        protected = set(g.outputs) | set(self.keep)
+        while True:
+            us = self.users[cur]
+            if len(us) != 1 or cur in protected:
+                break
+            nxt = g.nodes[us[0]]
+            if nxt.kind in (OpKind.LayoutTransform, OpKind.Flatten) and len(chain) < 3:
+                chain.append(nxt.id)
+                cur = nxt.id
+                continue
+            if nxt.kind == OpKind.Dense and nxt.inputs[0][0] == cur:
+                chain.append(nxt.id)
+                cur = nxt.id
+                if len(self.users[cur]) == 1 and cur not in protected:
+                    sm = g.nodes[self.users[cur][0]]
+                    if sm.kind == OpKind.Softmax:
+                        chain.append(sm.id)
+                break
+            break
+        kinds = [g.nodes[i].kind for i in chain]
+        if OpKind.Dense not in kinds or kinds[-2 if kinds[-1] == OpKind.Softmax else -1] != OpKind.Dense:
+            return None
+        if OpKind.Flatten not in kinds:
+            return None
+        dense = next(i for i in chain if g.nodes[i].kind == OpKind.Dense)
+        wt = g.nodes[g.nodes[dense].inputs[1][0]].attrs["value"]
+        if wt.ndim != 2 or wt.shape[1] != c:
+            return None
+        return {"anchor": chain[-1], "skip": chain[:-1], "src": src, "dense": dense,
+                "softmax": kinds[-1] == OpKind.Softmax}
 
     def _stem_fold_info(self, nid) -> dict | None:
         """Fold parameters if ``nid`` packs a few-channel graph input that
@@ -577,6 +636,8 @@ class DeviceProgram:
             elif kind == OpKind.LayoutTransform:
                 if out.alias is None:
                     self._bind_transform(node, ins[0], out)
+            elif nid in self.fused_head:
+                self._bind_head(self.fused_head[nid], out)
             elif nid in self.fused_stem:
                 self._bind_stem(node, out)
             elif kind in (OpKind.MaxPool, OpKind.AvgPool):
@@ -776,6 +837,28 @@ class DeviceProgram:
         self._emit(f"stem{cv_id}_pool{pool_node.id}", lambda: D.stem_conv_pool(
             x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream),
             _nb(x_t) + _vb(out))
+
+    def _bind_head(self, info: dict, out: _Val):
+        """Global avg pool -> dense (+bias) -> softmax as one
+        neo_classifier_head launch (reference: _pool2d, Dense, Softmax)."""
+        import torch
+        from . import device as D
+        g = self.g
+        src = self.vals[info["src"]]
+        if src.win is not None or src.tensor.dtype != torch.bfloat16 or out.tensor.dtype != torch.float32:
+            raise InputMismatch(f"fused head {info['anchor']}: unsupported operand storage")
+        dn = g.nodes[info["dense"]]
+        w = np.asarray(g.nodes[dn.inputs[1][0]].attrs["value"], np.float32)
+        units, c = w.shape
+        w_t = self._upload(w, torch.bfloat16)
+        b_t = self._upload(g.nodes[dn.inputs[2][0]].attrs["value"]) if len(dn.inputs) == 3 else None
+        n, cb, h, wd, y = src.shape
+        scratch = D.HeadScratch(n, c, units, self.device)
+        self.weights.append(scratch)
+        x_t, o_t, sm = src.tensor, out.tensor, info["softmax"]
+        self._emit(f"head{info['anchor']}", lambda: D.classifier_head(
+            x_t, w_t, b_t, o_t, n, c, h * wd, y, units, sm, scratch, self.stream),
+            _nb(x_t) + _nb(w_t) + _nb(o_t))
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
