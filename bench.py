@@ -345,7 +345,7 @@ def main():
                                     else "in-kernel default tiles",
                        "wall_s_timed_region": wall},
             "e2e": {"value": e2e_value, "unit": "images/s",
-                    "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
+                    "h2d_bytes_per_step": int(prog.upload_bytes),
                     "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size())},
             "gpu_launches": prog.kernel_launches * args.steps,
             "launches_per_step": prog.kernel_launches,

@@ -124,7 +124,9 @@ int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t n, int64_t
  * kernels.py:185-197, and _pool2d executor.py:103-128):
  *   out = maxpool3x3/2 pad 1 (-inf) ( relu?( conv7x7/2 pad 3 (x, w)
  *                                           * scale + shift + bias ) )
- * x: NCHW f32 (n, c, h, w) with c <= 4 and w % 4 == 0; K = 64 output
+ * x: NCHW (n, c, h, w) f32 or bf16 (x_dtype; f32 is rounded RN to bf16, so a
+ * host-rounded bf16 image gives identical results) with c <= 4 and 16-byte
+ * rows (w % 4 == 0 f32, w % 8 == 0 bf16); K = 64 output
  * channels; out: bf16 NCHW[y]c (n, out_cb_total, ph, pw, y), written at
  * channel-block offset out_cb_offset (concat in place), y in {8,16,32,64};
  * scale/shift/bias per output channel or NULL.  wimg is the 28 KB image
@@ -132,7 +134,7 @@ int neo_stem_fold(const float* src, void* dst, int dst_dtype, int64_t n, int64_t
 int neo_stem_pack_weights(const float* w_kcrs, void* img, int64_t k, int64_t c, int64_t r,
                           int64_t s, neo_stream_t stream);
 int64_t neo_stem_weight_bytes(void);
-int neo_stem_conv_pool(const float* x, const void* wimg, void* out, const float* scale,
+int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, void* out, const float* scale,
                        const float* shift, const float* bias, int relu, int64_t n, int64_t c,
                        int64_t h, int64_t w, int y, int out_cb_offset, int out_cb_total,
                        neo_stream_t stream);

@@ -88,7 +88,7 @@ SIGNATURES = {
                                _c_int, _c_int, _c_i64, _c_int, _c_int, _c_vp]),
     "neo_stem_pack_weights": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp]),
     "neo_stem_weight_bytes": (_c_i64, []),
-    "neo_stem_conv_pool": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
+    "neo_stem_conv_pool": (_c_int, [_c_vp, _c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
                                     _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_vp]),
     "neo_classifier_head": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
                                      _c_i64, _c_i64, _c_int, _c_i64, _c_int, _c_vp]),

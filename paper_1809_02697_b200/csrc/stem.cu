@@ -1,5 +1,5 @@
 // K-STEM: the image stem of ResNet / DenseNet / SSD-ResNet as ONE kernel:
-//   conv 7x7 stride 2 pad 3 over a C<=4 channel NCHW f32 image, K = 64
+//   conv 7x7 stride 2 pad 3 over a C<=4 channel NCHW f32 or bf16 image, K = 64
 //   -> scale/shift -> bias -> relu      (Epilogue, reference kernels.py:185-197)
 //   -> max pool 3x3 stride 2 pad 1      (reference executor.py:103-128, -inf pad)
 //   -> NCHW[y]c bf16 (optionally a channel-block window of a concat buffer).
@@ -24,11 +24,11 @@
 // weights.  The weights are a resident 28 KB image [step][chunk][64 k][8].
 //
 // Warp roles (768 threads, persistent over units, one CTA per SM):
-//   warp 0      TMA producer: f32 patch box (44 cols x 37 rows x C planes,
+//   warp 0      TMA producer: f32/bf16 patch box (37 rows x C planes,
 //               zero fill outside the image) into a 4-deep ring
 //   warp 1      TMEM allocator + single-thread MMA issuer (4 accumulators of
 //               2 x 64 columns)
-//   warps 2-7   converters: f32 planar box -> bf16 [row][col][4] patch
+//   warps 2-7   converters: planar box -> bf16 [row][col][4] patch (RN)
 //               (4-deep ring), then fence.proxy.async for the tensor core
 //   warps 8-23  epilogue: tcgen05.ld -> scale/shift/bias/relu -> bf16 conv
 //               tile in shared memory (double buffered, XOR-swizzled 16-byte
@@ -47,11 +47,18 @@ constexpr int kEpiThreads = 512;               // warps 8..23
 constexpr int kThreads = 64 + kConvWarps * 32 + kEpiThreads;
 constexpr int kRawStages = 4;                  // max f32 box ring depth
 constexpr int kPatchStages = 4;                // converted patches in flight
-// f32 input box per unit: 37 rows x 44 columns starting 8 columns left of
-// the conv tile's first tap (a TMA box must start on a 16-byte boundary of
-// its innermost dimension; a negative, unaligned start column faults), so
-// patch column j is box column j + kColOff
-constexpr int kBoxW = 44, kBoxH = 37, kColOff = 3;
+// input box per unit: 37 rows x kBoxW columns starting at the conv tile's
+// first tap column 4*q0 - 5 rounded down to a 16-byte boundary (a TMA box
+// must start 16-byte aligned in its innermost dimension; an unaligned,
+// negative start column faults), so patch column j is box column j + off
+// with off = (4*q0 - 5) - start: f32 boxes start 4 columns aligned (off = 3,
+// 44 columns), bf16 boxes 8 columns aligned (off 3 or 7, 48 columns)
+constexpr int kBoxH = 37;
+template <typename TX> struct BoxOf;
+template <> struct BoxOf<float> { static constexpr int W = 44, kAlign = 4; };
+template <> struct BoxOf<__nv_bfloat16> { static constexpr int W = 48, kAlign = 8; };
+__device__ __forceinline__ float to_float(float v) { return v; }
+__device__ __forceinline__ float to_float(__nv_bfloat16 v) { return __bfloat162float(v); }
 constexpr int kPatchCols = 38;                 // input columns the MMAs read
 constexpr int kPitch = kPatchCols * 8;         // bytes per bf16x4 patch row
 constexpr int kPatchBytes = kBoxH * kPitch;    // 11248
@@ -73,7 +80,7 @@ struct StemParams {
   int tiles_h, tiles_w, num_units;
   int y, out_cb_off, out_cb_total;
   int relu;
-  uint32_t raw_bytes;       // 44*37*C*4
+  uint32_t raw_bytes;       // BoxOf<TX>::W * 37 * C * sizeof(TX)
   int raw_stages;           // f32 box ring depth (4, 3 for C = 4)
   int dbg;                  // NEOB200_STEM_DBG: 1 no MMAs, 2 no TMEM loads, 4 no TMA,
                             // 8 no pooling, 16 no conversion, 32 phase clocks
@@ -113,7 +120,9 @@ __device__ __forceinline__ void unit_origin(const StemParams& p, int u, int& n, 
   q0 = tw * kPool;
 }
 
+template <typename TX>
 __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __grid_constant__ StemParams p) {
+  constexpr int kBoxW = BoxOf<TX>::W;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (sbase - smem_u32(smem_raw));
@@ -180,8 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         } else {
         mbar_arrive_expect_tx(raw_full(s), p.raw_bytes);
         // input origin: conv row 2*p0 - 1 -> input row 2*(2*p0 - 1) - 3;
-        // columns from 4*q0 - 5 - kColOff (16-byte aligned)
-        tma_load_3d(sRaw + s * raw_slot, &p.tmX, raw_full(s), 4 * q0 - 8, 4 * p0 - 5, n * p.C);
+        // first column 4*q0 - 5 rounded down to the 16-byte boundary
+        const int c0 = (4 * q0 - 5) & ~(BoxOf<TX>::kAlign - 1);
+        tma_load_3d(sRaw + s * raw_slot, &p.tmX, raw_full(s), c0, 4 * p0 - 5, n * p.C);
         }
         if (++s == p.raw_stages) {
           s = 0;
@@ -251,17 +261,20 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
       const int pb = it % kPatchStages;
       mbar_wait(raw_full(s), ph);
       mbar_wait(patch_empty(pb), ((uint32_t)(it / kPatchStages) & 1u) ^ 1u);
-      const float* raw = reinterpret_cast<const float*>(gbase + (sRaw + s * raw_slot - sbase));
+      const TX* raw = reinterpret_cast<const TX*>(gbase + (sRaw + s * raw_slot - sbase));
+      int un, up0, uq0;
+      unit_origin(p, u, un, up0, uq0);
+      const int off = (4 * uq0 - 5) - ((4 * uq0 - 5) & ~(BoxOf<TX>::kAlign - 1));
       uint8_t* patch = gbase + (sPatch + pb * kPatchSlot - sbase);
       constexpr int plane = kBoxW * kBoxH;
 #pragma unroll 4
       for (int idx = ctid; idx < nconv; idx += kConvWarps * 32) {
         const int row = idx / kPatchCols, col = idx - row * kPatchCols;
-        const float* rp = raw + row * kBoxW + col + kColOff;
-        const float v0 = rp[0];
-        const float v1 = C > 1 ? rp[plane] : 0.f;
-        const float v2 = C > 2 ? rp[2 * plane] : 0.f;
-        const float v3 = C > 3 ? rp[3 * plane] : 0.f;
+        const TX* rp = raw + row * kBoxW + col + off;
+        const float v0 = to_float(rp[0]);
+        const float v1 = C > 1 ? to_float(rp[plane]) : 0.f;
+        const float v2 = C > 2 ? to_float(rp[2 * plane]) : 0.f;
+        const float v3 = C > 3 ? to_float(rp[3 * plane]) : 0.f;
         *reinterpret_cast<uint2*>(patch + row * kPitch + col * 8) =
             make_uint2(pack_bf16x2(v0, v1), pack_bf16x2(v2, v3));
       }
@@ -451,15 +464,18 @@ extern "C" int neo_stem_pack_weights(const float* w_kcrs, void* img, int64_t k, 
 
 extern "C" int64_t neo_stem_weight_bytes(void) { return kWBytes; }
 
-extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
+extern "C" int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, void* out,
                                   const float* scale, const float* shift, const float* bias,
                                   int relu, int64_t n, int64_t c, int64_t h, int64_t w, int y,
                                   int out_cb_offset, int out_cb_total, neo_stream_t stream) {
   NEO_CHECK_ARG(x && wimg && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(x_dtype == NEO_F32 || x_dtype == NEO_BF16, NEO_ERR_INVALID_ARG, "bad input dtype");
+  const bool xbf = x_dtype == NEO_BF16;
+  const int es = xbf ? 2 : 4, box_w = xbf ? BoxOf<__nv_bfloat16>::W : BoxOf<float>::W;
   NEO_CHECK_ARG(n >= 1 && c >= 1 && c <= 4 && h >= 1 && w >= 1, NEO_ERR_SHAPE_MISMATCH,
                 "stem needs 1..4 input channels (C=%lld)", (long long)c);
-  NEO_CHECK_ARG(w % 4 == 0, NEO_ERR_UNSUPPORTED, "stem input width %lld must be a multiple of 4",
-                (long long)w);
+  NEO_CHECK_ARG((w * es) % 16 == 0, NEO_ERR_UNSUPPORTED,
+                "stem input rows must be 16-byte multiples (width %lld)", (long long)w);
   NEO_CHECK_ARG(y == 8 || y == 16 || y == 32 || y == 64, NEO_ERR_UNSUPPORTED,
                 "stem output block %d not in {8,16,32,64}", y);
   const int64_t OH = (h + 6 - 7) / 2 + 1, OW = (w + 6 - 7) / 2 + 1;
@@ -475,11 +491,11 @@ extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
   memset(&kp, 0, sizeof(kp));
   {
     cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)(n * c)};
-    cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)h * w * 4};
-    cuuint32_t box[3] = {(cuuint32_t)kBoxW, (cuuint32_t)kBoxH, (cuuint32_t)c};
-
+    cuuint64_t strides[2] = {(cuuint64_t)(w * es), (cuuint64_t)(h * w * es)};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)kBoxH, (cuuint32_t)c};
     cuuint32_t estr[3] = {1u, 1u, 1u};
-    CUresult r = encode(&kp.tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims,
+    CUresult r = encode(&kp.tmX, xbf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        3, const_cast<void*>(x), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -505,7 +521,7 @@ extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
   kp.out_cb_off = out_cb_offset;
   kp.out_cb_total = cbt;
   kp.relu = relu;
-  kp.raw_bytes = (uint32_t)(kBoxW * kBoxH * c * 4);
+  kp.raw_bytes = (uint32_t)(box_w * kBoxH * c * es);
   {
     static const char* dbg = getenv("NEOB200_STEM_DBG");
     kp.dbg = dbg ? atoi(dbg) : 0;
@@ -519,15 +535,21 @@ extern "C" int neo_stem_conv_pool(const float* x, const void* wimg, void* out,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
-    NEO_CUDA_TRY(cudaFuncSetAttribute(stem_conv_pool_kernel,
+    NEO_CUDA_TRY(cudaFuncSetAttribute(stem_conv_pool_kernel<float>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    NEO_CUDA_TRY(cudaFuncSetAttribute(stem_conv_pool_kernel<__nv_bfloat16>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_done[dev & 63] = true;
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(units, sms);
-  neo_launch(stem_conv_pool_kernel, dim3(grid), dim3(kThreads), smem,
-             static_cast<cudaStream_t>(stream), kp);
+  if (xbf)
+    neo_launch(stem_conv_pool_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreads), smem,
+               static_cast<cudaStream_t>(stream), kp);
+  else
+    neo_launch(stem_conv_pool_kernel<float>, dim3(grid), dim3(kThreads), smem,
+               static_cast<cudaStream_t>(stream), kp);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

@@ -251,11 +251,11 @@ def stem_conv_pool(x: torch.Tensor, wimg: torch.Tensor, out: torch.Tensor, n, c,
                    scale=None, shift=None, bias=None, relu=True, out_cb=(0, 0),
                    stream=None) -> None:
     """Fused stem: maxpool3x3/2(relu(conv7x7/2(x) * scale + shift + bias))
-    from NCHW f32 straight into bf16 NCHW[y]c (neo_stem_conv_pool)."""
-    if x.dtype != torch.float32 or out.dtype != torch.bfloat16:
-        raise E.InputMismatch("stem_conv_pool takes f32 input and writes bf16")
+    from NCHW f32 / bf16 straight into bf16 NCHW[y]c (neo_stem_conv_pool)."""
+    if x.dtype not in (torch.float32, torch.bfloat16) or out.dtype != torch.bfloat16:
+        raise E.InputMismatch("stem_conv_pool takes f32 or bf16 input and writes bf16")
     opt = lambda t: _ptr(t) if t is not None else None
-    L.call("neo_stem_conv_pool", _ptr(x), _ptr(wimg), _ptr(out), opt(scale), opt(shift),
+    L.call("neo_stem_conv_pool", _ptr(x), dtype_code(x), _ptr(wimg), _ptr(out), opt(scale), opt(shift),
            opt(bias), int(bool(relu)), n, c, h, w, y, out_cb[0], out_cb[1],
            stream_handle(stream))
 

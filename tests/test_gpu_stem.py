@@ -122,3 +122,47 @@ def test_resnet_executor_uses_fused_stem(cuda):
     ref = oracle.execute_reference(g, feeds)[0]
     assert oracle.rel_err(fused, ref) < 2e-2
     assert oracle.rel_err(fused, unfused) < 2e-2
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 64, 64), (3, 3, 40, 48), (1, 3, 224, 224)])
+def test_stem_bf16_input_identical(cuda, shape):
+    """A host-rounded bf16 image gives bit-identical results to the f32 image
+    (the kernel rounds f32 input RN to bf16 itself); the executor stores a
+    stem-only graph input as bf16 so uploads move half the bytes."""
+    import torch
+    from paper_1809_02697_b200 import device as D
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(shape).astype(np.float32)
+    w = (rng.standard_normal((64, 3, 7, 7)) * 0.1).astype(np.float32)
+    n, c, h, wd = shape
+    oh, ow = (h - 1) // 2 + 1, (wd - 1) // 2 + 1
+    ph, pw = (oh - 1) // 2 + 1, (ow - 1) // 2 + 1
+    wimg = D.pack_stem_weights(torch.from_numpy(w).to(dev))
+    outs = []
+    for xt in (torch.from_numpy(x).to(dev), torch.from_numpy(x).bfloat16().to(dev)):
+        out = torch.empty((n, 1, ph, pw, 64), dtype=torch.bfloat16, device=dev)
+        D.stem_conv_pool(xt, wimg, out, n, c, h, wd, 64)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_executor_bf16_stem_input(cuda):
+    import torch
+    from paper_1809_02697_b200 import build_model, compile_graph, model_input
+    from paper_1809_02697_b200.executor import DeviceProgram, ExecutablePlan
+    g = build_model("resnet18", batch=2, image=64, num_classes=10, softmax=False)
+    prog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode="bf16")), 0, "bf16")
+    name = prog.input_names()[0]
+    assert prog.input_tensor(name).dtype == torch.bfloat16
+    assert prog.upload_bytes == 2 * 3 * 64 * 64 * 2
+    feeds = model_input(g)
+    a = prog.run(feeds)[0]
+    # the serving loop (host rounding into pinned bf16, double-buffered uploads)
+    pinned = torch.from_numpy(feeds[name]).pin_memory()
+    outs = [torch.empty(a.shape, dtype=torch.float32).pin_memory() for _ in range(3)]
+    prog.pipeline([pinned] * 3, outs)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.numpy(), a)
