@@ -260,18 +260,6 @@ __device__ __forceinline__ void epi_chunk(const ConvTCParams& p, const uint32_t 
 // kernels.py:185-197 with one rounding per reference operation.
 constexpr int kParamFloats = 3 * 256;   // scale | shift | bias for BN <= 256
 
-__device__ __forceinline__ void load_par16(const float* par, int col, float (&dst)[16]) {
-  const float4* v4 = reinterpret_cast<const float4*>(par + col);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float4 t = v4[q];
-    dst[4 * q] = t.x;
-    dst[4 * q + 1] = t.y;
-    dst[4 * q + 2] = t.z;
-    dst[4 * q + 3] = t.w;
-  }
-}
-
 // One output channel block (y columns) of one pixel row: TMEM -> registers ->
 // epilogue -> swizzled smem row (which already holds the residual block when
 // HAS_RES).  OUT_F32 selects f32 vs bf16 storage.

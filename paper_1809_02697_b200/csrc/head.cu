@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const __grid_constant__ 
     __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(hsm);
     const int img_tiles = (p.N + kImgTile - 1) / kImgTile;
     const int unit_tiles = (p.units + kUnitTile - 1) / kUnitTile;
-    float* dst = p.softmax ? p.logits : p.out;
     const int g = lane >> 2, q = lane & 3;            // fragment row group / k pair
     // K split in two halves over twice the CTAs; the halves' partial logits
     // are summed in a fixed order afterwards (deterministic)
