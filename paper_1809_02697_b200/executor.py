@@ -1164,22 +1164,30 @@ class DeviceProgram:
             self._host_stage = [torch.empty(dst.shape, dtype=dst.dtype).pin_memory()
                                 for _ in range(2)]
             self._host_done = [None, None]
+        n = dst.shape[0]
+        chunks = [(lo, min(n, lo + max(1, n // 4))) for lo in range(0, n, max(1, n // 4))]
         for i, host in enumerate(batches):
             slot = i & 1
-            src = host
+            with torch.cuda.stream(self._copy_stream):
+                self._copy_stream.wait_event(self._consumed[slot])
             if convert:
                 if self._host_done[slot] is not None:
                     self._host_done[slot].synchronize()     # its previous upload finished
-                self._host_stage[slot].copy_(host)
-                src = self._host_stage[slot]
+                # round and upload in batch chunks: the upload of one chunk
+                # overlaps the host rounding of the next
+                for lo, hi in chunks:
+                    self._host_stage[slot][lo:hi].copy_(host[lo:hi])
+                    with torch.cuda.stream(self._copy_stream):
+                        self._staging[slot][lo:hi].copy_(self._host_stage[slot][lo:hi],
+                                                         non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._copy_stream)
+                self._host_done[slot] = ev
+            else:
+                with torch.cuda.stream(self._copy_stream):
+                    self._staging[slot].copy_(host, non_blocking=True)
             with torch.cuda.stream(self._copy_stream):
-                self._copy_stream.wait_event(self._consumed[slot])
-                self._staging[slot].copy_(src, non_blocking=True)
                 self._copied[slot].record(self._copy_stream)
-                if convert:
-                    ev = torch.cuda.Event()
-                    ev.record(self._copy_stream)
-                    self._host_done[slot] = ev
             with torch.cuda.stream(self.stream):
                 self.stream.wait_event(self._copied[slot])
                 dst.copy_(self._staging[slot], non_blocking=True)
