@@ -204,6 +204,17 @@ typedef struct neo_conv_params {
    * (0 = automatic: when it fits beside >= 3 activation stages, 1 = off,
    * 2 = on). */
   int weight_stationary;
+  /* second output (TF32/BF16, no residual, no split-K, no CTA pair): output
+   * channels [k_split, k) go to out2 (n, out2_cb_total, oh, ow, oc_bn) at
+   * channel block out2_cb_offset + (k - k_split) / oc_bn with relu2, so two
+   * sibling convs over the same input (a bottleneck's reduce 1x1 and its
+   * projection shortcut, passes.py:119-157 fuse nothing across siblings)
+   * run as one launch over concatenated weights and epilogue vectors;
+   * k_split must be a multiple of the N tile (0 = single output). */
+  void* out2;
+  int64_t k_split;
+  int relu2;
+  int out2_cb_offset, out2_cb_total;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);

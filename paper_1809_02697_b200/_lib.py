@@ -68,6 +68,8 @@ class ConvParams(ctypes.Structure):
         ("cta_pair", _c_int),
         ("pro_scale", _c_vp), ("pro_shift", _c_vp), ("pro_relu", _c_int),
         ("weight_stationary", _c_int),
+        ("out2", _c_vp), ("k_split", _c_i64), ("relu2", _c_int),
+        ("out2_cb_offset", _c_int), ("out2_cb_total", _c_int),
     ]
 
 

@@ -48,6 +48,7 @@ struct ConvTCParams {
   CUtensorMap tmB;  // 3-D: (x, K, slices)
   CUtensorMap tmO;  // 5-D output store map: (y, OW, OH, Kb_total, N)   (tma_epi)
   CUtensorMap tmR;  // 5-D residual load map, same geometry              (tma_epi)
+  CUtensorMap tmO2; // second output (k_split > 0), same geometry      (tma_epi)
   int N, OH, OW, K;
   int BW, BH, BNI, BN;
   int tiles_w, tiles_h, tiles_k;
@@ -68,6 +69,7 @@ struct ConvTCParams {
   void* out;
   int y, out_cb_off, out_cb_total, res_cb_off, res_cb_total;
   int relu, out_f32, round_tf32;
+  int k_split, relu2, out2_cb_off;   // channels >= k_split -> tmO2 (0: one output)
   int tma_epi;        // stage output blocks in smem and store them with TMA
   int rowb_out;       // y * sizeof(out elem) for the TMA epilogue
   uint32_t stage_out; // bytes of one staging buffer (128 rows * rowb_out)
@@ -634,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     if (p.tma_epi) {
       tma_prefetch_desc(&p.tmO);
       if (p.res) tma_prefetch_desc(&p.tmR);
+      if (p.k_split) tma_prefetch_desc(&p.tmO2);
     }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(full_bar(i), 1);
@@ -1055,7 +1058,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
           etick(e_res);
           if (leader) TRACE(28 + grp, t);
-          const float floor_v = p.relu ? 0.f : -INFINITY;
+          const bool sec = p.k_split > 0 && k0 >= p.k_split;   // second output's tile
+          const float floor_v = (sec ? p.relu2 : p.relu) ? 0.f : -INFINITY;
           const bool rnd = p.round_tf32 != 0;
           // the two warps of a lane quarter split the chunk's work: whole
           // blocks when there are several, 16-column pieces of one block else
@@ -1102,9 +1106,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           named_bar_sync(bar_id, gthreads);
           if (leader) TRACE(32 + grp, t);
           if (leader) {
+            const bool sec = p.k_split > 0 && k0 >= p.k_split;
+            const CUtensorMap* tmo = sec ? &p.tmO2 : &p.tmO;
+            const int cb0 = sec ? p.out2_cb_off + (k0 - p.k_split) / p.y : p.out_cb_off + k0 / p.y;
             for (int i = 0; i < cnt; ++i)
-              tma_store_5d(&p.tmO, sgrp + i * p.stage_out, 0, ow0, oh0,
-                           p.out_cb_off + (k0 + (b0 + i) * p.y) / p.y, n0);
+              tma_store_5d(tmo, sgrp + i * p.stage_out, 0, ow0, oh0, cb0 + b0 + i, n0);
             bulk_commit();
             if (pf) {
               // the group's next tile: its residual goes into the other set
@@ -1779,12 +1785,28 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.res = p->residual;
   kp.out = p->out;
   kp.y = p->oc_bn;
-  const int64_t kbt = neo_ceil_div(p->k, p->oc_bn);
+  const int64_t kbt = neo_ceil_div(p->k_split > 0 ? p->k_split : p->k, p->oc_bn);
   kp.out_cb_off = p->out_cb_offset;
   kp.out_cb_total = p->out_cb_total > 0 ? p->out_cb_total : (int)kbt;
   kp.res_cb_off = p->res_cb_offset;
   kp.res_cb_total = p->res_cb_total > 0 ? p->res_cb_total : (int)kbt;
   kp.relu = p->relu;
+  if (p->k_split > 0) {
+    // two outputs: channels [0, k_split) -> out, [k_split, k) -> out2
+    NEO_CHECK_ARG(p->out2 != nullptr && p->k_split < p->k && p->k_split % BN == 0 &&
+                      p->k_split % p->oc_bn == 0 && (p->k - p->k_split) % p->oc_bn == 0,
+                  NEO_ERR_SCHEDULE_INVALID,
+                  "second output needs k_split (%lld) a multiple of the N tile (%d) below K",
+                  (long long)p->k_split, BN);
+    NEO_CHECK_ARG(!p->residual && !pair && !p->pro_scale && kp.splits == 1, NEO_ERR_UNSUPPORTED,
+                  "two-output convs take no residual, CTA pair, prologue or split-K");
+    NEO_CHECK_ARG(p->out2_cb_total >= 1 &&
+                      p->out2_cb_offset + (p->k - p->k_split) / p->oc_bn <= p->out2_cb_total,
+                  NEO_ERR_SHAPE_MISMATCH, "second output window out of range");
+    kp.k_split = (int)p->k_split;
+    kp.relu2 = p->relu2;
+    kp.out2_cb_off = p->out2_cb_offset;
+  }
   kp.out_f32 = p->out_dtype == NEO_F32;
   kp.round_tf32 = (p->flags & NEO_FLAG_ROUND_TF32) ? 1 : 0;
   kp.pro = p->pro_scale != nullptr;
@@ -1805,6 +1827,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.nslot = (int)std::min<int64_t>(slots, (kp.res_pf ? 2 : 1) * per_tile);
   }
   kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
+  NEO_CHECK_ARG(kp.tma_epi || !kp.k_split, NEO_ERR_UNSUPPORTED,
+                "two-output convs need the TMA-store epilogue (oc_bn rows of 32/64/128 bytes)");
   if (kp.tma_epi) {
     const int y = p->oc_bn;
     kp.rowb_out = rb_out;
@@ -1826,6 +1850,10 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     };
     CUresult r = encode_fm(&kp.tmO, p->out, kp.out_cb_total);
     NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map O encode failed (%d)", (int)r);
+    if (kp.k_split) {
+      r = encode_fm(&kp.tmO2, p->out2, p->out2_cb_total);
+      NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map O2 encode failed (%d)", (int)r);
+    }
     if (p->residual) {
       r = encode_fm(&kp.tmR, p->residual, kp.res_cb_total);
       NEO_CHECK_ARG(r == CUDA_SUCCESS, NEO_ERR_CUDA, "tensor map R encode failed (%d)", (int)r);

@@ -96,7 +96,9 @@ def pack_weights_umma(w_kcrs: torch.Tensor, x: int, mode: int, pad_channels: boo
 def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 0), ic_bn=1,
                 oc_bn=1, scale=None, shift=None, bias=None, residual=None, relu=False,
                 x_cb=(0, 0), out_cb=(0, 0), res_cb=(0, 0), flags=0, tile=None,
-                prologue=None) -> L.ConvParams:
+                prologue=None, second=None) -> L.ConvParams:
+    """``second`` = (out2, k_split, relu2, out2_cb): channels [k_split, k)
+    are written to out2 (two sibling convs as one launch)."""
     p = L.ConvParams()
     p.mode = mode
     p.x, p.w, p.out = _ptr(x), _ptr(w), _ptr(out)
@@ -118,6 +120,10 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
         for key in ("tile_w", "tile_h", "tile_img", "tile_n", "slices_per_stage", "stages",
                     "split_k", "cta_pair", "weight_stationary"):
             setattr(p, key, int(tile.get(key, 0) or 0))
+    if second is not None:
+        out2, k_split, relu2, out2_cb = second
+        p.out2, p.k_split, p.relu2 = _ptr(out2), int(k_split), int(bool(relu2))
+        p.out2_cb_offset, p.out2_cb_total = out2_cb
     return p
 
 

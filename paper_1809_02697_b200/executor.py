@@ -259,6 +259,30 @@ class DeviceProgram:
                 if info:
                     self.fused_head[info["anchor"]] = info
                     self.skip.update(info["skip"])
+        # sibling 1x1 convs over one input (a bottleneck's reduce conv and its
+        # projection shortcut, Inception's branch reducers) run as one
+        # two-output launch over concatenated weights
+        self.sibling: dict[int, tuple[int, int]] = {}   # first conv -> (second, tile_n)
+        self.sibling_of: dict[int, int] = {}            # second -> first
+        if self.mode in ("bf16", "tf32") and not os.environ.get("NEOB200_NO_SIBLING"):
+            groups: dict[int, list[int]] = {}
+            for nid in order:
+                if self._sibling_eligible(nid):
+                    groups.setdefault(g.nodes[nid].inputs[0][0], []).append(nid)
+            for convs in groups.values():
+                convs = list(convs)
+                while len(convs) >= 2:
+                    a = convs.pop(0)
+                    pick = None
+                    for b in convs:
+                        tn = self._sibling_tile(a, b)
+                        if tn:
+                            pick = (b, tn)
+                            break
+                    if pick:
+                        convs.remove(pick[0])
+                        self.sibling[a] = pick
+                        self.sibling_of[pick[0]] = a
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -332,6 +356,10 @@ class DeviceProgram:
                 tgt.last = last_step
         for nid in self.plan.input_ids:
             self.vals[nid].first = -1
+        for second, first in self.sibling_of.items():   # written by the first's launch
+            tgt = self._storage(second)
+            if tgt is not None:
+                tgt.first = min(tgt.first, self.step[first])
         # a concat buffer lives as long as any of its windows
         for v in self.vals.values():
             if v.win is not None:
@@ -445,6 +473,51 @@ class DeviceProgram:
         if lay.tag != "NCHWc" or lay.x not in (8, 16, 32, 64):
             return None
         return cv.id, mp.id, g.nodes[t].inputs[0][0]
+
+    def _conv_kcrs(self, nid: int) -> np.ndarray:
+        wv = self.g.nodes[self.g.nodes[nid].inputs[1][0]].attrs["value"]
+        return host_unpack_kcrs(wv) if wv.ndim == 6 else np.asarray(wv, np.float32)
+
+    def _sibling_eligible(self, nid: int) -> bool:
+        """Unpadded 1x1 tensor-core conv without residual or prologue over a
+        blocked input, writing a blocked map whose rows suit the TMA-store
+        epilogue."""
+        g = self.g
+        node = g.nodes[nid]
+        if node.kind != OpKind.Conv2d or nid in self.prologue or nid in self.skip:
+            return False
+        epi = node.attrs.get("epilogue") or {}
+        if epi.get("residual") or hw_pair(node.attrs["pad"]) != (0, 0):
+            return False
+        src = node.inputs[0][0]
+        if src in self.stem_fold or src in self.skip:
+            return False
+        k, c, r, s = self._conv_kcrs(nid).shape
+        if (r, s) != (1, 1):
+            return False
+        dl, ol = self.specs[src].layout, self.specs[nid].layout
+        if dl.tag != "NCHWc" or ol.tag != "NCHWc" or not tc_legal_block(dl.x, self.mode):
+            return False
+        if c % dl.x or k % ol.x or (ol.x * bytes_per_elem(self.mode)) not in (32, 64, 128):
+            return False
+        return True
+
+    def _sibling_tile(self, a: int, b: int) -> int:
+        """N tile of the merged launch (k_split = K of ``a`` must be a whole
+        number of tiles), or 0 when the pair should not merge."""
+        g = self.g
+        na, nb = g.nodes[a], g.nodes[b]
+        if hw_pair(na.attrs["stride"]) != hw_pair(nb.attrs["stride"]):
+            return 0
+        if self.specs[a].layout.x != self.specs[b].layout.x:
+            return 0
+        ka, kb = self._conv_kcrs(a).shape[0], self._conv_kcrs(b).shape[0]
+        # measured (B200, b64): merging pays when both halves fill 128-256
+        # wide N tiles; 64-wide tiles (the 56x56 64 -> 64 reducer) lose
+        for tn in (256, 128):
+            if ka % tn == 0 and kb >= tn:
+                return tn
+        return 0
 
     def _fused_head_info(self, nid: int) -> dict | None:
         """Chain global AvgPool -> (NCHW transform) -> Flatten -> Dense ->
@@ -643,7 +716,11 @@ class DeviceProgram:
                 continue
             out = self.vals[nid]
             ins = [self.vals.get(src) for src, _ in node.inputs]
-            if kind == OpKind.Conv2d:
+            if kind == OpKind.Conv2d and nid in self.sibling_of:
+                continue                      # launched with its sibling
+            if kind == OpKind.Conv2d and nid in self.sibling:
+                self._bind_conv_pair(node, g.nodes[self.sibling[nid][0]], self.sibling[nid][1])
+            elif kind == OpKind.Conv2d:
                 self._bind_conv(node, out)
             elif kind == OpKind.LayoutTransform:
                 if out.alias is None:
@@ -700,6 +777,55 @@ class DeviceProgram:
                 D.set_workspace(p, self.workspace)
 
     # conv ---------------------------------------------------------------------
+    def _bind_conv_pair(self, na, nb, tile_n: int):
+        """Two sibling 1x1 convs over one input as one tensor-core launch:
+        weights and epilogue vectors concatenated along the output channels,
+        channels [0, K_a) -> a's map, [K_a, K_a + K_b) -> b's map, each with its
+        own relu (kernels.py:185-197 order per channel)."""
+        from . import _lib as L
+        from . import device as D
+        g = self.g
+        data = self.vals[na.inputs[0][0]]
+        oa, ob = self.vals[na.id], self.vals[nb.id]
+        parts = []
+        for node in (na, nb):
+            epi = dict(node.attrs.get("epilogue") or {})
+            kcrs = self._conv_kcrs(node.id)
+            k = kcrs.shape[0]
+            bias = epi.get("bias")
+            if len(node.inputs) >= 3:
+                bb = g.nodes[node.inputs[2][0]].attrs["value"]
+                bias = bb if bias is None else bias + bb
+            scale, shift = epi.get("scale"), epi.get("shift")
+            parts.append({"w": kcrs, "k": k, "bias": bias, "scale": scale, "shift": shift,
+                          "relu": bool(epi.get("relu"))})
+        ka = parts[0]["k"]
+        cat = lambda key, fill: (None if all(p_[key] is None for p_ in parts) else np.concatenate(
+            [np.asarray(p_[key], np.float32) if p_[key] is not None
+             else np.full(p_["k"], fill, np.float32) for p_ in parts]))
+        scale, shift, bias = cat("scale", 1.0), cat("shift", 0.0), cat("bias", 0.0)
+        if scale is not None and shift is None:
+            shift = np.zeros(scale.shape, np.float32)
+        if shift is not None and scale is None:
+            scale = np.ones(shift.shape, np.float32)
+        vec = lambda v: None if v is None else self._upload(v)
+        w = np.concatenate([parts[0]["w"], parts[1]["w"]])
+        k, c = w.shape[0], w.shape[1]
+        n, _, h, wd = self.specs[na.inputs[0][0]].logical_nchw
+        ic_bn, oc_bn = data.px, oa.layout.x
+        mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
+        wdev = D.pack_weights_umma(self._upload(w), ic_bn, mode)
+        self.weights.append(wdev)
+        flags = self.round_flag | L.FLAG_STATIC_WEIGHTS
+        p = D.conv_params(mode, data.tensor, wdev, oa.tensor, n, c, h, wd, k, 1, 1,
+                          hw_pair(na.attrs["stride"]), (0, 0), ic_bn, oc_bn, vec(scale),
+                          vec(shift), vec(bias), None, parts[0]["relu"],
+                          x_cb=self._window(data), out_cb=self._window(oa), flags=flags,
+                          tile={"tile_n": tile_n},
+                          second=(ob.tensor, ka, parts[1]["relu"], self._window(ob)))
+        self.tc_params.append(p)
+        self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream))
+
     def _bind_conv(self, node, out: _Val):
         import torch
         from . import _lib as L

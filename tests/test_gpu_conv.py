@@ -420,3 +420,50 @@ def test_tc_conv_bn_relu_prologue(cuda, mode_name, shape):
             x_bn, mode), out_b, n, c, h, w, k, 3, 3, (1, 1), (1, 1), x_bn, y,
             prologue=(sc, sh, True))
         D.conv2d(bad)
+
+
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("ka,kb,tile_n,stride", [(128, 512, 128, 2), (256, 256, 256, 1),
+                                                 (128, 192, 128, 1)])
+def test_tc_conv_two_outputs(cuda, mode_name, ka, kb, tile_n, stride):
+    """Sibling 1x1 convs as one launch: channels [0, ka) -> out (relu, bias),
+    [ka, ka + kb) -> out2 (no relu, scale/shift) written into a channel window
+    of a larger buffer; each part matches its own oracle conv."""
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(ka + kb + stride)
+    n, c, h, w = 4, 128, 14, 14
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    act = torch.bfloat16 if mode_name == "bf16" else torch.float32
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wa = rnd((rng.standard_normal((ka, c, 1, 1)) * 0.1).astype(np.float32))
+    wb = rnd((rng.standard_normal((kb, c, 1, 1)) * 0.1).astype(np.float32))
+    ba = rng.normal(0, 0.1, ka).astype(np.float32)
+    sb = rng.uniform(0.5, 1.5, kb).astype(np.float32)
+    tb = rng.normal(0, 0.1, kb).astype(np.float32)
+    oh = (h - 1) // stride + 1
+    y = 8 if kb % 16 else 16
+    xb = 64 if mode_name == "bf16" else 32
+    xt = torch.from_numpy(pack_nchw(x, xb)).to(dev).to(act)
+    wd = D.pack_weights_umma(torch.from_numpy(np.concatenate([wa, wb])).to(dev), xb, mode)
+    oa = torch.empty((n, ka // y, oh, oh, y), dtype=act, device=dev)
+    ob = torch.full((n, kb // y + 3, oh, oh, y), 5.0, dtype=act, device=dev)
+    cat = lambda a, b: torch.from_numpy(np.concatenate([a, b]).astype(np.float32)).to(dev)
+    p = D.conv_params(mode, xt, wd, oa, n, c, h, w, ka + kb, 1, 1, (stride, stride), (0, 0),
+                      xb, y, cat(np.ones(ka), sb), cat(np.zeros(ka), tb), cat(ba, np.zeros(kb)),
+                      None, True, tile={"tile_n": tile_n},
+                      second=(ob, ka, False, (2, kb // y + 3)),
+                      flags=L.FLAG_ROUND_TF32 if mode_name == "tf32" else 0)
+    D.conv2d(p)
+    torch.cuda.synchronize()
+    ref_a = oracle.conv2d(x, wa, stride, 0, None, None, ba, relu=True)
+    ref_b = oracle.conv2d(x, wb, stride, 0, sb, tb, None, relu=False)
+    got_a = unpack_nchw(oa.float().cpu().numpy())
+    obn = ob.float().cpu().numpy()
+    got_b = unpack_nchw(obn[:, 2:2 + kb // y])
+    tol = 2e-2 if mode_name == "bf16" else 1e-3
+    assert oracle.rel_err(got_a, ref_a) < tol and oracle.rel_err(got_b, ref_b) < tol
+    assert np.all(obn[:, :2] == 5.0) and np.all(obn[:, 2 + kb // y:] == 5.0)
