@@ -305,8 +305,22 @@ extern "C" int neo_classifier_head(const void* x, const void* w_bf16, const floa
                                       (int)kSmem));
     attr_done[dev & 63] = true;
   }
-  neo_launch(head_kernel, dim3(grid), dim3(kThreads), kSmem, static_cast<cudaStream_t>(stream), p);
-  NEO_LAUNCH_CHECK();
+  // cooperative: the grid barriers need every CTA resident; the launch fails
+  // (instead of deadlocking) where that cannot be guaranteed (e.g. an MPS
+  // client limited to fewer SMs)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = neo_pdl_enabled() ? 2 : 1;
+  NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, head_kernel, p));
   return NEO_OK;
 }
 
