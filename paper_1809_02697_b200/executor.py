@@ -1287,9 +1287,11 @@ class DeviceProgram:
         if convert and not hasattr(self, "_host_stage"):
             # f32 host batch -> pinned bf16 (RN, multi-threaded on the host)
             # while the GPU runs the previous forward; half the PCIe bytes
+            # three host buffers: the rounding of a batch may run up to three
+            # batches ahead of the GPU, which absorbs host scheduling hiccups
             self._host_stage = [torch.empty(dst.shape, dtype=dst.dtype).pin_memory()
-                                for _ in range(2)]
-            self._host_done = [None, None]
+                                for _ in range(3)]
+            self._host_done = [None, None, None]
         n = dst.shape[0]
         chunks = [(lo, min(n, lo + max(1, n // 4))) for lo in range(0, n, max(1, n // 4))]
         for i, host in enumerate(batches):
@@ -1297,18 +1299,19 @@ class DeviceProgram:
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(self._consumed[slot])
             if convert:
-                if self._host_done[slot] is not None:
-                    self._host_done[slot].synchronize()     # its previous upload finished
+                hs = i % 3
+                if self._host_done[hs] is not None:
+                    self._host_done[hs].synchronize()       # its previous upload finished
                 # round and upload in batch chunks: the upload of one chunk
                 # overlaps the host rounding of the next
                 for lo, hi in chunks:
-                    self._host_stage[slot][lo:hi].copy_(host[lo:hi])
+                    self._host_stage[hs][lo:hi].copy_(host[lo:hi])
                     with torch.cuda.stream(self._copy_stream):
-                        self._staging[slot][lo:hi].copy_(self._host_stage[slot][lo:hi],
+                        self._staging[slot][lo:hi].copy_(self._host_stage[hs][lo:hi],
                                                          non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self._copy_stream)
-                self._host_done[slot] = ev
+                self._host_done[hs] = ev
             else:
                 with torch.cuda.stream(self._copy_stream):
                     self._staging[slot].copy_(host, non_blocking=True)
