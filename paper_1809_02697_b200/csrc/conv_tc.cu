@@ -286,20 +286,25 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         const int cc = col + q * kPer + 4 * j4;
         const float4 bi = *reinterpret_cast<const float4*>(par + 512 + cc);
         const float* vv = reinterpret_cast<const float*>(v) + q * kPer + 4 * j4;
+        // packed f32x2 FMA / add (FFMA2 / FADD2): the same IEEE RN operations
+        // as the scalar forms, half the instructions
+        const float2 v01 = make_float2(vv[0], vv[1]), v23 = make_float2(vv[2], vv[3]);
+        const float2 b01 = make_float2(bi.x, bi.y), b23 = make_float2(bi.z, bi.w);
+        float2 r01, r23;
         if constexpr (AFFINE) {
           const float4 sc = *reinterpret_cast<const float4*>(par + cc);
           const float4 sh = *reinterpret_cast<const float4*>(par + 256 + cc);
-          f[4 * j4 + 0] = fmaf(vv[0], sc.x, sh.x) + bi.x;
-          f[4 * j4 + 1] = fmaf(vv[1], sc.y, sh.y) + bi.y;
-          f[4 * j4 + 2] = fmaf(vv[2], sc.z, sh.z) + bi.z;
-          f[4 * j4 + 3] = fmaf(vv[3], sc.w, sh.w) + bi.w;
+          r01 = __fadd2_rn(__ffma2_rn(v01, make_float2(sc.x, sc.y), make_float2(sh.x, sh.y)), b01);
+          r23 = __fadd2_rn(__ffma2_rn(v23, make_float2(sc.z, sc.w), make_float2(sh.z, sh.w)), b23);
         } else {
           // identity scale/shift: fma(v, 1, 0) == v, so this is the same value
-          f[4 * j4 + 0] = vv[0] + bi.x;
-          f[4 * j4 + 1] = vv[1] + bi.y;
-          f[4 * j4 + 2] = vv[2] + bi.z;
-          f[4 * j4 + 3] = vv[3] + bi.w;
+          r01 = __fadd2_rn(v01, b01);
+          r23 = __fadd2_rn(v23, b23);
         }
+        f[4 * j4 + 0] = r01.x;
+        f[4 * j4 + 1] = r01.y;
+        f[4 * j4 + 2] = r23.x;
+        f[4 * j4 + 3] = r23.y;
       }
       const uint32_t off = swz_offset(m, c * kChunks16 + q, p.rowb_out);
       uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
