@@ -341,8 +341,12 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
           const uint32_t* r = reinterpret_cast<const uint32_t*>(&rv);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(r[j]));
-            if (relu) asm("max.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(0u));
+            // relu(h * 1 + r): h * 1 is exact, so this is the rounded bf16
+            // add followed by the clamp, in one packed instruction
+            if (relu)
+              asm("fma.rn.relu.bf16x2 %0, %0, %1, %2;" : "+r"(h[j]) : "r"(0x3F803F80u), "r"(r[j]));
+            else
+              asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(r[j]));
           }
         }
         *slot = packed;
