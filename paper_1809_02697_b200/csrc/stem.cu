@@ -355,9 +355,15 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
 #pragma unroll
             for (int e = 0; e < 8; ++e) f[e] = fmaf(__uint_as_float(v[h * 8 + e]), sc[e], sh[e]) + bi[e];
           } else {
-            // identity scale/shift: fma(v, 1, 0) == v
+            // identity scale/shift: fma(v, 1, 0) == v; packed f32x2 adds
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[h * 8 + e]) + bi[e];
+            for (int e = 0; e < 8; e += 2) {
+              const float2 r = __fadd2_rn(make_float2(__uint_as_float(v[h * 8 + e]),
+                                                      __uint_as_float(v[h * 8 + e + 1])),
+                                          make_float2(bi[e], bi[e + 1]));
+              f[e] = r.x;
+              f[e + 1] = r.y;
+            }
           }
           uint32_t o[4];
 #pragma unroll
