@@ -272,6 +272,11 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
                                               int c_step) {
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
+  // swz_offset(m, chunk, rowb) hoisted: the row's base and its XOR pattern
+  // are fixed per thread (chunk * 16 < rowb keeps o >> 7 == base >> 7)
+  const uint32_t srow = (uint32_t)m * (uint32_t)p.rowb_out;
+  const uint32_t smask = p.rowb_out == 128 ? 7u : p.rowb_out == 64 ? 3u : p.rowb_out == 32 ? 1u : 0u;
+  const uint32_t sxr = (srow >> 7) & smask;
   // one chunk: 16 accumulator columns of row m -> scale/shift/bias
   // (+ residual from the slot) -> relu -> the swizzled staging slot
   auto finish = [&](const uint32_t (&v)[16], int c) {
@@ -306,7 +311,7 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         f[4 * j4 + 2] = r23.x;
         f[4 * j4 + 3] = r23.y;
       }
-      const uint32_t off = swz_offset(m, c * kChunks16 + q, p.rowb_out);
+      const uint32_t off = srow + ((((uint32_t)(c * kChunks16 + q)) ^ sxr) << 4);
       uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
       if constexpr (OUT_F32) {
         float o[4];
