@@ -1291,16 +1291,29 @@ class DeviceProgram:
             # batches ahead of the GPU, which absorbs host scheduling hiccups
             self._host_stage = [torch.empty(dst.shape, dtype=dst.dtype).pin_memory()
                                 for _ in range(3)]
-            self._host_done = [None, None, None]
+            self._host_done = [torch.cuda.Event() for _ in range(3)]
+            self._host_used = [False, False, False]
         n = dst.shape[0]
         chunks = [(lo, min(n, lo + max(1, n // 4))) for lo in range(0, n, max(1, n // 4))]
+        # a collector pause inside the loop would stall the uploads behind it
+        import gc
+        gc_was = gc.isenabled()
+        gc.disable()
+        try:
+            self._pipeline_loop(batches, outputs, dst, out_dev, convert, chunks)
+        finally:
+            if gc_was:
+                gc.enable()
+
+    def _pipeline_loop(self, batches, outputs, dst, out_dev, convert, chunks):
+        import torch
         for i, host in enumerate(batches):
             slot = i & 1
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(self._consumed[slot])
             if convert:
                 hs = i % 3
-                if self._host_done[hs] is not None:
+                if self._host_used[hs]:
                     self._host_done[hs].synchronize()       # its previous upload finished
                 # round and upload in batch chunks: the upload of one chunk
                 # overlaps the host rounding of the next
@@ -1309,9 +1322,8 @@ class DeviceProgram:
                     with torch.cuda.stream(self._copy_stream):
                         self._staging[slot][lo:hi].copy_(self._host_stage[hs][lo:hi],
                                                          non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self._copy_stream)
-                self._host_done[hs] = ev
+                self._host_done[hs].record(self._copy_stream)
+                self._host_used[hs] = True
             else:
                 with torch.cuda.stream(self._copy_stream):
                     self._staging[slot].copy_(host, non_blocking=True)
