@@ -724,9 +724,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       for (int i = 0;; ++i) {
         const int u = cta_unit(p, i, rank);
         if (u < 0) break;
-        const int t = u / p.splits;
-        const int ks0 = (u - t * p.splits) * p.kps;
-        const int ks1 = min(p.kstages, ks0 + p.kps);
+        const int t = p.splits == 1 ? u : u / p.splits;
+        const int ks0 = p.splits == 1 ? 0 : (u - t * p.splits) * p.kps;
+        const int ks1 = p.splits == 1 ? p.kstages : min(p.kstages, ks0 + p.kps);
         int n0, oh0, ow0, k0;
         decode_tile(p, t, n0, oh0, ow0, k0);
         const int iw0 = ow0 * p.stride_w - p.pad_w;
@@ -953,14 +953,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     };
     // pair: accumulator releases go to the leader CTA's tempty barriers
     const uint32_t tempty_base = PAIR ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
+    const uint32_t ng_log2 = (uint32_t)(__ffs(p.ngroups) - 1);
     for (int it = grp;; it += p.ngroups) {
       const int u = cta_unit(p, it, rank);
       if (u < 0) break;
-      const int t = u / p.splits;
+      const int t = p.splits == 1 ? u : (int)((uint32_t)u / (uint32_t)p.splits);
       int n0, oh0, ow0, k0;
       decode_tile(p, t, n0, oh0, ow0, k0);
       const int acc = grp;
-      const uint32_t acc_phase = (it / p.ngroups) & 1;
+      const uint32_t acc_phase = ((uint32_t)it >> ng_log2) & 1u;   // ngroups is 2 or 4
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.BN;
       const int ncols = min(p.BN, p.K - k0);
       if (p.splits > 1) {
@@ -1017,7 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const bool has_res = p.res != nullptr;
         const int nblk = ncols / p.y;
         const bool pf = p.res_pf != 0;
-        const int lt = it / p.ngroups;            // this group's tile counter
+        const int lt = (int)((uint32_t)it >> ng_log2);   // this group's tile counter
         const int set = pf ? (lt & 1) : 0;        // prefetch: alternate slot sets
         const uint32_t sgrp = sO + (grp * p.nslot + set * (p.nslot / 2)) * p.stage_out;
         uint8_t* sgrp_gen = gen_base + (sgrp - sA);
