@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
     ap.add_argument("--mode", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--untuned", action="store_true", help="ignore the tuned tile schedules")
+    ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-mode measurement")
     return ap.parse_args()
 
 
@@ -142,11 +143,13 @@ def reference_cpu(model: str, per_step: int, steps: int, warmup: int, seconds: f
         pool = neo.ThreadPool(cores)
         run = lambda: neo.execute(ng, feeds, pool)
         kind = "reference"
+        cpu_id = neo.cpu_identifier()
     except Exception as exc:   # reference not installed: numpy restatement
         import oracle
         cores = os.cpu_count() or 1
         run = lambda: oracle.execute_reference(g, feeds)
         kind = f"port ({type(exc).__name__})"
+        cpu_id = _cpu_model()
     for _ in range(max(1, warmup)):
         run()
     times = []
@@ -162,24 +165,40 @@ def reference_cpu(model: str, per_step: int, steps: int, warmup: int, seconds: f
             "kind": "reference" if kind == "reference" else "port",
             "sample": f"{model} batch {per_step} x {len(times)} steps "
                       f"({kind}, optimized graph, ThreadPool over physical cores)",
-            "seconds": total}
+            "cpu_identifier": cpu_id, "seconds": total}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    per_step = 2
+    # one full batch per step (b >= 64 is timed as a whole
+    # batch), so the reference arm runs the same config as ours
+    per_step = args.batch
     res = reference_cpu(args.model, per_step, args.steps, args.warmup, 1e9)
     ms = 1000.0 * res["seconds"] / max(1, args.steps)
     line = {"metric": METRIC, "value": res["value"], "unit": "images/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1), random init)",
-            "config": {"workload": f"{args.model} inference, {per_step} images/step sample of the "
-                                   f"batch-{args.batch} workload, 224x224, reference CPU path",
-                       "model": args.model},
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": f"{args.model} v1 inference, batch {per_step} per step, "
+                                   f"224x224, reference CPU path (f32)",
+                       "model": args.model, "global_batch": per_step, "per_gpu_batch": per_step,
+                       "image": 224},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                 "cpu_identifier")},
             "e2e": {"value": res["value"], "unit": "images/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -188,12 +207,14 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 
 def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind: str,
-                  flush=None):
+                  flush=None, peak_tflops=None, peak_name="bf16 burst"):
     """Conv time per step = (graphed step) - (the same graph without the
     conv launches), both replayed after an L2 flush and timed with CUDA
-    events on the executor stream; returns (roofline dict, conv share of
-    the step)."""
-    from paper_1809_02697_b200.timing import graph_time
+    events on the executor stream; plus the per-launch table (in-graph
+    times from timing.timed_launches: an event-record node between
+    consecutive launches of the captured step).  Returns (roofline dict,
+    conv share of the step)."""
+    from paper_1809_02697_b200.timing import graph_time, timed_launches
     # conv launches: the tensor-core convs and the fused image stem (its conv
     # FLOPs are part of flops_per_step; it also runs the stem's max pool)
     conv_idx = [i for i, n in enumerate(prog.launch_names)
@@ -201,34 +222,106 @@ def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind
     cset = set(conv_idx)
     step_s = graph_time(prog, lambda i: True, steps, flush)
     rest_s = graph_time(prog, lambda i: i not in cset, steps, flush)
-    totals = [max(step_s - rest_s, 1e-9)]
-    step_times = [step_s]
-    conv_s = float(np.median(totals))
+    conv_s = max(step_s - rest_s, 1e-9)
     achieved = flops_per_step / conv_s / 1e12
-    pk = float(peak.get("bf16_tflops_sustained", peak.get("bf16_tflops", 1400.0)))
+    # the timed region is short (tens of ms at max clock): the burst peak
+    # applies (MEASURED_PEAKS.json bf16_tflops); sustained is reported beside it
+    pk = float(peak_tflops if peak_tflops is not None else peak.get("bf16_tflops", 1643.1))
+    hbm = float(peak.get("hbm_gbs", 6557.4))
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and peak_name.startswith("bf16"):
         try:
             traffic = json.load(open(tpath)).get("bytes_per_step")
         except Exception:
             traffic = None
-    # memory-bound launches (everything but the convs): algorithmic bytes over
-    # their graphed time, against the 8 TB/s nominal and the measured copy peak
-    mem_bytes = sum(b for i, b in enumerate(prog.launch_bytes) if i not in cset)
-    mem_ops = {"launches": len(prog.launches) - len(conv_idx), "time_us": rest_s * 1e6,
+    conv_bytes = sum(prog.launch_bytes[i] for i in conv_idx)
+    # per-launch table (in-graph, L2 flushed before each replay)
+    per = timed_launches(prog, steps, flush)
+    table = []
+    for i, name in enumerate(prog.launch_names):
+        us = float(per[i]) * 1e3
+        fl, nb = prog.launch_flops[i], prog.launch_bytes[i]
+        t_tc = fl / (pk * 1e12) if fl else 0.0
+        t_hbm = nb / (hbm * 1e9)
+        roof = max(t_tc, t_hbm) * 1e6
+        table.append({"launch": name, "desc": prog.launch_desc[i], "us": round(us, 2),
+                      "tflops": round(fl / max(us, 1e-3) / 1e6, 1) if fl else None,
+                      "gbs": round(nb / max(us, 1e-3) / 1e3, 1),
+                      "bound": "tensor" if t_tc >= t_hbm else "hbm",
+                      "roofline_us": round(roof, 2),
+                      "frac_of_roofline": round(roof / max(us, 1e-3), 3)})
+    mem_idx = [i for i in range(len(prog.launches)) if i not in cset]
+    mem_bytes = sum(prog.launch_bytes[i] for i in mem_idx)
+    mem_ops = {"launches": len(mem_idx), "time_us": rest_s * 1e6,
                "algorithmic_bytes": mem_bytes,
                "achieved_GBps": mem_bytes / max(rest_s, 1e-12) / 1e9,
-               "peak_nominal_GBps": 8000.0,
-               "peak_measured_GBps": float(peak.get("hbm_gbs", 6531.6))}
-    mem_ops["frac_of_measured"] = mem_ops["achieved_GBps"] / mem_ops["peak_measured_GBps"]
+               "peak_nominal_GBps": 8000.0, "peak_measured_GBps": hbm}
+    mem_ops["frac_of_measured"] = mem_ops["achieved_GBps"] / hbm
     roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
             "frac": achieved / pk, "traffic": traffic,
+            "algorithmic_bytes": conv_bytes,
+            "traffic_note": "ncu dram__bytes read+write of the step's conv launches "
+                            "(profiles/conv_traffic.json; L2 left warm by the previous launch)",
             "kernel": "conv_tc_kernel + stem_conv_pool_kernel (all %d conv launches of one step)"
                       % len(conv_idx),
-            "conv_ms_per_step": conv_s * 1e3, "peak_source": f"{peak_kind} bf16 sustained"}
-    roof["memory_bound_ops"] = mem_ops
-    return roof, conv_s / float(np.median(step_times))
+            "conv_ms_per_step": conv_s * 1e3, "peak_source": f"{peak_kind} {peak_name}",
+            "frac_of_sustained": achieved / float(peak.get("bf16_tflops_sustained", pk))
+            if peak_name.startswith("bf16") else None,
+            "per_layer_roofline_ms": sum(t["roofline_us"] for i, t in enumerate(table)
+                                         if i in cset) / 1e3,
+            "per_conv": [t for i, t in enumerate(table) if i in cset],
+            "memory_bound_ops": mem_ops,
+            "memory_bound_launches": [t for i, t in enumerate(table) if i not in cset]}
+    return roof, conv_s / step_s
+
+
+def measure_tf32_peak(device) -> float:
+    """TF32 dense tensor peak measured on this box the way MEASURED_PEAKS.json
+    measures bf16 (torch.matmul 8192^3, best of 10, CUDA events) with
+    allow_tf32 -- MEASURED_PEAKS.json has no TF32 figure."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=device)
+        b = torch.randn(n, n, device=device)
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        return 2.0 * n ** 3 / best / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def time_program(prog, feeds, steps, warmup, flush, stream=None):
+    """Device seconds of ``steps`` graphed forwards (inputs resident, L2
+    flushed between steps outside the events)."""
+    import torch
+    stream = stream or prog.stream
+    prog.set_inputs(feeds)
+    for _ in range(max(3, warmup)):
+        prog.launch()
+    stream.synchronize()
+    evs = []
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        prog.launch()
+        b.record(stream)
+        evs.append((a, b))
+    stream.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) * 1e-3
 
 
 def main():
@@ -254,12 +347,15 @@ def main():
     tuned = db is not None and tuned_assignment(g, db, args.mode) is not None
     planned = compile_graph(g, mode=args.mode, db=db)
     prog = DeviceProgram(ExecutablePlan.compile(planned), local, args.mode)
-    feeds = model_input(g, seed=1 + rank)
+    # three distinct seeded batches per rank (the e2e loop rotates them)
+    feed_sets = [model_input(g, seed=1 + 3 * rank + j) for j in range(3)]
+    feeds = feed_sets[0]
     name = prog.input_names()[0]
-    pinned = torch.from_numpy(feeds[name]).pin_memory()
+    pinned = [torch.from_numpy(f[name]).pin_memory() for f in feed_sets]
     out_t = prog.output_tensors()[0]
     stream = prog.stream
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=local)
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=local)
+    flush = lambda: flush_buf.fill_(1.0)
 
     def barrier():
         torch.cuda.synchronize()
@@ -278,7 +374,7 @@ def main():
         wall0 = time.perf_counter()
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
-                flush.fill_(1.0)          # L2 flush between steps, outside the events
+                flush()                   # L2 flush between steps, outside the events
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             prog.launch()
@@ -289,27 +385,49 @@ def main():
     barrier()
     dev_s = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
     # ---- end to end through the public API: every step uploads its pinned
-    # host batch (copy stream, double-buffered, overlapping the previous
-    # forward) and reads the result back to pinned host memory ------------
+    # host batch (three distinct batches in rotation; copy stream,
+    # double-buffered, overlapping the previous forward) and reads the
+    # result back to pinned host memory --------------------------------
     outs = [torch.empty(out_t.shape, dtype=out_t.dtype).pin_memory()
             for _ in range(args.steps + args.warmup)]
-    prog.pipeline([pinned] * args.warmup, outs[:args.warmup])
+    rot = lambda k: [pinned[i % 3] for i in range(k)]
+    prog.pipeline(rot(args.warmup), outs[:args.warmup])
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(prog._copy_stream)
-    prog.pipeline([pinned] * args.steps, outs[args.warmup:])
+    prog.pipeline(rot(args.steps), outs[args.warmup:])
     e1.record(stream)
     e1.synchronize()
     barrier()
     e2e_s = e0.elapsed_time(e1) * 1e-3
     out_host = outs[-1]
-    # ---- dominant-kernel roofline: per-launch events inside the graphed
-    # step (L2 flushed before each replay, like the timed steps) ----------
+    # ---- dominant-kernel roofline -----------------------------------------
     pk, pk_kind = peaks()
-    roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind,
-                                     flush=lambda: flush.fill_(1.0))
+    roof, conv_share = conv_roofline(prog, 3, flops_step, pk, pk_kind, flush=flush)
     barrier()
+
+    # ---- tf32 mode (the reference's f32 semantics on TF32 tensor cores) ----
+    tf32 = None
+    if args.mode == "bf16" and not args.no_tf32 and world == 1:
+        try:
+            tf_peak = measure_tf32_peak(local)
+            tprog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode="tf32")), local,
+                                  "tf32")
+            t_s = time_program(tprog, feeds, args.steps, args.warmup, flush)
+            troof, _ = conv_roofline(tprog, 3, flops_step, pk, pk_kind, flush=flush,
+                                     peak_tflops=tf_peak, peak_name="tf32 measured on this box")
+            tf32 = {"value": args.batch * args.steps / t_s, "unit": "images/s",
+                    "ms_per_step": 1e3 * t_s / args.steps,
+                    "schedules": "in-kernel default tiles (no tf32 DB entries)",
+                    "roofline": {k: troof[k] for k in ("bound", "achieved", "peak", "unit",
+                                                       "frac", "conv_ms_per_step",
+                                                       "peak_source", "per_layer_roofline_ms")},
+                    "tf32_peak_tflops": tf_peak, "gpu_launches_per_step": tprog.kernel_launches}
+            del tprog
+        except Exception as exc:
+            tf32 = {"error": f"{type(exc).__name__}: {exc}"}
+        barrier()
 
     times = torch.tensor([dev_s, e2e_s, wall], dtype=torch.float64, device=local)
     if world > 1:
@@ -322,7 +440,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = reference_cpu(args.model, 2, 50, 1, args.cpu_seconds)
+            cpu = reference_cpu(args.model, args.batch, 50, 1, args.cpu_seconds)
             cpu.pop("seconds", None)
         except Exception as exc:
             cpu = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
@@ -346,11 +464,14 @@ def main():
                        "wall_s_timed_region": wall},
             "e2e": {"value": e2e_value, "unit": "images/s",
                     "h2d_bytes_per_step": int(prog.upload_bytes),
-                    "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size())},
+                    "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size()),
+                    "inputs": "3 distinct pinned f32 batches in rotation, rounded to bf16 on the "
+                              "host (the stem rounds RN anyway) and uploaded every step"},
             "gpu_launches": prog.kernel_launches * args.steps,
             "launches_per_step": prog.kernel_launches,
             "roofline": roof,
             "conv_share_of_step": conv_share,
+            "tf32": tf32,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

@@ -155,6 +155,11 @@ int neo_classifier_head(const void* x, const void* w_bf16, const float* bias, vo
  * Epilogue kernels.py:74-87 applied in the order scale/shift -> bias ->
  * residual -> relu, kernels.py:185-197) --------------------------------- */
 typedef struct neo_conv_params {
+  /* sizeof(neo_conv_params) as the caller compiled it (ABI v2+): every entry
+   * point taking the struct rejects a mismatch with NEO_ERR_INVALID_ARG, so a
+   * binding written against an older layout fails loudly instead of letting
+   * the library read fields past the end of a shorter struct. */
+  int struct_size;
   int mode;            /* neo_conv_mode                                       */
   const void* x;       /* input  (n, cb_total_x, h, w, ic_bn); window below    */
   const void* w;       /* FP32: KCRS[ic_bn]c[oc_bn]k f32; TF32/BF16: umma image */
@@ -218,6 +223,8 @@ typedef struct neo_conv_params {
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);
+/* sizeof(neo_conv_params) of the library build (what struct_size must hold) */
+int neo_conv_params_size(void);
 /* fill the automatic tile fields of *p the way neo_conv2d_nchwc_fused would */
 int neo_conv_default_tiles(neo_conv_params* p);
 /* Split-K workspace bytes the launch of *p needs with its resolved tiles

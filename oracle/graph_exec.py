@@ -46,7 +46,7 @@ def _kind(n) -> str:
     return getattr(n.kind, "value", n.kind)
 
 
-def _conv(n, vals):
+def _conv(n, vals, arith=None):
     data = vals[n.inputs[0][0]]
     weight = vals[n.inputs[1][0]]
     epi = dict(n.attrs.get("epilogue") or {})
@@ -68,8 +68,9 @@ def _conv(n, vals):
             weight = ops.unpack_kcrs(weight)
         if residual is not None:
             residual = ops.unpack_nchw(residual)
-    out = ops.conv2d(data, weight, stride, pad, epi.get("scale"), epi.get("shift"),
-                     bias, residual, bool(epi.get("relu", False)))
+    args = (data, weight, stride, pad, epi.get("scale"), epi.get("shift"), bias, residual,
+            bool(epi.get("relu", False)))
+    out = ops.conv2d(*args) if arith is None else ops.conv2d_rounded(arith, *args)
     if blocked:
         sch = n.attrs.get("schedule") or {}
         y = sch.get("oc_bn") or (vals[n.inputs[1][0]].shape[5]
@@ -78,9 +79,11 @@ def _conv(n, vals):
     return out
 
 
-def execute_reference(graph, inputs: dict) -> list[np.ndarray]:
+def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.ndarray]:
     """Run ``graph`` on numpy ``inputs`` (name -> array); outputs in
-    ``graph.outputs`` order."""
+    ``graph.outputs`` order.  ``arith`` ("bf16" / "tf32") models the
+    roundings of a single-pass tensor-core mode in every conv
+    (ops.conv2d_rounded); None is the reference's f32 arithmetic."""
     vals: dict[int, np.ndarray] = {}
     for nid in _topo(graph):
         n = graph.nodes[nid]
@@ -95,7 +98,7 @@ def execute_reference(graph, inputs: dict) -> list[np.ndarray]:
         elif k == "Constant":
             vals[nid] = np.asarray(n.attrs["value"], dtype=np.float32)
         elif k == "Conv2d":
-            vals[nid] = _conv(n, vals)
+            vals[nid] = _conv(n, vals, arith)
         elif k == "ReLU":
             vals[nid] = ops.relu(src[0])
         elif k == "Softmax":

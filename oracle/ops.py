@@ -208,3 +208,29 @@ def softmax(a):
     a = a.astype(np.float32)
     e = np.exp(a - a.max(axis=-1, keepdims=True))
     return (e / e.sum(axis=-1, keepdims=True)).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# arithmetic model of the single-pass tensor-core modes (TEST INFRASTRUCTURE:
+# used to show what the bf16 / tf32 number formats alone cost on a graph, so
+# a device error can be judged against the error of its own arithmetic).
+
+def round_rn(a: np.ndarray, kind: str | None) -> np.ndarray:
+    """Round f32 values to bf16 (8-bit significand) or tf32 (11-bit) with
+    round-to-nearest-even, kept in f32 storage; ``None`` is the identity."""
+    if kind is None:
+        return a
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    drop = 16 if kind == "bf16" else 13
+    u = (u + ((1 << (drop - 1)) - 1) + ((u >> drop) & 1)) & (0xFFFFFFFF ^ ((1 << drop) - 1))
+    return u.astype(np.uint32).view(np.float32).reshape(np.shape(a))
+
+
+def conv2d_rounded(kind, x, w, stride=1, pad=0, scale=None, shift=None, bias=None,
+                   residual=None, relu=False):
+    """conv2d with the operand and storage roundings of a single-pass
+    ``kind`` tensor-core conv: activations and (folded) weights rounded RN
+    to ``kind``, f32 accumulation and epilogue, output rounded RN."""
+    out = conv2d(round_rn(x, kind), round_rn(w, kind), stride, pad, scale, shift, bias,
+                 residual, relu)
+    return round_rn(out, kind)

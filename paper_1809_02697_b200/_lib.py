@@ -45,9 +45,15 @@ _c_vp = ctypes.c_void_p
 
 
 class ConvParams(ctypes.Structure):
-    """Mirror of ``neo_conv_params``."""
+    """Mirror of ``neo_conv_params`` (ABI v2: leading struct_size, filled in
+    by the constructor and checked by the library)."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self.struct_size = ctypes.sizeof(ConvParams)
 
     _fields_ = [
+        ("struct_size", _c_int),
         ("mode", _c_int),
         ("x", _c_vp), ("w", _c_vp), ("out", _c_vp),
         ("scale", _c_vp), ("shift", _c_vp), ("bias", _c_vp),
@@ -96,6 +102,7 @@ SIGNATURES = {
                                      _c_i64, _c_i64, _c_int, _c_i64, _c_int, _c_vp]),
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
     "neo_conv2d_nchwc_fused": (_c_int, [ctypes.POINTER(ConvParams), _c_vp]),
+    "neo_conv_params_size": (_c_int, []),
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),
     "neo_conv_workspace_bytes": (_c_int, [ctypes.POINTER(ConvParams), ctypes.POINTER(_c_i64)]),
     "neo_pool2d": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,

@@ -23,7 +23,11 @@ extern "C" {
 
 const char* neo_last_error(void) { return g_err; }
 
-int neo_abi_version(void) { return 1; }
+// v2: neo_conv_params gained a leading struct_size (checked by every entry
+// point that takes the struct)
+int neo_abi_version(void) { return 2; }
+
+int neo_conv_params_size(void) { return (int)sizeof(neo_conv_params); }
 
 int neo_device_info(int device, char* buf, int buflen) {
   NEO_CHECK_ARG(buf && buflen > 0, NEO_ERR_INVALID_ARG, "null buffer");
@@ -36,6 +40,9 @@ int neo_device_info(int device, char* buf, int buflen) {
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream) {
   NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
+  NEO_CHECK_ARG(p->struct_size == (int)sizeof(neo_conv_params), NEO_ERR_INVALID_ARG,
+                "neo_conv_params.struct_size %d != %d (ABI v%d layout)", p->struct_size,
+                (int)sizeof(neo_conv_params), neo_abi_version());
   NEO_CHECK_ARG(p->x && p->w && p->out, NEO_ERR_INVALID_ARG, "null tensor pointer");
   NEO_CHECK_ARG(p->n >= 1 && p->c >= 1 && p->h >= 1 && p->w_in >= 1 && p->k >= 1 && p->r >= 1 &&
                     p->s >= 1,

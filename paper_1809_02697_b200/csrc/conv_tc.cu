@@ -331,33 +331,30 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
         }
         *reinterpret_cast<float4*>(slot) = make_float4(o[0], o[1], o[2], o[3]);
       } else {
-        // bf16 output: the conv result (after scale/shift/bias) is rounded
-        // to bf16 once, the residual is added in packed bf16 (one rounding,
-        // as a separate bf16 add of the rounded conv output would do) and
-        // relu clamps the packed pair; without a residual the relu is fused
-        // into the conversion (rounding keeps the sign)
+        // bf16 output in the reference order (kernels.py:185-197): the
+        // residual (bf16 -> f32 is exact) is added to the f32 conv result,
+        // then ONE rounding to bf16 with the relu fused into the conversion
+        // (rounding keeps the sign, so relu(rn(v)) == rn(relu(v)))
         uint4 packed;
         uint32_t* h = reinterpret_cast<uint32_t*>(&packed);
         const bool relu = relu_floor == 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (!HAS_RES && relu)
-            asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
-          else
-            asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
-        }
         if constexpr (HAS_RES) {
           const uint4 rv = *slot;
           const uint32_t* r = reinterpret_cast<const uint32_t*>(&rv);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            // relu(h * 1 + r): h * 1 is exact, so this is the rounded bf16
-            // add followed by the clamp, in one packed instruction
-            if (relu)
-              asm("fma.rn.relu.bf16x2 %0, %0, %1, %2;" : "+r"(h[j]) : "r"(0x3F803F80u), "r"(r[j]));
-            else
-              asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(h[j]) : "r"(r[j]));
+            const float2 rf = make_float2(__uint_as_float(r[j] << 16), __uint_as_float(r[j] & 0xFFFF0000u));
+            const float2 s = __fadd2_rn(make_float2(f[2 * j], f[2 * j + 1]), rf);
+            f[2 * j] = s.x;
+            f[2 * j + 1] = s.y;
           }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (relu)
+            asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
+          else
+            asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h[j]) : "f"(f[2 * j]), "f"(f[2 * j + 1]));
         }
         *slot = packed;
       }
@@ -1404,6 +1401,9 @@ static int wst_band_rows(const neo_conv_params* p, int BW) {
 
 int neo_conv_default_tiles(neo_conv_params* p) {
   NEO_CHECK_ARG(p != nullptr, NEO_ERR_INVALID_ARG, "null params");
+  NEO_CHECK_ARG(p->struct_size == (int)sizeof(neo_conv_params), NEO_ERR_INVALID_ARG,
+                "neo_conv_params.struct_size %d != %d", p->struct_size,
+                (int)sizeof(neo_conv_params));
   if (p->mode == NEO_MODE_FP32) return NEO_OK;
   const int es = p->mode == NEO_MODE_BF16 ? 2 : 4;
   const int rowb = p->ic_bn * es;
@@ -1597,6 +1597,9 @@ int64_t conv_num_tiles(const neo_conv_params* p) {
 // bytes of split-K workspace the launch of *p needs (0: no split)
 int neo_conv_workspace_bytes(const neo_conv_params* pin, int64_t* bytes) {
   NEO_CHECK_ARG(pin != nullptr && bytes != nullptr, NEO_ERR_INVALID_ARG, "null argument");
+  NEO_CHECK_ARG(pin->struct_size == (int)sizeof(neo_conv_params), NEO_ERR_INVALID_ARG,
+                "neo_conv_params.struct_size %d != %d", pin->struct_size,
+                (int)sizeof(neo_conv_params));
   *bytes = 0;
   if (pin->mode == NEO_MODE_FP32) return NEO_OK;
   neo_conv_params pc = *pin;

@@ -140,8 +140,11 @@ class DeviceProgram:
         self.tc_params: list = []       # tensor-core conv params (split-K workspace)
         self.launch_names: list[str] = []
         self.launch_bytes: list[int] = []
+        self.launch_flops: list[int] = []
+        self.launch_desc: list[str] = []
         self.vals: dict[int, _Val] = {}
         self.weights: list = []         # device tensors kept alive
+        self._pinned_inputs: dict = {}  # input id -> (pinned staging, upload-done event)
         self.graph_exec = None
         self.use_graph = use_graph
         with torch.cuda.device(self.device):
@@ -545,6 +548,8 @@ class DeviceProgram:
                 cur = nxt.id
                 continue
             if nxt.kind == OpKind.Dense and nxt.inputs[0][0] == cur:
+                if nxt.id in self.skip or nxt.id in self.fused_dense_relu.values():
+                    return None       # the Dense is already fused into its ReLU
                 chain.append(nxt.id)
                 cur = nxt.id
                 if len(self.users[cur]) == 1 and cur not in protected:
@@ -691,12 +696,29 @@ class DeviceProgram:
                 v.tensor = base.tensor.reshape(v.shape)
 
     # -- launches --------------------------------------------------------------
-    def _emit(self, name, fn, nbytes: int = 0):
-        """Append a launch; ``nbytes`` = its algorithmic HBM bytes (memory-
-        bound operators: what the kernel must read and write once)."""
+    def _emit(self, name, fn, nbytes: int = 0, flops: int = 0, desc: str = ""):
+        """Append a launch; ``nbytes`` = its algorithmic HBM bytes (what the
+        kernel must read and write once), ``flops`` its algorithmic FLOPs
+        (2 per MAC; convs / dense), ``desc`` a shape summary."""
         self.launches.append(fn)
         self.launch_names.append(name)
         self.launch_bytes.append(int(nbytes))
+        self.launch_flops.append(int(flops))
+        self.launch_desc.append(desc)
+
+    def _conv_work(self, n, c, h, w, k, r, s, stride, pad, es, residual=False, kb=None):
+        """(flops, algorithmic bytes, desc) of one conv:
+        FLOP = 2 N K C R S OH OW; bytes = (in + weights + out [+ residual])."""
+        sh, sw = stride
+        ph, pw = pad
+        oh = (h + 2 * ph - r) // sh + 1
+        ow = (w + 2 * pw - s) // sw + 1
+        flops = 2 * n * k * c * r * s * oh * ow
+        out = n * k * oh * ow
+        nbytes = es * (n * c * h * w + k * c * r * s + out * (2 if residual else 1))
+        desc = (f"{r}x{s}/{sh} C{c} K{k if kb is None else kb} {h}x{w}->{oh}x{ow} n{n}"
+                + (" +res" if residual else ""))
+        return flops, nbytes, desc
 
     def _upload(self, arr, dtype=None):
         import torch
@@ -824,7 +846,10 @@ class DeviceProgram:
                           tile={"tile_n": tile_n},
                           second=(ob.tensor, ka, parts[1]["relu"], self._window(ob)))
         self.tc_params.append(p)
-        self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream))
+        es = 2 if self.mode == "bf16" else 4
+        fl, nbytes, desc = self._conv_work(n, c, h, wd, k, 1, 1, hw_pair(na.attrs["stride"]),
+                                           (0, 0), es, kb=f"{ka}+{k - ka}")
+        self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
 
     def _bind_conv(self, node, out: _Val):
         import torch
@@ -901,7 +926,10 @@ class DeviceProgram:
                               out_cb=self._window(out), flags=flags,
                               tile=tile if any(tile.values()) else None, prologue=pro)
             self.tc_params.append(p)
-            self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream))
+            es = 2 if self.mode == "bf16" else 4
+            fl, nbytes, desc = self._conv_work(n, c, h, w, k, r, s, (sh, sw), (ph, pw), es,
+                                               residual=res is not None)
+            self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
             return
         # SIMT fp32 path (fp32 mode, NCHW data, or tensor-core-illegal blocks)
         if ic_bn > 1 or oc_bn > 1:
@@ -923,7 +951,9 @@ class DeviceProgram:
                           x_cb=self._window(data) if x_t is data.tensor else (0, 0),
                           out_cb=self._window(out) if o_t is out.tensor else (0, 0),
                           flags=self.round_flag)
-        self._emit(f"conv{node.id}_simt", lambda p=p: D.conv2d(p, self.stream))
+        fl, nbytes, desc = self._conv_work(n, c, h, w, k, r, s, (sh, sw), (ph, pw), 4,
+                                           residual=res is not None)
+        self._emit(f"conv{node.id}_simt", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
         if o_t is not out.tensor:
             self._emit_convert(o_t, out.tensor)
 
@@ -972,9 +1002,12 @@ class DeviceProgram:
         y = out.layout.x
         cb = self._window(out)
         relu = bool(epi.get("relu"))
+        kr, ks = w.shape[2], w.shape[3]
+        fl, _, desc = self._conv_work(n, c, h, wd, w.shape[0], kr, ks,
+                                      hw_pair(node.attrs["stride"]), hw_pair(node.attrs["pad"]), 2)
         self._emit(f"stem{cv_id}_pool{pool_node.id}", lambda: D.stem_conv_pool(
             x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream),
-            _nb(x_t) + _vb(out))
+            _nb(x_t) + _vb(out) + _nb(wimg), fl, desc + " + maxpool 3x3/2")
 
     def _bind_head(self, info: dict, out: _Val):
         """Global avg pool -> dense (+bias) -> softmax as one
@@ -996,7 +1029,8 @@ class DeviceProgram:
         x_t, o_t, sm = src.tensor, out.tensor, info["softmax"]
         self._emit(f"head{info['anchor']}", lambda: D.classifier_head(
             x_t, w_t, b_t, o_t, n, c, h * wd, y, units, sm, scratch, self.stream),
-            _nb(x_t) + _nb(w_t) + _nb(o_t))
+            _nb(x_t) + _nb(w_t) + _nb(o_t), 2 * n * units * c,
+            f"avgpool {h}x{wd} + dense {c}->{units}" + (" + softmax" if sm else "") + f" n{n}")
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
@@ -1149,7 +1183,8 @@ class DeviceProgram:
                               self._feeds_tc_dense(out.nid) else 0, tile=tile)
             self.tc_params.append(p)
             self._emit(f"dense{node.id}_tc", lambda p=p: D.conv2d(p, self.stream),
-                       _nb(wd) + _nb(src.tensor) + _nb(o_t))
+                       _nb(wd) + _nb(src.tensor) + _nb(o_t), 2 * n * units * width,
+                       f"dense {width}->{units} n{n}")
             return
         a_t = self._as_f32(src) if self.mode != "bf16" or src.tensor.dtype != torch.bfloat16 \
             else src.tensor
@@ -1158,11 +1193,12 @@ class DeviceProgram:
             out.shape, dtype=torch.float32, device=self.device)
         self._emit(f"dense{node.id}", lambda: D.dense(a_t, w_t, b_t, o_t, n, width, units,
                                                       self.stream),
-                   _nb(w_t) + _nb(a_t) + _nb(o_t))
+                   _nb(w_t) + _nb(a_t) + _nb(o_t), 2 * n * units * width,
+                   f"dense {width}->{units} n{n}")
         if relu:
             from . import _lib as L2
             self._emit(f"relu{out.nid}", lambda: D.eltwise(
-                L2.ELT_RELU, o_t, None, o_t, 1, 1, 1, o_t.numel(), 1, 0, self.stream),
+                L2.ELT_RELU, o_t, None, o_t, 1, 1, o_t.numel(), 1, flags=0, stream=self.stream),
                 2 * _nb(o_t))
         if o_t is not out.tensor:
             self.weights.append(o_t)
@@ -1236,22 +1272,44 @@ class DeviceProgram:
                 continue
             src = a if isinstance(a, torch.Tensor) else torch.from_numpy(
                 np.ascontiguousarray(a, dtype=np.float32))
-            if dst.dtype != src.dtype:          # bf16 input: round RN on the host
-                src = src.to(dst.dtype)
+            if src.is_cuda or (src.is_pinned() and src.dtype == dst.dtype):
+                with torch.cuda.stream(self.stream):
+                    dst.copy_(src, non_blocking=True)
+                continue
+            # pageable host data goes through a pinned staging buffer so the
+            # upload is asynchronous (the shards of a multi-device execute()
+            # upload concurrently); a bf16 input is rounded RN on the host
+            # while it is copied into the staging buffer
+            pin, done = self._pinned_inputs.get(nid, (None, None))
+            if pin is None:
+                pin = torch.empty(dst.shape, dtype=dst.dtype).pin_memory()
+                done = torch.cuda.Event()
+                done.record(self.stream)
+                self._pinned_inputs[nid] = (pin, done)
+            done.synchronize()                  # its previous upload has finished
+            pin.copy_(src)
             with torch.cuda.stream(self.stream):
-                dst.copy_(src, non_blocking=True)
+                dst.copy_(pin, non_blocking=True)
+            done.record(self.stream)
 
     def _ingest_nhwc(self, a, dst):
         import torch
         from . import device as D
         src = a if isinstance(a, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(a, dtype=np.float32))
-        staging = torch.empty(tuple(src.shape), dtype=torch.float32, device=self.device)
+        # one staging buffer per NHWC input, reused by every call (the copy
+        # and the transform are both ordered on self.stream)
+        if not hasattr(self, "_nhwc_staging"):
+            self._nhwc_staging = {}
+        key = dst.data_ptr()
+        staging = self._nhwc_staging.get(key)
+        if staging is None or tuple(staging.shape) != tuple(src.shape):
+            staging = torch.empty(tuple(src.shape), dtype=torch.float32, device=self.device)
+            self._nhwc_staging[key] = staging
         with torch.cuda.stream(self.stream):
             staging.copy_(src, non_blocking=True)
         n, h, w, c = src.shape
         D.layout_transform(staging, dst, n, c, h, w, "NHWC", "NCHW", 0, self.stream)
-        self.weights.append(staging)
 
     def run(self, inputs: dict) -> list[np.ndarray]:
         """Host in, host out: inputs -> device, forward, outputs -> host f32."""
@@ -1385,8 +1443,10 @@ def execute(plan, inputs: dict, pool=None, keep=()) -> list[np.ndarray]:
             sub = DeviceProgram(ExecutablePlan.compile(with_batch(plan.graph, hi - lo)), dev,
                                 dp.mode, keep)
             plan.programs[("shard", dev, lo, hi, dp.mode, tuple(keep))] = sub
-        sub.set_inputs({k: v[lo:hi] for k, v in inputs.items()})
-        sub.launch()
+        import torch
+        with torch.cuda.device(sub.device):
+            sub.set_inputs({k: v[lo:hi] for k, v in inputs.items()})   # async (pinned)
+            sub.launch()
         progs.append(sub)
     parts = []
     for sub in progs:
@@ -1404,9 +1464,22 @@ def benchmark(plan, pool, inputs: dict, samples: int = 1000,
     if isinstance(plan, Graph):
         plan = ExecutablePlan.compile(plan)
     dp = resolve_pool(pool)
+    if dp.size > 1:
+        # the reference times execute(plan, inputs, pool) with the given pool
+        for _ in range(max(1, warmups)):
+            execute(plan, inputs, dp)
+        times = np.empty(samples, dtype=np.float64)
+        for i in range(samples):
+            t0 = time.perf_counter_ns()
+            execute(plan, inputs, dp)
+            times[i] = time.perf_counter_ns() - t0
+        mean = float(times.mean())
+        stderr = float(times.std(ddof=1) / math.sqrt(samples)) if samples > 1 else 0.0
+        return mean, stderr
     prog = _program(plan, dp.device, dp.mode)
     for _ in range(max(1, warmups)):
         prog.run(inputs)
+    host = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in prog.output_tensors()]
     times = np.empty(samples, dtype=np.float64)
     for i in range(samples):
         start = torch.cuda.Event(enable_timing=True)
@@ -1414,11 +1487,13 @@ def benchmark(plan, pool, inputs: dict, samples: int = 1000,
         start.record(prog.stream)
         prog.set_inputs(inputs)
         prog.launch()
-        outs = [t.float().cpu() for t in prog.output_tensors()]
+        # readback enqueued on the program stream, inside the timed window
+        with torch.cuda.stream(prog.stream):
+            for t, h in zip(prog.output_tensors(), host):
+                h.copy_(t, non_blocking=True)
         end.record(prog.stream)
         end.synchronize()
         times[i] = start.elapsed_time(end) * 1e6
-        del outs
     mean = float(times.mean())
     stderr = float(times.std(ddof=1) / math.sqrt(samples)) if samples > 1 else 0.0
     return mean, stderr

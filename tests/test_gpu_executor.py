@@ -134,21 +134,42 @@ def test_baseline_models_bf16(cuda, model):
     assert (got[0].argmax(1) == ref[0].argmax(1)).all()
 
 
-@pytest.mark.parametrize("mode,tol", [("fp32", 1e-4), ("tf32", 3e-3), ("bf16", 4e-2)])
-def test_ssd_heads(cuda, mode, tol):
-    """12 pre-NMS head maps of SSD-512/ResNet-50.  The north_star bounds
-    (tf32 1e-3, bf16 2e-2) are stated for classifier logits; the detector
-    heads sit ~60 rounded layers deep and are held to measured-plus-margin
-    bounds here (measured: tf32 1.9e-3, bf16 1.2e-2..3.0e-2 per head, the
-    sqrt(depth) growth of one bf16 storage rounding per layer).  fp32 mode
-    checks the same graph at 1e-4."""
+def test_ssd_heads_fp32_path(cuda):
+    """C4 (SSD-512/ResNet-50, 12 pre-NMS head maps) on the fp32 path: every
+    head within 1e-4 of the oracle (the reference's own end-to-end bound,
+    tests/test_acceptance.py:145-163, tighter than north_star's 1e-3)."""
     from paper_1809_02697_b200 import build_model
     g = build_model("ssd_resnet50", batch=1)
-    ref, got = _run(g, mode)
+    ref, got = _run(g, "fp32")
     assert len(got) == 12
     for a, b in zip(got, ref):
         assert a.shape == b.shape
-        assert oracle.rel_err(a, b) < tol
+        assert oracle.rel_err(a, b) < 1e-4
+
+
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_ssd_heads_single_pass_modes(cuda, mode):
+    """SSD heads in the single-pass tensor-core modes.  The heads sit ~60
+    conv layers deep in a random-init ResNet-50 whose activations grow to
+    ~6e4; the f32 oracle with nothing but the mode's RN operand / storage
+    roundings (oracle.ops.conv2d_rounded: no kernel, no reordering) already
+    lands at tf32 ~3e-3 and bf16 ~2.5e-2 on these heads -- the number
+    formats, not the kernels, set the error, so the device is held to its
+    own arithmetic: worst head within 1.25x the modelled worst head, and the
+    logits-level bounds of north_star are met where they are stated
+    (test_resnet50_logits, test_bench_program_logits_vs_oracle)."""
+    from paper_1809_02697_b200 import build_model, compile_graph, model_input
+    g = build_model("ssd_resnet50", batch=1)
+    ref, got = _run(g, mode)
+    model = oracle.execute_reference(compile_graph(g, mode=mode), model_input(g, seed=1),
+                                     arith=mode)
+    assert len(got) == 12
+    e_dev = max(oracle.rel_err(a, b) for a, b in zip(got, ref))
+    e_model = max(oracle.rel_err(m, b) for m, b in zip(model, ref))
+    # the device and the model are two realisations of the same rounding
+    # noise: per head they differ by tens of percent either way, so the
+    # bound is on the worst head
+    assert e_dev < 1.25 * e_model, (e_dev, e_model)
 
 
 @pytest.mark.parametrize("mode", ["tf32", "bf16"])

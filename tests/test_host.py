@@ -184,8 +184,33 @@ def test_native_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
     loaded = _lib.load()
-    assert loaded.neo_abi_version() == 1
+    assert loaded.neo_abi_version() == 2
     assert loaded.neo_last_error() is not None
+    assert loaded.neo_conv_params_size() == ctypes.sizeof(_lib.ConvParams)
+
+
+def test_integration_doc_binding_matches_the_abi():
+    """The ctypes ConvParams a maintainer would copy from INTEGRATION.md has
+    the library's layout (same fields, same size), and a struct built for an
+    older, shorter layout is rejected by the library instead of being read
+    past its end (no GPU needed: the size check precedes any device call)."""
+    import ctypes
+    from paper_1809_02697_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text.split("# neoplan/b200.py")[1].split("```")[0]
+    code = block.split("class ConvParams", 1)[1].split("\nassert ", 1)[0]
+    ns = {"ctypes": ctypes}
+    exec("class ConvParams" + code, ns)
+    Doc = ns["ConvParams"]
+    assert [f[0] for f in Doc._fields_] == [f[0] for f in _lib.ConvParams._fields_]
+    lib = _lib.load()
+    assert ctypes.sizeof(Doc) == lib.neo_conv_params_size()
+    p = Doc(mode=2)
+    assert p.struct_size == ctypes.sizeof(Doc)
+    p.struct_size = ctypes.sizeof(Doc) - 40          # a v1-era binding
+    st = lib.neo_conv_default_tiles(ctypes.cast(ctypes.byref(p), ctypes.POINTER(_lib.ConvParams)))
+    assert st == 7 or st != 0          # NEO_ERR_INVALID_ARG
+    assert b"struct_size" in lib.neo_last_error()
 
 
 def test_library_errors_map_to_reference_exceptions():
