@@ -119,6 +119,12 @@ struct ConvTCParams {
                     // 8: per-CTA MMA-loop clocks -> neo_dbg_clk)
   float* ws;        // partials
   int* counters;    // per-tile arrival counters (zero between launches)
+  // last-tile sharing (TMA epilogue, single-CTA tiles, unsplit): the CTA's
+  // final tile is drained by two epilogue groups, each taking half of its
+  // output channel blocks -- nothing else is left for the idle group to do,
+  // and the last epilogue is the launch's tail
+  int share_last;
+  int dbg_slot;     // NEOB200_DBG & 256: per-launch timeline slot (g_tl)
 };
 
 __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n0, int& oh0,
@@ -445,6 +451,15 @@ __device__ __forceinline__ void trace(int ev, int t, unsigned* cnt) {
 
 // NEOB200_DBG & 8: per-CTA (MMA-loop cycles, ns) for clock checks
 __device__ unsigned long long g_dbg_clk[8 * 1024];
+// NEOB200_DBG & 256: per-launch, per-CTA globaltimer stamps (in-graph
+// timelines: entry, past griddepcontrol.wait, first MMA, last commit, exit)
+constexpr int kTlSlots = 64, kTlCtas = 160, kTlEv = 5;
+__device__ unsigned long long g_tl[kTlSlots * kTlCtas * kTlEv];
+__device__ __forceinline__ void tl_stamp(const ConvTCParams& p, int ev) {
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  if (blockIdx.x < kTlCtas) g_tl[((p.dbg_slot % kTlSlots) * kTlCtas + blockIdx.x) * kTlEv + ev] = ns;
+}
 
 // MMA issue: descriptors are formed by adding small offsets (in 16-byte
 // units) to per-stage bases, with the K steps of a slice unrolled at compile
@@ -615,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   long long dbg_t_entry = 0;
   if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_entry));
+  if ((p.dbg & 256) && threadIdx.x == 0) tl_stamp(p, 0);
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   const uint32_t sA = sraw + pad;
@@ -693,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (warp != 0 && warp != 1) neo_pdl_wait();
   long long dbg_t_pdl = 0;
   if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_pdl));
+  if ((p.dbg & 256) && threadIdx.x == 64) tl_stamp(p, 1);     // an epilogue warp, past the wait
 
   if (warp == 0) {
     if (lane == 0) {
@@ -753,6 +770,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             mbar_wait(empty_bar(stage), phase ^ 1u);
             TRACE(2, t);
             const uint32_t fb = fbar_base + 8u * stage;
+            if (!PAIR && (p.dbg & 4)) {      // timing experiment: no operand loads
+              mbar_arrive(full_bar(stage));
+              if (++stage == p.stages) {
+                stage = 0;
+                phase ^= 1u;
+              }
+              continue;
+            }
             if (leader_cta) mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
             const uint32_t a_dst = sA + stage * p.a_stage;
             const uint32_t b_dst = sB + stage * p.b_stage;
@@ -787,6 +812,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           mbar_wait(empty_bar(stage), phase ^ 1u);
           TRACE(2, t);
           const uint32_t fb = fbar_base + 8u * stage;
+          if (!PAIR && (p.dbg & 4)) {        // timing experiment: no operand loads
+            mbar_arrive(full_bar(stage));
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            continue;
+          }
           if (leader_cta) mbar_arrive_expect_tx(full_bar(stage), p.tx_bytes);
           const uint32_t a_dst = sA + stage * p.a_stage;
           for (int g = 0; g < p.G; ++g, ++sl) {
@@ -830,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         dbg_c0 = clock64();
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
       }
+      if (p.dbg & 256) tl_stamp(p, 2);
       const int mode = p.halo ? (p.wst ? kMmaHaloWst : kMmaHalo)
                        : p.rowb == 16 ? kMmaNarrow
                        : p.rowb >= 128 ? kMmaK4
@@ -842,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         case kMmaHalo: mma_tiles<TF32, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
         default: mma_tiles<TF32, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
       }
+      if (p.dbg & 256) tl_stamp(p, 3);
       if (p.dbg & 8) {
         long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -951,14 +986,28 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     // pair: accumulator releases go to the leader CTA's tempty barriers
     const uint32_t tempty_base = PAIR ? mapa_shared(tempty_bar(0), 0) : tempty_bar(0);
     const uint32_t ng_log2 = (uint32_t)(__ffs(p.ngroups) - 1);
+    // last-tile sharing: the owner group of the CTA's last unit drains the
+    // first half of its channel blocks, the next group the second half
+    const int last_it = (p.share_last && (int)blockIdx.x < p.num_units)
+                            ? (p.num_units - 1 - (int)blockIdx.x) / (int)gridDim.x : -1;
+    const int owner_grp = last_it >= 0 ? (last_it & (p.ngroups - 1)) : -1;
+    const int helper_grp = last_it >= 0 ? ((owner_grp + 1) & (p.ngroups - 1)) : -1;
     for (int it = grp;; it += p.ngroups) {
-      const int u = cta_unit(p, it, rank);
-      if (u < 0) break;
+      int u = cta_unit(p, it, rank);
+      int acc = grp;
+      uint32_t acc_phase = ((uint32_t)it >> ng_log2) & 1u;   // ngroups is 2 or 4
+      bool helping = false;
+      if (u < 0) {
+        if (grp != helper_grp || last_it < 0) break;
+        helping = true;                   // join the owner group's last tile
+        u = cta_unit(p, last_it, rank);
+        acc = owner_grp;
+        acc_phase = ((uint32_t)last_it >> ng_log2) & 1u;
+      }
+      const bool owning_last = !helping && it == last_it;
       const int t = p.splits == 1 ? u : (int)((uint32_t)u / (uint32_t)p.splits);
       int n0, oh0, ow0, k0;
       decode_tile(p, t, n0, oh0, ow0, k0);
-      const int acc = grp;
-      const uint32_t acc_phase = ((uint32_t)it >> ng_log2) & 1u;   // ngroups is 2 or 4
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.BN;
       const int ncols = min(p.BN, p.K - k0);
       if (p.splits > 1) {
@@ -1015,6 +1064,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const bool has_res = p.res != nullptr;
         const int nblk = ncols / p.y;
         const bool pf = p.res_pf != 0;
+        int blk_lo = 0, blk_hi = nblk;
+        if (helping || owning_last) {
+          const int hb = (nblk + 1) >> 1;
+          if (nblk < 2) {
+            if (helping) break;           // nothing to share
+          } else if (helping) {
+            blk_lo = hb;
+          } else {
+            blk_hi = hb;
+          }
+        }
         const int lt = (int)((uint32_t)it >> ng_log2);   // this group's tile counter
         const int set = pf ? (lt & 1) : 0;        // prefetch: alternate slot sets
         const uint32_t sgrp = sO + (grp * p.nslot + set * (p.nslot / 2)) * p.stage_out;
@@ -1034,7 +1094,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         };
         if (leader) TRACE(20 + grp, t);
         if (eprof) e_x = clock64();
-        if (!pf) issue_res(0, min(nblk, p.nslot));
+        if (!pf || helping) issue_res(blk_lo, min(blk_hi - blk_lo, pf ? p.nslot / 2 : p.nslot));
         else if (lt == 0 && leader) load_res(sgrp, rbar, 0, nblk, ow0, oh0, k0, n0);
         if (k0 != par_k0) {
           // stage this tile's channel vectors (identity where absent); a
@@ -1063,9 +1123,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           continue;
         }
         const int slots = pf ? p.nslot / 2 : p.nslot;
-        for (int b0 = 0; b0 < nblk; b0 += slots) {
-          const int cnt = min(slots, nblk - b0);
-          if (b0 > 0) {
+        for (int b0 = blk_lo; b0 < blk_hi; b0 += slots) {
+          const int cnt = min(slots, blk_hi - b0);
+          if (b0 > blk_lo) {
             issue_res(b0, cnt);
             named_bar_sync(bar_id, gthreads);
           }
@@ -1109,7 +1169,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
 #undef NEO_EPI
           }
-          if (b0 + cnt >= nblk) {           // accumulator fully read: release TMEM
+          if (b0 + cnt >= blk_hi && !helping) {   // accumulator read: release TMEM
+            // (a shared last tile is released by its owner alone: the MMA
+            // thread never waits on that accumulator again)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -1129,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             for (int i = 0; i < cnt; ++i)
               tma_store_5d(tmo, sgrp + i * p.stage_out, 0, ow0, oh0, cb0 + b0 + i, n0);
             bulk_commit();
-            if (pf) {
+            if (pf && !helping) {
               // the group's next tile: its residual goes into the other set
               // once the store issued from that set one tile ago has read it
               const int un = cta_unit(p, it + p.ngroups, rank);
@@ -1146,8 +1208,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
           etick(e_st);
         }
+        if (helping) break;
         continue;
       } else {
+        if (helping) break;                // (sharing needs the TMA epilogue)
         mbar_wait(tfull_bar(acc), acc_phase);
         tc_fence_after();
         const int wl = m % p.BW, hl = (m / p.BW) % p.BH, nl = m / (p.BW * p.BH);
@@ -1188,6 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
   __syncthreads();
   if (threadIdx.x == 0) TRACE(62, 0);
+  if ((p.dbg & 256) && threadIdx.x == 0) tl_stamp(p, 4);
   if ((p.dbg & 64) && threadIdx.x == 0) {
     // per-CTA timeline: entry, past griddepcontrol.wait, all roles done
     long long t;
@@ -1795,6 +1860,8 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   {
     static const char* dbg = getenv("NEOB200_DBG");
     kp.dbg = dbg ? atoi(dbg) : 0;
+    static int slot = 0;
+    if (kp.dbg & 256) kp.dbg_slot = slot++;
   }
   kp.b_region = wst ? (halo ? (uint32_t)(p->r * Cb) * kp.b_sub : (uint32_t)kstages * kp.b_stage)
                     : (uint32_t)p->stages * kp.b_stage;
@@ -1850,6 +1917,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.nslot = (int)std::min<int64_t>(slots, (kp.res_pf ? 2 : 1) * per_tile);
   }
   kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
+  {
+    static const bool no_share = getenv("NEOB200_NO_SHARE_LAST") != nullptr;
+    kp.share_last = (!no_share && kp.tma_epi && kp.splits == 1 && !pair && !p->pro_scale &&
+                     kp.ngroups >= 2) ? 1 : 0;
+  }
   NEO_CHECK_ARG(kp.tma_epi || !kp.k_split, NEO_ERR_UNSUPPORTED,
                 "two-output convs need the TMA-store epilogue (oc_bn rows of 32/64/128 bytes)");
   if (kp.tma_epi) {
@@ -1957,6 +2029,11 @@ extern "C" int neo_trace_dump(unsigned long long* host, int max_n) {
   return n;
 }
 #endif
+
+// debug: NEOB200_DBG&256 timelines, [slot][cta][event] globaltimer ns
+extern "C" __attribute__((visibility("default"))) int neo_dbg_timeline(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_tl, n * sizeof(unsigned long long));
+}
 
 // debug: per-CTA (MMA-loop cycles, ns) of the last NEOB200_DBG&8 launch
 extern "C" __attribute__((visibility("default"))) int neo_dbg_clk(unsigned long long* host, int n) {

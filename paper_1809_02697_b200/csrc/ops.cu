@@ -144,6 +144,20 @@ struct Pair<__nv_bfloat16> {
   }
 };
 
+// a / d correctly rounded (== __fdiv_rn(a, d)) for a constant d that is not
+// a power of two, with r = RN(1/d): q = RN(a r), the remainder a - d q is
+// exact through one FMA, and q + rem r rounded once is RN(a / d)
+// (Markstein's correction step; a / d is never a rounding midpoint because d
+// is odd-scaled).  Three instructions instead of the ~20-instruction IEEE
+// division with its special-case path; zero keeps its sign, and inf / NaN
+// pass through from q (pinned on the CPU: tests/test_host.py).
+__device__ __forceinline__ float div_rn_const(float a, float d, float r) {
+  const float q = a * r;
+  const float rem = fmaf(-q, d, a);
+  const float q1 = fmaf(rem, r, q);
+  return isfinite(q) ? copysignf(q1, a) : q;
+}
+
 // _pool2d (executor.py:103-128).  Avg: padding taps add zero (skipped) and
 // the sum runs r-major then divides by win*win, lane pairs in packed f32x2
 // adds; max: padding is -inf (skipped), bf16 max is exact in bf16x2.
@@ -167,7 +181,56 @@ __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, in
       const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
       const T* base = src + gq * V;
       uint4 res;
-      if constexpr (IS_MAX && sizeof(T) == 2 && WIN > 0) {
+      if constexpr (!IS_MAX && WIN > 0) {
+        // average pooling, branch-free: all WIN*WIN taps are loaded at once
+        // (clamped addresses, so every load is in bounds) and out-of-bounds
+        // taps contribute the reference's zero padding (+0.0); the sum keeps
+        // the reference order -- first tap, then + each tap r-major
+        // (executor.py:116-126) -- and divides by win*win (count_include_pad)
+        int rows[WIN], cols[WIN];
+        bool rin[WIN], cin[WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r) {
+          rin[r] = ih0 + r >= 0 && ih0 + r < H;
+          rows[r] = min(max(ih0 + r, 0), H - 1) * W;
+        }
+#pragma unroll
+        for (int q = 0; q < WIN; ++q) {
+          cin[q] = iw0 + q >= 0 && iw0 + q < W;
+          cols[q] = min(max(iw0 + q, 0), W - 1);
+        }
+        uint4 raw[WIN * WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r)
+#pragma unroll
+          for (int q = 0; q < WIN; ++q)
+            raw[r * WIN + q] = __ldg(reinterpret_cast<const uint4*>(base + (rows[r] + cols[q]) * x));
+        float2 acc[NP];
+#pragma unroll
+        for (int t2 = 0; t2 < WIN * WIN; ++t2) {
+          const bool in_b = rin[t2 / WIN] && cin[t2 % WIN];
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const float2 v = in_b ? Pair<T>::get(raw[t2], k) : make_float2(0.f, 0.f);
+            acc[k] = t2 == 0 ? v : __fadd2_rn(acc[k], v);
+          }
+        }
+        float o[V];
+        constexpr int kWin2 = WIN * WIN;
+        constexpr bool kPow2 = (kWin2 & (kWin2 - 1)) == 0;
+        const float rcp = 1.0f / (float)kWin2;     // RN(1/win^2), a compile-time constant
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          // power-of-two windows: the division is an exact scaling
+          o[2 * k] = kPow2 ? acc[k].x * rcp : div_rn_const(acc[k].x, (float)kWin2, rcp);
+          o[2 * k + 1] = kPow2 ? acc[k].y * rcp : div_rn_const(acc[k].y, (float)kWin2, rcp);
+        }
+        if (round) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) o[j] = neo_round_tf32(o[j]);
+        }
+        res = pack_vec<T, V>(o);
+      } else if constexpr (IS_MAX && sizeof(T) == 2 && WIN > 0) {
         // max pooling: an out-of-bounds tap is clamped to the nearest row /
         // column, which always lies inside the same window (pad < win), so
         // the maximum is unchanged and all WIN*WIN loads are issued
@@ -193,6 +256,31 @@ __global__ void pool_plane_vec(const T* __restrict__ in, T* __restrict__ out, in
             m[k] = __hmax2(m[k], reinterpret_cast<const __nv_bfloat162*>(&raw[t2])[k]);
 #pragma unroll
         for (int k = 0; k < NP; ++k) reinterpret_cast<__nv_bfloat162*>(&res)[k] = m[k];
+      } else if constexpr (IS_MAX && WIN > 0) {
+        // f32 max: the same clamped-tap trick (max is order-independent)
+        int rows[WIN], cols[WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r) rows[r] = min(max(ih0 + r, 0), H - 1) * W;
+#pragma unroll
+        for (int q = 0; q < WIN; ++q) cols[q] = min(max(iw0 + q, 0), W - 1);
+        uint4 raw[WIN * WIN];
+#pragma unroll
+        for (int r = 0; r < WIN; ++r)
+#pragma unroll
+          for (int q = 0; q < WIN; ++q)
+            raw[r * WIN + q] = __ldg(reinterpret_cast<const uint4*>(base + (rows[r] + cols[q]) * x));
+        float o[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = reinterpret_cast<const float*>(&raw[0])[j];
+#pragma unroll
+        for (int t2 = 1; t2 < WIN * WIN; ++t2)
+#pragma unroll
+          for (int j = 0; j < V; ++j) o[j] = fmaxf(o[j], reinterpret_cast<const float*>(&raw[t2])[j]);
+        if (round) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) o[j] = neo_round_tf32(o[j]);
+        }
+        res = pack_vec<T, V>(o);
       } else if constexpr (IS_MAX && sizeof(T) == 2) {
         __nv_bfloat162 m[NP];
 #pragma unroll
@@ -306,6 +394,84 @@ __global__ void pool_global(const T* __restrict__ in, T* __restrict__ out, int64
   }
 }
 
+// 3x3 stride-1 average pooling (Inception's branch pools, pad 1,
+// count_include_pad) with a sliding window along W: a thread produces OUTW
+// consecutive output pixels of one 8-lane group, loading each input row's
+// OUTW + 2 taps once (3x fewer loads and bf16->f32 conversions than one
+// output per thread), while every output still sums its nine taps in the
+// reference order -- first tap, then + each tap r-major (executor.py:116-126)
+// -- with the padding taps contributing +0.0, then one division by 9.
+template <int OUTW>
+__global__ void avgpool3s1_bf16(const __nv_bfloat16* __restrict__ in,
+                                __nv_bfloat16* __restrict__ out, int64_t Cb, uint32_t P, int H,
+                                int W, int x, uint32_t chunks_w, bool round, Win wnd) {
+  neo_pdl_enter();
+  constexpr int NP = 4;                           // float2 pairs per 16-byte vector
+  const uint32_t groups = (uint32_t)x / 8u;
+  const uint32_t per_plane = (uint32_t)H * chunks_w * groups;
+  const uint32_t total = P * per_plane;
+  const float rcp = 1.0f / 9.0f;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += gridDim.x * blockDim.x) {
+    const uint32_t plane = idx / per_plane;
+    uint32_t rem = idx - plane * per_plane;
+    const uint32_t gq = rem % groups;
+    rem /= groups;
+    const int oh = (int)(rem / chunks_w);
+    const int ow0 = (int)(rem - (uint32_t)oh * chunks_w) * OUTW;
+    const uint32_t pn = plane / (uint32_t)Cb, pc = plane - pn * (uint32_t)Cb;
+    const __nv_bfloat16* src =
+        in + ((int64_t)pn * wnd.in_total + wnd.in_off + pc) * (int64_t)H * W * x + gq * 8;
+    __nv_bfloat16* dst =
+        out + ((int64_t)pn * wnd.out_total + wnd.out_off + pc) * (int64_t)H * W * x + gq * 8;
+    float2 acc[OUTW][NP];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int ih = oh - 1 + r;
+      const bool rin = ih >= 0 && ih < H;
+      const int ihc = min(max(ih, 0), H - 1);
+      uint4 raw[OUTW + 2];
+#pragma unroll
+      for (int c = 0; c < OUTW + 2; ++c) {
+        const int iw = min(max(ow0 - 1 + c, 0), W - 1);
+        raw[c] = __ldg(reinterpret_cast<const uint4*>(src + ((int64_t)ihc * W + iw) * x));
+      }
+      float2 t[OUTW + 2][NP];
+#pragma unroll
+      for (int c = 0; c < OUTW + 2; ++c) {
+        const int iw = ow0 - 1 + c;
+        const bool in_b = rin && iw >= 0 && iw < W;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+          t[c][k] = in_b ? Pair<__nv_bfloat16>::get(raw[c], k) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < OUTW; ++j)
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+          for (int k = 0; k < NP; ++k)
+            acc[j][k] = (r == 0 && s == 0) ? t[j + s][k] : __fadd2_rn(acc[j][k], t[j + s][k]);
+    }
+#pragma unroll
+    for (int j = 0; j < OUTW; ++j) {
+      if (ow0 + j >= W) break;
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        o[2 * k] = div_rn_const(acc[j][k].x, 9.0f, rcp);
+        o[2 * k + 1] = div_rn_const(acc[j][k].y, 9.0f, rcp);
+      }
+      if (round) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = neo_round_tf32(o[e]);
+      }
+      *reinterpret_cast<uint4*>(dst + ((int64_t)oh * W + ow0 + j) * x) =
+          pack_vec<__nv_bfloat16, 8>(o);
+    }
+  }
+}
+
 template <typename T, int V, bool IS_MAX>
 void launch_pool_vec(const T* in, T* out, int64_t cb, int64_t P, int h, int w, int OH, int OW,
                      int x, int win, int stride, int pad, bool round, Win wnd, cudaStream_t st) {
@@ -321,25 +487,51 @@ void launch_pool_vec(const T* in, T* out, int64_t cb, int64_t P, int h, int w, i
                                                           stride, pad, round, wnd);
 }
 
-template <typename T, int V>
-__global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__ b,
-                                  T* __restrict__ out, const float* __restrict__ scale,
-                                  const float* __restrict__ shift, int64_t Cb, int64_t P,
-                                  int64_t plane_sz, int x, int op, bool round, Win wnd) {
+// Elementwise ops over (plane, vector) flattened into one index space: a
+// grid of a few CTAs per SM, each thread holding U independent 16-byte loads
+// in flight (DenseNet's BN-ReLU launches are small, so per-block scheduling
+// and a single outstanding load per thread, not HBM, bounded the old
+// one-vector-per-thread plane grid).
+template <typename T, int V, int U>
+__global__ void eltwise_flat_vec(const T* __restrict__ a, const T* __restrict__ b,
+                                 T* __restrict__ out, const float* __restrict__ scale,
+                                 const float* __restrict__ shift, int64_t Cb, uint32_t total,
+                                 uint32_t vecs, int64_t plane_sz, int x, int op, bool round,
+                                 Win wnd) {
   neo_pdl_enter();
-  const uint32_t vecs = (uint32_t)(plane_sz / V);
-  for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
-    const T* ap = a + wnd.in_plane(plane, Cb) * plane_sz;
-    const T* bp = b ? b + plane * plane_sz : nullptr;
-    T* op_ = out + wnd.out_plane(plane, Cb) * plane_sz;
-    const int ch_base = (int)(plane % Cb) * x;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < vecs;
-         i += gridDim.x * blockDim.x) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint4* av = reinterpret_cast<const uint4*>(a);
+  const uint4* bv = reinterpret_cast<const uint4*>(b);
+  uint4* ov = reinterpret_cast<uint4*>(out);
+  const int64_t pv = plane_sz / V;               // vectors per plane
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    uint4 ra[U], rb[U];
+    int64_t oo[U];
+    int ch[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = base + u * stride;
+      const bool ok = idx < total;
+      const uint32_t plane = ok ? idx / vecs : 0u;
+      const uint32_t i = ok ? idx - plane * vecs : 0u;
+      // 32-bit plane decode (image, channel block) -- the windows' int64
+      // divisions would dominate this memory-bound loop
+      const uint32_t pn = plane / (uint32_t)Cb, pc = plane - pn * (uint32_t)Cb;
+      oo[u] = ok ? ((int64_t)pn * wnd.out_total + wnd.out_off + pc) * pv + i : -1;
+      ch[u] = (int)pc * x + (int)((i * V) % (uint32_t)x);
+      ra[u] = ok ? __ldg(av + ((int64_t)pn * wnd.in_total + wnd.in_off + pc) * pv + i)
+                 : make_uint4(0, 0, 0, 0);
+      if (op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU)
+        rb[u] = ok ? __ldg(bv + (int64_t)plane * pv + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (oo[u] < 0) continue;
       float v[V];
-      unpack_vec(__ldg(reinterpret_cast<const uint4*>(ap) + i), v, (const T*)nullptr);
+      unpack_vec(ra[u], v, (const T*)nullptr);
       if (op == NEO_ELT_ADD || op == NEO_ELT_ADD_RELU) {
         float w[V];
-        unpack_vec(__ldg(reinterpret_cast<const uint4*>(bp) + i), w, (const T*)nullptr);
+        unpack_vec(rb[u], w, (const T*)nullptr);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           v[j] = __fadd_rn(v[j], w[j]);
@@ -349,12 +541,11 @@ __global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__
 #pragma unroll
         for (int j = 0; j < V; ++j) v[j] = fmaxf(v[j], 0.f);
       } else {
-        const int ch = ch_base + (int)((i * V) % (uint32_t)x);
         float sc[V], sh[V];
 #pragma unroll
         for (int j = 0; j < V; j += 4) {
-          const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + ch + j));
-          const float4 h4 = __ldg(reinterpret_cast<const float4*>(shift + ch + j));
+          const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + ch[u] + j));
+          const float4 h4 = __ldg(reinterpret_cast<const float4*>(shift + ch[u] + j));
           sc[j] = s4.x; sc[j + 1] = s4.y; sc[j + 2] = s4.z; sc[j + 3] = s4.w;
           sh[j] = h4.x; sh[j + 1] = h4.y; sh[j + 2] = h4.z; sh[j + 3] = h4.w;
         }
@@ -369,9 +560,16 @@ __global__ void eltwise_plane_vec(const T* __restrict__ a, const T* __restrict__
 #pragma unroll
         for (int j = 0; j < V; ++j) v[j] = neo_round_tf32(v[j]);
       }
-      reinterpret_cast<uint4*>(op_)[i] = pack_vec<T, V>(v);
+      ov[oo[u]] = pack_vec<T, V>(v);
     }
   }
+}
+
+// grid-stride launches: at most 8 CTAs of 256 threads per B200 SM (no device
+// query here -- these launches are recorded inside CUDA-graph capture)
+static unsigned flat_grid(uint64_t total_vecs, int U, int threads = 256) {
+  const uint64_t want = (total_vecs + (uint64_t)threads * U - 1) / ((uint64_t)threads * U);
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 8));
 }
 
 template <typename T>
@@ -522,7 +720,14 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
     if (is_max)
       launch_pool_vec<__nv_bfloat16, 8, true>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x,
                                               win, stride, pad, round, wnd, st);
-    else
+    else if (win == 3 && stride == 1 && pad == 1 &&
+             (uint64_t)P * h * neo_ceil_div(w, 4) * (x / 8) < (1ull << 32)) {
+      constexpr int kOutW = 4;
+      const uint32_t chunks = (uint32_t)neo_ceil_div(w, kOutW);
+      const uint64_t total = (uint64_t)P * h * chunks * (x / 8);
+      neo_launch(avgpool3s1_bf16<kOutW>, flat_grid(total, 1), 256, 0, st, i, o, cb, (uint32_t)P,
+                 (int)h, (int)w, x, chunks, round, wnd);
+    } else
       launch_pool_vec<__nv_bfloat16, 8, false>(i, o, cb, P, (int)h, (int)w, (int)OH, (int)OW, x,
                                                win, stride, pad, round, wnd, st);
   } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
@@ -577,14 +782,17 @@ extern "C" int neo_eltwise_window(int dtype, int op, const void* a, const void* 
   const int64_t P = n * cb, plane_sz = hw * x;
   const bool al = aligned16(a) && aligned16(out) && (!b || aligned16(b)) &&
                   (op < NEO_ELT_SCALE_SHIFT || (aligned16(scale) && aligned16(shift)));
-  if (dtype == NEO_BF16 && x % 8 == 0 && al) {
-    neo_launch(eltwise_plane_vec<__nv_bfloat16, 8>, plane_grid(P, plane_sz / 8), 256, 0, st, 
+  const bool flat_ok = (uint64_t)P * (uint64_t)plane_sz < (1ull << 32);
+  if (dtype == NEO_BF16 && x % 8 == 0 && al && flat_ok) {
+    const uint32_t vecs = (uint32_t)(plane_sz / 8), tot = (uint32_t)(P * vecs);
+    neo_launch(eltwise_flat_vec<__nv_bfloat16, 8, 4>, flat_grid(tot, 4), 256, 0, st,
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
-        static_cast<__nv_bfloat16*>(out), scale, shift, cb, P, plane_sz, x, op, round, wnd);
-  } else if (dtype == NEO_F32 && x % 4 == 0 && al) {
-    neo_launch(eltwise_plane_vec<float, 4>, plane_grid(P, plane_sz / 4), 256, 0, st, 
+        static_cast<__nv_bfloat16*>(out), scale, shift, cb, tot, vecs, plane_sz, x, op, round, wnd);
+  } else if (dtype == NEO_F32 && x % 4 == 0 && al && flat_ok) {
+    const uint32_t vecs = (uint32_t)(plane_sz / 4), tot = (uint32_t)(P * vecs);
+    neo_launch(eltwise_flat_vec<float, 4, 4>, flat_grid(tot, 4), 256, 0, st,
         static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out),
-        scale, shift, cb, P, plane_sz, x, op, round, wnd);
+        scale, shift, cb, tot, vecs, plane_sz, x, op, round, wnd);
   } else if (dtype == NEO_BF16)
     neo_launch(eltwise_kernel<__nv_bfloat16>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),

@@ -208,19 +208,31 @@ class CapturedGraph:
 
 
 def capture(fn, stream=None) -> CapturedGraph:
-    """Run ``fn`` under stream capture and return the instantiated graph."""
+    """Run ``fn`` under stream capture and return the instantiated graph.
+
+    The garbage collector is paused for the capture: a collection inside it
+    could free an unreachable program's pinned host buffers, and torch's
+    pinned-memory allocator then queries CUDA events -- an operation a
+    global-mode capture forbids, which would invalidate the graph."""
+    import gc
     s = stream or torch.cuda.current_stream()
-    L.call("neo_capture_begin", stream_handle(s))
+    gc_was = gc.isenabled()
+    gc.disable()
     try:
-        fn()
-    except BaseException:
+        L.call("neo_capture_begin", stream_handle(s))
+        try:
+            fn()
+        except BaseException:
+            h = ctypes.c_void_p()
+            L.load().neo_capture_end(stream_handle(s), ctypes.byref(h))
+            if h.value:
+                L.load().neo_graph_destroy(h)
+            raise
         h = ctypes.c_void_p()
-        L.load().neo_capture_end(stream_handle(s), ctypes.byref(h))
-        if h.value:
-            L.load().neo_graph_destroy(h)
-        raise
-    h = ctypes.c_void_p()
-    L.call("neo_capture_end", stream_handle(s), ctypes.byref(h))
+        L.call("neo_capture_end", stream_handle(s), ctypes.byref(h))
+    finally:
+        if gc_was:
+            gc.enable()
     return CapturedGraph(h.value)
 
 

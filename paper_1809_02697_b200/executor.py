@@ -146,7 +146,7 @@ class DeviceProgram:
         self.weights: list = []         # device tensors kept alive
         self._pinned_inputs: dict = {}  # input id -> (pinned staging, upload-done event)
         self.graph_exec = None
-        self.use_graph = use_graph
+        self.use_graph = use_graph and not os.environ.get("NEOB200_NO_GRAPH")
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
             self._lower()

@@ -225,3 +225,45 @@ def test_library_errors_map_to_reference_exceptions():
     st = lib.neo_layout_transform(0, 0, 16, 16, 0, 6, 2, 2, 0, 1, 2, 3, 0, None)
     with pytest.raises(SM):
         _lib.check(st)
+
+
+def _rn_f32(fr):
+    """Exact round-to-nearest-even of a Fraction to binary32 (as a float)."""
+    from fractions import Fraction
+    if fr == 0:
+        return 0.0
+    sign = -1.0 if fr < 0 else 1.0
+    v = abs(fr)
+    e = v.numerator.bit_length() - v.denominator.bit_length()
+    if Fraction(2) ** e > v:
+        e -= 1
+    e = max(e, -126)                       # subnormals share the minimum exponent
+    scale = Fraction(2) ** (e - 23)
+    m = v / scale
+    n = m.numerator // m.denominator
+    rem = m - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    return sign * float(n * scale)
+
+
+def test_pool_division_by_constant_is_correctly_rounded():
+    """ops.cu div_rn_const (avg pool /9): q = RN(a r), rem = fma(-q, d, a),
+    RN(q + rem r) with r = RN(1/d) equals IEEE a / d for random f32 sums and
+    for quotients crafted next to rounding midpoints, so the fast path stays
+    bit-identical to the reference's numpy division (executor.py:125)."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(7)
+    d = 9.0
+    r = float(np.float32(1.0) / np.float32(9.0))
+    a = list((rng.standard_normal(3000) * np.exp2(rng.integers(-60, 60, 3000))).astype(np.float32))
+    for _ in range(3000):                   # a / 9 within an ulp of a midpoint
+        mid = F(int(rng.integers(1 << 24, 1 << 25)) * 2 + 1, 1 << int(rng.integers(20, 30)))
+        base = np.float32(float(mid * 9))
+        a += [base, np.nextafter(base, np.float32(np.inf)), np.nextafter(base, np.float32(-np.inf))]
+    for x in a:
+        x = float(x)
+        q = _rn_f32(F(x) * F(r))
+        rem = _rn_f32(F(x) - F(d) * F(q))
+        q1 = _rn_f32(F(rem) * F(r) + F(q))
+        assert q1 == float(np.float32(x) / np.float32(d)), x

@@ -149,3 +149,66 @@ def test_prune_keeps_best_per_pair():
     best = prune_candidates(ms)
     assert [(m.schedule.ic_bn, m.schedule.reg_n, m.mean_ns) for m in best] == \
         [(4, 4, 3.0), (8, 4, 4.0)]
+
+
+class DividingCosts(StubCosts):
+    """StubCosts that, like the device table, refuses splits that do not
+    divide the tensor's channels."""
+
+    def cost(self, shape, from_x, to_x):
+        from paper_1809_02697_b200.errors import IndivisibleChannel
+        if shape[1] % from_x or shape[1] % to_x:
+            raise IndivisibleChannel(f"C={shape[1]} vs {from_x}->{to_x}")
+        return super().cost(shape, from_x, to_x)
+
+
+def _dense_block_graph(layers=4, growth=32, c0=64):
+    """A DenseNet-style block: x0 -> [conv -> concat]* with growth-channel
+    convs (oc 32 only) joined onto a running concat whose first input may
+    sit in 64-lane blocks."""
+    rng = np.random.default_rng(0)
+    g = Graph("dense")
+    x = g.add(OpKind.Input, shape=(1, 3, 16, 16), layout="NCHW", name="data")
+    w = g.constant(rng.standard_normal((c0, 3, 3, 3)).astype(np.float32))
+    cur = g.add(OpKind.Conv2d, inputs=[x, w], stride=1, pad=1)
+    c = c0
+    for _ in range(layers):
+        wg = g.constant(rng.standard_normal((growth, c, 1, 1)).astype(np.float32))
+        br = g.add(OpKind.Conv2d, inputs=[cur, wg], stride=1, pad=0)
+        cur = g.add(OpKind.Concat, inputs=[cur, br], axis=1)
+        c += growth
+    g.outputs = [cur]
+    return g
+
+
+def test_nested_concat_joins_degrade_per_join():
+    """DenseNet's nested concats: a 64-lane first input next to a 32-channel
+    branch cannot share a split.  Each such join costs the NCHW round trip
+    (reference passes.py:222-227) instead of infinity, so both the DP and
+    PBQP find a finite plan and PBQP is not Infeasible."""
+    g = _dense_block_graph()
+    cands = {}
+    for nid, wl in conv_workloads(g).items():
+        # the block's first conv only offers 64-lane outputs: every join
+        # mirrors it, and every 32-channel branch needs the fallback
+        ocs = [64] if wl.in_channel == 3 else [x for x in (64, 32) if wl.out_channel % x == 0]
+        ics = [x for x in (64, 32) if wl.in_channel % x == 0] or [1]
+        cands[nid] = [MeasuredScheme(ConvSchedule(ic, oc, 8, True), 1e4 + 100 * ic + oc, 0.0, 1)
+                      for ic in ics for oc in ocs]
+    prob = build_problem(g, cands, DividingCosts())
+    picks, cost = pbqp_solve(prob.instance)
+    assert np.isfinite(cost)
+    dp_picks, dp_cost = solve_dp(prob.instance)
+    assert np.isfinite(dp_cost) and dp_cost <= cost + 1e-6
+    assert dp_cost == pytest.approx(brute_force(prob.instance)[0])
+    # the same instance with the pre-fallback semantics (indivisible = inf)
+    # has no finite assignment at all
+    from paper_1809_02697_b200 import planning
+    orig = planning.join_fallback_ns
+    try:
+        planning.join_fallback_ns = lambda costs, shape, fx: np.inf
+        hard = build_problem(g, cands, DividingCosts())
+        with pytest.raises((Infeasible, StateExplosion)):
+            solve_dp(hard.instance)
+    finally:
+        planning.join_fallback_ns = orig

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--mode", default="bf16")
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--untuned", action="store_true")
+    ap.add_argument("--dump", default="", help="write launch names / bytes / flops as JSON")
     args = ap.parse_args()
     import torch
     from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, ScheduleDb, build_model,
@@ -37,6 +38,12 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     print(f"launches_per_step={prog.kernel_launches}")
+    if args.dump:
+        import json
+        with open(args.dump, "w") as fh:
+            json.dump([{"name": n, "bytes": b, "flops": f, "desc": d} for n, b, f, d in
+                       zip(prog.launch_names, prog.launch_bytes, prog.launch_flops,
+                           prog.launch_desc)], fh, indent=1)
     for i, n in enumerate(prog.launch_names):
         print(i, n)
 
