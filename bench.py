@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--untuned", action="store_true", help="ignore the tuned tile schedules")
     ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-mode measurement")
+    ap.add_argument("--upload", default="auto", choices=["auto", "bf16", "f32"],
+                    help="e2e image upload: bf16 rounded on the host (half the PCIe bytes) "
+                         "or f32 rounded by the stem on the device (no host compute); auto = "
+                         "bf16 on one GPU, f32 when several ranks share the host")
     return ap.parse_args()
 
 
@@ -346,7 +350,9 @@ def main():
     db = None if args.untuned else ScheduleDb(DEFAULT_DB)
     tuned = db is not None and tuned_assignment(g, db, args.mode) is not None
     planned = compile_graph(g, mode=args.mode, db=db)
-    prog = DeviceProgram(ExecutablePlan.compile(planned), local, args.mode)
+    upload = args.upload if args.upload != "auto" else ("bf16" if world == 1 else "f32")
+    prog = DeviceProgram(ExecutablePlan.compile(planned), local, args.mode,
+                         host_round=upload == "bf16")
     # three distinct seeded batches per rank (the e2e loop rotates them)
     feed_sets = [model_input(g, seed=1 + 3 * rank + j) for j in range(3)]
     feeds = feed_sets[0]
@@ -465,8 +471,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "images/s",
                     "h2d_bytes_per_step": int(prog.upload_bytes),
                     "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size()),
-                    "inputs": "3 distinct pinned f32 batches in rotation, rounded to bf16 on the "
-                              "host (the stem rounds RN anyway) and uploaded every step"},
+                    "inputs": "3 distinct pinned f32 batches in rotation, uploaded every step "
+                              + ("rounded to bf16 on the host (the stem rounds RN anyway)"
+                                 if upload == "bf16" else
+                                 "as f32 (the fused stem rounds RN on the device)"),
+                    "upload": upload},
             "gpu_launches": prog.kernel_launches * args.steps,
             "launches_per_step": prog.kernel_launches,
             "roofline": roof,

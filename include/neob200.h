@@ -231,6 +231,20 @@ int neo_conv_default_tiles(neo_conv_params* p);
  * (0 when it will not split). */
 int neo_conv_workspace_bytes(const neo_conv_params* p, int64_t* bytes);
 
+/* Two chained 1x1 convolutions (bf16, NCHW[64]c) as ONE launch -- the junction
+ * between two bottleneck blocks: y1 = relu1?(x * W1 + b1 + residual) (block
+ * i's expand conv with its fused shortcut) and y2 = relu2?(y1 * W2 + b2)
+ * (block i+1's reduce conv), y2 computed from y1 in shared memory.  Replaces
+ * two conv_blocked calls (kernels.py:250-303, Epilogue :74-87 in the order
+ * of :185-197); y1 and y2 are bit-identical to the two separate convs.
+ * w1 / w2: neo_pack_weights_umma images (x = 64) of the (N1, C1, 1, 1) and
+ * (N2, N1, 1, 1) weights.  Needs C1 % 64 == 0, N1 % 128 == 0, N2 in
+ * {64, 128, 192, 256}; residual may be NULL.  Unpadded, stride 1. */
+int neo_conv_junction(const void* x, const void* w1, const float* b1, const void* residual,
+                      void* y1, const void* w2, const float* b2, void* y2, int64_t n, int64_t c1,
+                      int64_t h, int64_t w, int64_t n1, int64_t n2, int relu1, int relu2,
+                      neo_stream_t stream);
+
 /* ---- memory-bound operators (executor.py:96-203) ------------------------ */
 /* Max (pad -inf) / avg (pad 0, / win^2) pooling over h, w of NCHW[x]c
  * (x = 1 is NCHW), replaces _pool2d executor.py:103-128. */

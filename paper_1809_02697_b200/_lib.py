@@ -103,6 +103,9 @@ SIGNATURES = {
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
     "neo_conv2d_nchwc_fused": (_c_int, [ctypes.POINTER(ConvParams), _c_vp]),
     "neo_conv_params_size": (_c_int, []),
+    "neo_conv_junction": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
+                                   _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
+                                   _c_vp]),
     "neo_conv_default_tiles": (_c_int, [ctypes.POINTER(ConvParams)]),
     "neo_conv_workspace_bytes": (_c_int, [ctypes.POINTER(ConvParams), ctypes.POINTER(_c_i64)]),
     "neo_pool2d": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,

@@ -1056,6 +1056,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         if (leader && atomicAdd(p.counters + t, 1) == 2 * p.splits - 1) p.counters[t] = 0;
         continue;
       }
+      if (p.tma_epi && (p.dbg & 1)) {
+        // timing experiment (NEOB200_DBG & 1): drain nothing -- wait for the
+        // accumulator and release it at once (no residual loads, no stores)
+        if (helping) break;
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(tempty_base + 8u * acc);
+          else mbar_arrive(tempty_bar(acc));
+        }
+        continue;
+      }
       if (p.tma_epi) {
         // staged epilogue: the tile's output channel blocks go through up to
         // p.nslot swizzled smem slots; residual blocks are fetched by TMA
@@ -1116,12 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         if (leader) TRACE(26 + grp, t);
         tc_fence_after();
         etick(e_tf);
-        if (p.dbg & 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty_bar(acc));
-          continue;
-        }
+
         const int slots = pf ? p.nslot / 2 : p.nslot;
         for (int b0 = blk_lo; b0 < blk_hi; b0 += slots) {
           const int cnt = min(slots, blk_hi - b0);

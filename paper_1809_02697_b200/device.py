@@ -127,6 +127,15 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
     return p
 
 
+def conv_junction(x, w1, b1, residual, y1, w2, b2, y2, n, c1, h, w, n1, n2, relu1=True,
+                  relu2=True, stream=None) -> None:
+    """y1 = relu1(x W1 + b1 + residual); y2 = relu2(y1 W2 + b2) in one launch
+    (bf16 NCHW[64]c; w1 / w2 are pack_weights_umma images with x = 64)."""
+    L.call("neo_conv_junction", _ptr(x), _ptr(w1), _ptr(b1), _ptr(residual), _ptr(y1), _ptr(w2),
+           _ptr(b2), _ptr(y2), n, c1, h, w, n1, n2, int(bool(relu1)), int(bool(relu2)),
+           stream_handle(stream))
+
+
 def conv_workspace_bytes(p: L.ConvParams) -> int:
     """Split-K workspace the launch of ``p`` needs (0 = no split)."""
     out = ctypes.c_int64(0)

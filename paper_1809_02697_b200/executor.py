@@ -123,7 +123,12 @@ class DeviceProgram:
     """One compiled forward of ``plan`` on ``device`` in ``mode``."""
 
     def __init__(self, plan: ExecutablePlan, device: int = 0, mode: str = "bf16",
-                 keep=(), use_graph: bool = True):
+                 keep=(), use_graph: bool = True, host_round: bool | None = None):
+        """``host_round``: an image read only by fused stems is uploaded as
+        bf16 rounded on the host (half the PCIe bytes, host CPU work per
+        batch) when True (default), or as f32 and rounded by the stem's
+        loader (bit-identical, no host compute: what several ranks sharing one
+        host want) when False; NEOB200_HOST_ROUND=0 flips the default."""
         import torch
         from . import _lib as L
         L.load()
@@ -147,6 +152,8 @@ class DeviceProgram:
         self._pinned_inputs: dict = {}  # input id -> (pinned staging, upload-done event)
         self.graph_exec = None
         self.use_graph = use_graph and not os.environ.get("NEOB200_NO_GRAPH")
+        self.host_round = (os.environ.get("NEOB200_HOST_ROUND", "1") != "0") if host_round is None \
+            else bool(host_round)
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
             self._lower()
@@ -247,7 +254,7 @@ class DeviceProgram:
         # rounds it RN to bf16 anyway, so rounding on the host before the
         # upload gives identical results with half the host->device bytes
         self.bf16_inputs: set[int] = set()
-        stem_srcs = {src for _, src in self.fused_stem.values()}
+        stem_srcs = {src for _, src in self.fused_stem.values()} if self.host_round else set()
         for src in stem_srcs:
             if all(u in self.skip for u in self.users[src]) and src not in g.outputs \
                     and g.nodes[src].attrs.get("layout", "NCHW") == "NCHW" \
@@ -286,6 +293,23 @@ class DeviceProgram:
                         convs.remove(pick[0])
                         self.sibling[a] = pick
                         self.sibling_of[pick[0]] = a
+        # junctions between bottleneck blocks: an expand conv (1x1, fused
+        # shortcut) and the next block's reduce conv (1x1) reading its output
+        # run as one neo_conv_junction launch; the reduce conv takes the
+        # expand's output from shared memory (both maps are still written).
+        # Opt-in (NEOB200_JUNCTION=1): bit-identical and faster per launch
+        # in isolation, but measured slower inside the graphed ResNet-50 b64
+        # step (1.190 vs 1.183 ms with only the 56x56 junctions, 1.235 ms with
+        # all): one tile in flight per SM drains its chunks serially, while the
+        # two tuned stand-alone convs overlap tiles and neighbouring launches
+        self.junction: dict[int, int] = {}       # expand conv -> reduce conv
+        self.junction_of: dict[int, int] = {}    # reduce conv -> expand conv
+        if self.mode == "bf16" and os.environ.get("NEOB200_JUNCTION") == "1":
+            for nid in order:
+                r = self._junction_partner(nid)
+                if r is not None and r not in self.junction_of and nid not in self.junction_of:
+                    self.junction[nid] = r
+                    self.junction_of[r] = nid
         # physical block size for tensor-core-illegal packed inputs
         self.phys_x: dict[int, int] = {}
         if self.mode in ("bf16", "tf32"):
@@ -359,8 +383,8 @@ class DeviceProgram:
                 tgt.last = last_step
         for nid in self.plan.input_ids:
             self.vals[nid].first = -1
-        for second, first in self.sibling_of.items():   # written by the first's launch
-            tgt = self._storage(second)
+        for second, first in list(self.sibling_of.items()) + list(self.junction_of.items()):
+            tgt = self._storage(second)                # written by the first's launch
             if tgt is not None:
                 tgt.first = min(tgt.first, self.step[first])
         # a concat buffer lives as long as any of its windows
@@ -504,6 +528,54 @@ class DeviceProgram:
         if c % dl.x or k % ol.x or (ol.x * bytes_per_elem(self.mode)) not in (32, 64, 128):
             return False
         return True
+
+    def _junction_conv_ok(self, nid: int, residual: bool) -> bool:
+        """Unpadded stride-1 1x1 bf16 conv over NCHW[64]c into NCHW[64]c,
+        bias-only epilogue (BN folded), with / without a fused residual."""
+        g = self.g
+        node = g.nodes[nid]
+        if node.kind != OpKind.Conv2d or nid in self.skip or nid in self.prologue:
+            return False
+        if nid in self.sibling or nid in self.sibling_of or nid in self.stem_fold:
+            return False
+        epi = node.attrs.get("epilogue") or {}
+        if bool(epi.get("residual")) != residual or epi.get("scale") is not None \
+                or epi.get("shift") is not None:
+            return False
+        if hw_pair(node.attrs["stride"]) != (1, 1) or hw_pair(node.attrs["pad"]) != (0, 0):
+            return False
+        k, c, r, s_ = self._conv_kcrs(nid).shape
+        src = node.inputs[0][0]
+        dl, ol = self.specs[src].layout, self.specs[nid].layout
+        if (r, s_) != (1, 1) or dl.tag != "NCHWc" or ol.tag != "NCHWc":
+            return False
+        if dl.x != 64 or ol.x != 64 or c % 64 or k % 64 or src in self.stem_fold:
+            return False
+        if residual and self.specs[node.inputs[-1][0]].layout.x != 64:
+            return False
+        return True
+
+    def _junction_partner(self, nid: int) -> int | None:
+        """Reduce conv R that can share a launch with expand conv ``nid``."""
+        if not self._junction_conv_ok(nid, residual=True):
+            return None
+        n1 = self._conv_kcrs(nid).shape[0]
+        if n1 % 128:
+            return None
+        _, _, h, w = self.specs[nid].logical_nchw
+        if h * w < int(os.environ.get("NEOB200_JUNCTION_MIN_HW", "0")):
+            return None
+        for u in self.users[nid]:
+            if u == nid or self.g.nodes[u].inputs[0][0] != nid:
+                continue
+            if not self._junction_conv_ok(u, residual=False):
+                continue
+            if self.pro_src.get(nid) is not None:
+                continue
+            n2 = self._conv_kcrs(u).shape[0]
+            if n2 <= 256:
+                return u
+        return None
 
     def _sibling_tile(self, a: int, b: int) -> int:
         """N tile of the merged launch (k_split = K of ``a`` must be a whole
@@ -731,6 +803,7 @@ class DeviceProgram:
     def _bind(self):
         from . import device as D
         g = self.g
+        self.junction_bound: set[int] = set()
         for nid in self.plan.order:
             node = g.nodes[nid]
             kind = node.kind
@@ -740,6 +813,13 @@ class DeviceProgram:
             ins = [self.vals.get(src) for src, _ in node.inputs]
             if kind == OpKind.Conv2d and nid in self.sibling_of:
                 continue                      # launched with its sibling
+            if kind == OpKind.Conv2d and nid in self.junction_of and \
+                    self.junction_of[nid] in self.junction_bound:
+                continue                      # launched with its expand conv
+            if kind == OpKind.Conv2d and nid in self.junction:
+                if self._bind_junction(node, g.nodes[self.junction[nid]]):
+                    self.junction_bound.add(nid)
+                    continue
             if kind == OpKind.Conv2d and nid in self.sibling:
                 self._bind_conv_pair(node, g.nodes[self.sibling[nid][0]], self.sibling[nid][1])
             elif kind == OpKind.Conv2d:
@@ -850,6 +930,47 @@ class DeviceProgram:
         fl, nbytes, desc = self._conv_work(n, c, h, wd, k, 1, 1, hw_pair(na.attrs["stride"]),
                                            (0, 0), es, kb=f"{ka}+{k - ka}")
         self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
+
+    def _bind_junction(self, ne, nr) -> bool:
+        """Expand conv ``ne`` (+ residual) and reduce conv ``nr`` as one
+        neo_conv_junction launch; False (bind them separately) when a window
+        or the kernel's shape limits rule it out."""
+        from . import _lib as L
+        from . import device as D
+        g = self.g
+        x, y1, y2 = self.vals[ne.inputs[0][0]], self.vals[ne.id], self.vals[nr.id]
+        res = self.vals[ne.inputs[-1][0]]
+        if any(v.win is not None or v.alias is not None for v in (x, y1, y2, res)):
+            return False
+        if any(v.px != 64 for v in (x, y1, y2, res)):
+            return False
+        w1, w2 = self._conv_kcrs(ne.id), self._conv_kcrs(nr.id)
+        n1, c1 = w1.shape[:2]
+        n2 = w2.shape[0]
+        n, _, h, w = self.specs[ne.inputs[0][0]].logical_nchw
+
+        def bias_of(node, k):
+            epi = node.attrs.get("epilogue") or {}
+            b = epi.get("bias")
+            extra = 1 if epi.get("residual") else 0
+            if len(node.inputs) - extra >= 3:
+                bb = g.nodes[node.inputs[2][0]].attrs["value"]
+                b = bb if b is None else b + bb
+            return None if b is None else self._upload(np.asarray(b, np.float32))
+
+        b1, b2 = bias_of(ne, n1), bias_of(nr, n2)
+        wd1 = D.pack_weights_umma(self._upload(w1), 64, L.MODE_BF16)
+        wd2 = D.pack_weights_umma(self._upload(w2), 64, L.MODE_BF16)
+        self.weights += [wd1, wd2]
+        relu1 = bool((ne.attrs.get("epilogue") or {}).get("relu"))
+        relu2 = bool((nr.attrs.get("epilogue") or {}).get("relu"))
+        xt, rt, y1t, y2t = x.tensor, res.tensor, y1.tensor, y2.tensor
+        fl1, nb1, d1 = self._conv_work(n, c1, h, w, n1, 1, 1, (1, 1), (0, 0), 2, residual=True)
+        fl2, nb2, d2 = self._conv_work(n, n1, h, w, n2, 1, 1, (1, 1), (0, 0), 2)
+        self._emit(f"conv{ne.id}>{nr.id}", lambda: D.conv_junction(
+            xt, wd1, b1, rt, y1t, wd2, b2, y2t, n, c1, h, w, n1, n2, relu1, relu2, self.stream),
+            nb1 + nb2 - _nb(y1t), fl1 + fl2, f"junction [{d1}] > [{d2}]")
+        return True
 
     def _bind_conv(self, node, out: _Val):
         import torch

@@ -263,3 +263,28 @@ def test_nhwc_ingest_reuses_staging(cuda):
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() == before
     assert np.array_equal(a, b)
+
+
+def test_f32_upload_equals_host_rounded_upload(cuda):
+    """host_round=False uploads the f32 image and lets the fused stem round
+    it (what bench.py does when several ranks share one host): identical
+    results to rounding on the host, twice the PCIe bytes, no host compute."""
+    import torch
+    from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, build_model, compile_graph,
+                                       model_input)
+    g = build_model("resnet18", batch=3, image=64, num_classes=10)
+    plan = ExecutablePlan.compile(compile_graph(g, mode="bf16"))
+    a = DeviceProgram(plan, 0, "bf16", host_round=True)
+    b = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode="bf16")), 0, "bf16",
+                      host_round=False)
+    name = a.input_names()[0]
+    assert a.input_tensor(name).dtype == torch.bfloat16
+    assert b.input_tensor(name).dtype == torch.float32
+    assert b.upload_bytes == 2 * a.upload_bytes
+    feeds = model_input(g, seed=9)
+    assert np.array_equal(a.run(feeds)[0], b.run(feeds)[0])
+    pinned = [torch.from_numpy(model_input(g, seed=s)[name]).pin_memory() for s in (1, 2)]
+    outs = [torch.empty((3, 10)).pin_memory() for _ in range(2)]
+    b.pipeline(pinned, outs)
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[1].numpy(), a.run({name: pinned[1].numpy()})[0])
