@@ -8,16 +8,27 @@ same planned graph for its own batch shard (weak scaling, no collective on
 the hot path; NCCL/torch.distributed only for the barrier and the max-over-
 ranks of the timings).
 
-Prints ONE JSON line on rank 0.  ``value`` is device-resident throughput
-(input already in HBM, per-step CUDA events on the executor stream, L2
-flushed between steps); ``e2e`` is the same metric through the public
-DeviceProgram API with pinned host input copied in and the output read back
-every step.  ``roofline`` describes the dominant kernel (the tcgen05 conv,
-all conv launches of a step) from an instrumented pass with CUDA events
-around every conv launch.  ``cpu_baseline`` times the unmodified reference
-(neoplan, numba, all host cores) on a bounded sample.
+Prints ONE JSON line on rank 0:
+  value     device-resident images/s (input already in HBM, per-step CUDA
+            events on the executor stream around one CUDA-graph launch, L2
+            flushed between steps outside the events);
+  e2e       the same metric through the public DeviceProgram API: every step
+            uploads one of three distinct pinned f32 batches (rounded to bf16
+            on the host at N=1, uploaded as f32 and rounded by the stem when
+            several ranks share the host) and reads the softmax back;
+  roofline  the dominant kernel = all conv launches of a step: conv time =
+            graphed step - the same graph without the conv launches; frac
+            against the measured bf16 BURST peak (the timed region is tens of
+            ms at max clock), sustained beside it; per_conv / memory_bound_
+            launches tables (in-graph, per launch: shape, us, TFLOP/s, GB/s,
+            bound, frac of its own roofline);
+  tf32      the same forward in tf32 mode against a TF32 peak measured on
+            this box (torch.matmul 8192^3, allow_tf32);
+  cpu_baseline  the unmodified reference (neoplan, numba, all host cores)
+            on full 64-image batches for ~20 s, with its cpu_identifier.
 
-``--impl reference`` runs only the reference CPU implementation (rank 0).
+``--impl reference`` runs only the reference CPU implementation (rank 0), one
+64-image batch per step.
 """
 
 from __future__ import annotations
@@ -242,14 +253,23 @@ def conv_roofline(prog, steps: int, flops_per_step: float, peak: dict, peak_kind
     conv_bytes = sum(prog.launch_bytes[i] for i in conv_idx)
     # per-launch table (in-graph, L2 flushed before each replay)
     per = timed_launches(prog, steps, flush)
+    # event nodes between launches serialise them (no PDL overlap), so the
+    # bracketed times sum to more than the graphed step: each launch's share
+    # is scaled so the conv launches sum to the measured conv time and the
+    # rest to the rest of the step
+    csum = sum(float(per[i]) for i in conv_idx) * 1e-3
+    rsum = sum(float(per[i]) for i in range(len(per)) if i not in cset) * 1e-3
     table = []
     for i, name in enumerate(prog.launch_names):
-        us = float(per[i]) * 1e3
+        us_ev = float(per[i]) * 1e3
+        scale = (conv_s / max(csum, 1e-12)) if i in cset else (rest_s / max(rsum, 1e-12))
+        us = us_ev * scale
         fl, nb = prog.launch_flops[i], prog.launch_bytes[i]
         t_tc = fl / (pk * 1e12) if fl else 0.0
         t_hbm = nb / (hbm * 1e9)
         roof = max(t_tc, t_hbm) * 1e6
         table.append({"launch": name, "desc": prog.launch_desc[i], "us": round(us, 2),
+                      "us_event_bracketed": round(us_ev, 2),
                       "tflops": round(fl / max(us, 1e-3) / 1e6, 1) if fl else None,
                       "gbs": round(nb / max(us, 1e-3) / 1e3, 1),
                       "bound": "tensor" if t_tc >= t_hbm else "hbm",
@@ -418,14 +438,16 @@ def main():
     if args.mode == "bf16" and not args.no_tf32 and world == 1:
         try:
             tf_peak = measure_tf32_peak(local)
-            tprog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode="tf32")), local,
-                                  "tf32")
+            tuned_tf = db is not None and tuned_assignment(g, db, "tf32") is not None
+            tprog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode="tf32", db=db)),
+                                  local, "tf32")
             t_s = time_program(tprog, feeds, args.steps, args.warmup, flush)
             troof, _ = conv_roofline(tprog, 3, flops_step, pk, pk_kind, flush=flush,
                                      peak_tflops=tf_peak, peak_name="tf32 measured on this box")
             tf32 = {"value": args.batch * args.steps / t_s, "unit": "images/s",
                     "ms_per_step": 1e3 * t_s / args.steps,
-                    "schedules": "in-kernel default tiles (no tf32 DB entries)",
+                    "schedules": "per-layer tuned tf32 tiles (schedules/b200.npsd)" if tuned_tf
+                                 else "in-kernel default tiles",
                     "roofline": {k: troof[k] for k in ("bound", "achieved", "peak", "unit",
                                                        "frac", "conv_ms_per_step",
                                                        "peak_source", "per_layer_roofline_ms")},
