@@ -24,6 +24,8 @@ Prints ONE JSON line on rank 0:
             bound, frac of its own roofline);
   tf32      the same forward in tf32 mode against a TF32 peak measured on
             this box (torch.matmul 8192^3, allow_tf32);
+  fp8       the same forward in the FP8 (e4m3) conv mode against an fp8
+            peak measured on this box (torch._scaled_mm 8192^3);
   cpu_baseline  the unmodified reference (neoplan, numba, all host cores)
             on full 64-image batches for ~20 s, with its cpu_identifier.
 
@@ -61,6 +63,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--untuned", action="store_true", help="ignore the tuned tile schedules")
     ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-mode measurement")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the extra fp8-mode measurement")
     ap.add_argument("--upload", default="auto", choices=["auto", "bf16", "f32"],
                     help="e2e image upload: bf16 rounded on the host (half the PCIe bytes) "
                          "or f32 rounded by the stem on the device (no host compute); auto = "
@@ -326,6 +329,32 @@ def measure_tf32_peak(device) -> float:
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+def measure_fp8_peak(device) -> float | None:
+    """Dense e4m3 tensor peak measured on this box like the TF32 one:
+    torch._scaled_mm (cuBLASLt fp8) 8192^3, best of 10, CUDA events.  None
+    when the build offers no fp8 GEMM."""
+    import torch
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=device).to(torch.float8_e4m3fn)
+        b = torch.randn(n, n, device=device).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=device)
+        mm = lambda: torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        for _ in range(3):
+            mm()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            mm()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        return 2.0 * n ** 3 / best / 1e12
+    except Exception:
+        return None
+
+
 def time_program(prog, feeds, steps, warmup, flush, stream=None):
     """Device seconds of ``steps`` graphed forwards (inputs resident, L2
     flushed between steps outside the events)."""
@@ -457,6 +486,38 @@ def main():
             tf32 = {"error": f"{type(exc).__name__}: {exc}"}
         barrier()
 
+    # ---- fp8 mode (e4m3 activations and weights, static scales) ------------
+    fp8 = None
+    if args.mode == "bf16" and not args.no_fp8 and world == 1 and args.model.startswith("resnet"):
+        try:
+            f8_peak = measure_fp8_peak(local)
+            t_c = time.time()
+            fcg = compile_graph(g, mode="fp8")
+            calib_s = time.time() - t_c
+            fprog = DeviceProgram(ExecutablePlan.compile(fcg), local, "fp8")
+            t_s = time_program(fprog, feeds, args.steps, args.warmup, flush)
+            pk8 = f8_peak if f8_peak else 2.0 * float(pk.get("bf16_tflops", 1643.1))
+            froof, _ = conv_roofline(fprog, 3, flops_step, pk, pk_kind, flush=flush,
+                                     peak_tflops=pk8,
+                                     peak_name="fp8 measured on this box" if f8_peak
+                                     else "fp8 = 2 x bf16 burst (no fp8 GEMM to measure)")
+            fp8 = {"value": args.batch * args.steps / t_s, "unit": "images/s",
+                   "ms_per_step": 1e3 * t_s / args.steps,
+                   "quantization": "e4m3 activations (static power-of-two per-tensor scales, "
+                                   "bf16 calibration forward on 4 seeded images) x e4m3 weights "
+                                   "(per-output-channel absmax/448); fp32 accumulation",
+                   "calibration_s": calib_s,
+                   "schedules": "in-kernel default tiles",
+                   "roofline": {k: froof[k] for k in ("bound", "achieved", "peak", "unit",
+                                                      "frac", "conv_ms_per_step",
+                                                      "peak_source", "per_layer_roofline_ms")},
+                   "per_conv": froof["per_conv"],
+                   "fp8_peak_tflops": f8_peak, "gpu_launches_per_step": fprog.kernel_launches}
+            del fprog
+        except Exception as exc:
+            fp8 = {"error": f"{type(exc).__name__}: {exc}"}
+        barrier()
+
     times = torch.tensor([dev_s, e2e_s, wall], dtype=torch.float64, device=local)
     if world > 1:
         torch.distributed.all_reduce(times, op=torch.distributed.ReduceOp.MAX)
@@ -503,6 +564,7 @@ def main():
             "roofline": roof,
             "conv_share_of_step": conv_share,
             "tf32": tf32,
+            "fp8": fp8,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

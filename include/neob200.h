@@ -16,8 +16,11 @@
  *   - return value: NEO_OK (0) or a neo_status; neo_last_error() returns the
  *     thread-local message of the last failure.  The Python shim maps codes to
  *     the reference exception taxonomy (errors.py:4-59).
- *   - data types: NEO_F32 = IEEE float32, NEO_BF16 = bfloat16.  "tf32" values
- *     are float32 containers whose low 13 mantissa bits are zero.
+ *   - data types: NEO_F32 = IEEE float32, NEO_BF16 = bfloat16, NEO_FP8 = OCP
+ *     e4m3 ("e4m3fn": no infinities, max 448) in one byte.  "tf32" values
+ *     are float32 containers whose low 13 mantissa bits are zero.  An e4m3
+ *     tensor carries a per-tensor scale s outside the buffer: the value of a
+ *     stored byte q is e4m3(q) * s.
  */
 #ifndef NEOB200_H
 #define NEOB200_H
@@ -41,7 +44,7 @@ typedef enum {
   NEO_ERR_INVALID_ARG = 7         /* bad pointer / size          */
 } neo_status;
 
-typedef enum { NEO_F32 = 0, NEO_BF16 = 1 } neo_dtype;
+typedef enum { NEO_F32 = 0, NEO_BF16 = 1, NEO_FP8 = 2 } neo_dtype;
 
 /* feature-map layout tags (layout.py:21-71).  NCHW == NCHW[1]c in memory. */
 typedef enum { NEO_NCHW = 0, NEO_NHWC = 1, NEO_NCHWC = 2 } neo_layout_tag;
@@ -50,7 +53,11 @@ typedef enum { NEO_NCHW = 0, NEO_NHWC = 1, NEO_NCHWC = 2 } neo_layout_tag;
 typedef enum {
   NEO_MODE_FP32 = 0, /* SIMT fp32 direct conv (parity anchor; conv_reference) */
   NEO_MODE_TF32 = 1, /* tcgen05 kind::tf32, fp32 activations rounded to tf32 */
-  NEO_MODE_BF16 = 2  /* tcgen05 kind::f16 (bf16 in, fp32 accumulate)        */
+  NEO_MODE_BF16 = 2, /* tcgen05 kind::f16 (bf16 in, fp32 accumulate)        */
+  NEO_MODE_FP8 = 3   /* tcgen05 kind::f8f6f4, e4m3 activations (per-tensor
+                        scale) x e4m3 weights (per-output-channel scale),
+                        fp32 accumulate; quantized inference, the paper's
+                        stated future work                   */
 } neo_conv_mode;
 
 typedef enum { NEO_POOL_MAX = 0, NEO_POOL_AVG = 1 } neo_pool_mode;
@@ -104,6 +111,17 @@ int neo_unpack_weights(int dtype, const void* src, void* dst, int64_t k, int64_t
 int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_dtype, int64_t k, int64_t c,
                           int64_t r, int64_t s, int x, int64_t slices_padded, int flags,
                           neo_stream_t stream);
+/* NEO_MODE_FP8 weight image: the same slice-major layout in e4m3 bytes,
+ * dst[.., k, ..] = e4m3_rn_satfinite(src[k, ..] / wscale[k]) (IEEE f32
+ * division, then round-to-nearest-even to e4m3).  wscale: device f32 per
+ * output channel (normally absmax_k / 448); the conv folds it back in through
+ * its per-channel epilogue scale. */
+int neo_pack_weights_umma_fp8(const float* src_kcrs, void* dst, const float* wscale, int64_t k,
+                              int64_t c, int64_t r, int64_t s, int x, int64_t slices_padded,
+                              int flags, neo_stream_t stream);
+/* max |x| over n elements of a device buffer of `dtype` (fp8 bytes decoded
+ * without scale) into *out (a device float); used by FP8 calibration. */
+int neo_absmax(int dtype, const void* x, int64_t n, float* out, neo_stream_t stream);
 /* number of slices the conv kernel expects for (c, r, s, x, mode, tile cfg);
  * the weight image must be packed with at least that many slices. */
 int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
@@ -138,6 +156,13 @@ int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, void* out, 
                        const float* shift, const float* bias, int relu, int64_t n, int64_t c,
                        int64_t h, int64_t w, int y, int out_cb_offset, int out_cb_total,
                        neo_stream_t stream);
+/* neo_stem_conv_pool with the output type chosen: out_dtype NEO_BF16 (as
+ * above) or NEO_FP8, then every pooled bf16 value v is stored as
+ * e4m3_rn_satfinite(v / out_scale) (out_scale > 0). */
+int neo_stem_conv_pool_q(const void* x, int x_dtype, const void* wimg, void* out, int out_dtype,
+                         float out_scale, const float* scale, const float* shift,
+                         const float* bias, int relu, int64_t n, int64_t c, int64_t h, int64_t w,
+                         int y, int out_cb_offset, int out_cb_total, neo_stream_t stream);
 
 /* Fused classifier head (B200 lowering of the reference's global average
  * pool executor.py:103-128, Flatten, Dense executor.py:197-203 and Softmax
@@ -150,6 +175,13 @@ int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, void* out, 
 int neo_classifier_head(const void* x, const void* w_bf16, const float* bias, void* pooled,
                         float* logits, float* out, int* bar, int64_t n, int64_t c, int64_t hw,
                         int y, int64_t units, int softmax, neo_stream_t stream);
+/* Same head over an e4m3 NCHW[y]c map with per-tensor scale x_scale:
+ *   pooled[n, c] = bf16(x_scale * sum_t e4m3(x[n, c, t]) / hw)  (x_dtype
+ *   NEO_FP8; NEO_BF16 ignores x_scale and equals neo_classifier_head). */
+int neo_classifier_head_q(const void* x, int x_dtype, float x_scale, const void* w_bf16,
+                          const float* bias, void* pooled, float* logits, float* out, int* bar,
+                          int64_t n, int64_t c, int64_t hw, int y, int64_t units, int softmax,
+                          neo_stream_t stream);
 
 /* ---- fused blocked convolution (kernels.py:250-303 conv_blocked, with the
  * Epilogue kernels.py:74-87 applied in the order scale/shift -> bias ->
@@ -175,7 +207,7 @@ typedef struct neo_conv_params {
   int x_cb_offset, x_cb_total;     /* input channel-block window (0,0 = dense) */
   int out_cb_offset, out_cb_total; /* concat-in-place destination window      */
   int res_cb_offset, res_cb_total;
-  int out_dtype;       /* NEO_F32 / NEO_BF16 (residual has the same dtype)    */
+  int out_dtype;       /* NEO_F32 / NEO_BF16 / NEO_FP8 (residual: same dtype) */
   int flags;           /* NEO_FLAG_ROUND_TF32 | NEO_FLAG_PAD_CHANNELS          */
   /* tile configuration (0 = automatic).  tile_w x tile_h x tile_img output
    * pixels (<= 128) form the M tile; tile_n output channels (multiple of 16,
@@ -220,6 +252,14 @@ typedef struct neo_conv_params {
   int64_t k_split;
   int relu2;
   int out2_cb_offset, out2_cb_total;
+  /* e4m3 storage scales (ABI v3; ignored unless the tensor is NEO_FP8; 0
+   * means 1): a stored residual byte q stands for e4m3(q) * res_scale, and
+   * an output value v is stored as e4m3_rn_satfinite(v / out_scale)
+   * (out2_scale for the second output).  The input's own scale is not a
+   * field: NEO_MODE_FP8 callers fold x_scale * wscale[k] into `scale`. */
+  float res_scale;
+  float out_scale;
+  float out2_scale;
 } neo_conv_params;
 
 int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream);

@@ -79,12 +79,58 @@ def _conv(n, vals, arith=None):
     return out
 
 
+def _conv_fp8(n, vals, q8: set, scales: dict):
+    """FP8-mode conv of a compiled graph (node attr ``fp8_scale`` = scale of
+    its stored e4m3 output): an e4m3 input gives an e4m3 conv
+    (ops.conv2d_fp8); the image stem (input not e4m3) runs in bf16 like the
+    device's fused stem and leaves its output unquantized."""
+    data_id = n.inputs[0][0]
+    if data_id not in q8:
+        return _conv(n, vals, "bf16"), False
+    epi = dict(n.attrs.get("epilogue") or {})
+    ins = [vals[i] for i, _ in n.inputs]
+    extra = 1 if epi.get("residual") else 0
+    residual = ins[-1] if extra else None
+    bias = epi.get("bias")
+    if len(n.inputs) - extra >= 3:
+        bias = ins[2] if bias is None else bias + ins[2]
+    data, weight = vals[data_id], vals[n.inputs[1][0]]
+    if data.ndim == 5:
+        data = ops.unpack_nchw(data)
+        if residual is not None:
+            residual = ops.unpack_nchw(residual)
+    if weight.ndim == 6:
+        weight = ops.unpack_kcrs(weight)
+    xs = np.float32(scales[data_id])
+    out_scale = n.attrs["fp8_scale"]
+    stored = ops.conv2d_fp8(data / xs, weight, xs, out_scale, n.attrs["stride"], n.attrs["pad"],
+                            epi.get("scale"), epi.get("shift"), bias, residual,
+                            bool(epi.get("relu", False)))
+    out = (stored * np.float32(out_scale)).astype(np.float32)
+    if vals[data_id].ndim == 5:
+        sch = n.attrs.get("schedule") or {}
+        y = sch.get("oc_bn") or (vals[n.inputs[1][0]].shape[5]
+                                 if vals[n.inputs[1][0]].ndim == 6 else 1)
+        out = ops.pack_nchw(out, y)
+    return out, True
+
+
+
 def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.ndarray]:
     """Run ``graph`` on numpy ``inputs`` (name -> array); outputs in
     ``graph.outputs`` order.  ``arith`` ("bf16" / "tf32") models the
     roundings of a single-pass tensor-core mode in every conv
-    (ops.conv2d_rounded); None is the reference's f32 arithmetic."""
+    (ops.conv2d_rounded); "fp8" models the FP8 mode on a graph compiled with
+    e4m3 scales (node attr ``fp8_scale``): e4m3 maps are the dequantized
+    stored values; None is the reference's f32 arithmetic."""
     vals: dict[int, np.ndarray] = {}
+    q8: set = set()                       # nodes whose values are e4m3 maps
+    scales = {nid: float(nd.attrs["fp8_scale"]) for nid, nd in graph.nodes.items()
+              if "fp8_scale" in nd.attrs} if arith == "fp8" else {}
+    return _execute(graph, inputs, arith, vals, q8, scales)
+
+
+def _execute(graph, inputs, arith, vals, q8, scales):
     for nid in _topo(graph):
         n = graph.nodes[nid]
         k = _kind(n)
@@ -97,6 +143,10 @@ def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.
             vals[nid] = a
         elif k == "Constant":
             vals[nid] = np.asarray(n.attrs["value"], dtype=np.float32)
+        elif k == "Conv2d" and arith == "fp8":
+            vals[nid], quant = _conv_fp8(n, vals, q8, scales)
+            if quant:
+                q8.add(nid)
         elif k == "Conv2d":
             vals[nid] = _conv(n, vals, arith)
         elif k == "ReLU":
@@ -115,6 +165,12 @@ def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.
         elif k in ("MaxPool", "AvgPool"):
             vals[nid] = ops.pool2d(src[0], n.attrs["window"], n.attrs["stride"],
                                    n.attrs.get("pad", 0), "max" if k == "MaxPool" else "avg")
+            if arith == "fp8" and nid in scales and n.inputs[0][0] not in q8 \
+                    and vals[nid].ndim == 5 and k == "MaxPool":
+                # the fused stem's pooled bf16 map stored as e4m3
+                s8 = np.float32(scales[nid])
+                vals[nid] = (ops.round_e4m3(vals[nid] / s8) * s8).astype(np.float32)
+                q8.add(nid)
         elif k == "ElementwiseAdd":
             vals[nid] = ops.add(src[0], src[1])
         elif k == "Concat":

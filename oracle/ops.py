@@ -234,3 +234,79 @@ def conv2d_rounded(kind, x, w, stride=1, pad=0, scale=None, shift=None, bias=Non
     out = conv2d(round_rn(x, kind), round_rn(w, kind), stride, pad, scale, shift, bias,
                  residual, relu)
     return round_rn(out, kind)
+
+
+# ---------------------------------------------------------------------------
+# e4m3 (OCP FP8 "e4m3fn": 4 exponent bits, bias 7, 3 mantissa bits, no
+# infinities, max 448) -- TEST INFRASTRUCTURE for the FP8 conv mode, which the
+# reference does not have (quantized inference is PAPER.md:433's future work).
+
+E4M3_MAX = 448.0
+
+
+def round_e4m3(a) -> np.ndarray:
+    """Round to the nearest e4m3 value, ties to even, saturating to +-448
+    (PTX cvt.rn.satfinite.e4m3x2.f32); f32 in, f32 out."""
+    x = np.asarray(a, np.float64)
+    mag = np.abs(x)
+    _, ex = np.frexp(mag)                          # mag = m * 2^ex, m in [0.5, 1)
+    e = np.maximum(ex - 1, -6)                     # normal exponent, subnormals below 2^-6
+    q = np.ldexp(1.0, e - 3)                       # spacing: 3 mantissa bits
+    r = np.minimum(np.rint(mag / q) * q, E4M3_MAX)  # rint: round half to even
+    return (np.sign(x) * r).astype(np.float32)
+
+
+def e4m3_to_bytes(v) -> np.ndarray:
+    """Encode e4m3-representable values as their bytes (uint8)."""
+    x = np.asarray(v, np.float64)
+    sign = (np.signbit(x)).astype(np.uint8) << 7
+    mag = np.abs(x)
+    _, ex = np.frexp(mag)
+    e = ex - 1
+    normal = (mag >= 2.0 ** -6)
+    exp_field = np.where(normal, e + 7, 0)
+    man = np.where(normal, np.rint((mag / np.ldexp(1.0, np.where(normal, e, 0)) - 1.0) * 8),
+                   np.rint(mag / 2.0 ** -9))
+    out = sign | (exp_field.astype(np.uint8) << 3) | man.astype(np.uint8)
+    return np.where(mag == 0, sign, out).astype(np.uint8)
+
+
+def e4m3_from_bytes(b) -> np.ndarray:
+    """Decode e4m3 bytes (uint8) to f32 (0x7f / 0xff, the NaN codes, -> nan)."""
+    u = np.asarray(b, np.uint8).astype(np.int64)
+    sign = np.where(u & 0x80, -1.0, 1.0)
+    ef = (u >> 3) & 0xF
+    man = u & 0x7
+    val = np.where(ef == 0, man * 2.0 ** -9, (1.0 + man / 8.0) * np.ldexp(1.0, ef - 7))
+    val = np.where((u & 0x7F) == 0x7F, np.nan, val)
+    return (sign * val).astype(np.float32)
+
+
+def fp8_weight_scales(w: np.ndarray) -> np.ndarray:
+    """Per-output-channel e4m3 weight scales absmax_k / 448 in f32 (1 for an
+    all-zero channel) -- the quantization rule the FP8 mode documents."""
+    w = np.asarray(w, np.float32)
+    ws = (np.abs(w.reshape(w.shape[0], -1)).max(axis=1).astype(np.float32)
+          / np.float32(E4M3_MAX)).astype(np.float32)
+    ws[ws == 0] = np.float32(1.0)
+    return ws
+
+
+def conv2d_fp8(x_q, w, x_scale, out_scale=None, stride=1, pad=0, scale=None, shift=None,
+               bias=None, residual=None, relu=False):
+    """Arithmetic model of an FP8 (e4m3) tensor-core conv: ``x_q`` holds the
+    input's e4m3 values (stored value = x_q * x_scale), weights quantized per
+    output channel (W_q = RN_e4m3(W / ws[k])), exact products accumulated
+    (f64 here, f32 on the device), the epilogue scale x_scale * ws[k] (* BN
+    scale) folded into the reference's scale slot, then bias -> residual ->
+    relu (kernels.py:185-197) and one RN_e4m3 of value / out_scale (None:
+    unquantized f32 output).  Returns the stored e4m3 values (or f32)."""
+    ws = fp8_weight_scales(w)
+    wq = round_e4m3(np.asarray(w, np.float32) / ws.reshape(-1, 1, 1, 1))
+    sc = np.float32(x_scale) * ws
+    if scale is not None:
+        sc = (sc * np.asarray(scale, np.float32)).astype(np.float32)
+    out = conv2d(x_q, wq, stride, pad, sc, shift, bias, residual, relu)
+    if out_scale is None:
+        return out
+    return round_e4m3(out / np.float32(out_scale))

@@ -30,9 +30,9 @@ _STATUS_EXC = {
 }
 
 # enums
-F32, BF16 = 0, 1
+F32, BF16, FP8 = 0, 1, 2
 NCHW_TAG, NHWC_TAG, NCHWC_TAG = 0, 1, 2
-MODE_FP32, MODE_TF32, MODE_BF16 = 0, 1, 2
+MODE_FP32, MODE_TF32, MODE_BF16, MODE_FP8 = 0, 1, 2, 3
 POOL_MAX, POOL_AVG = 0, 1
 ELT_RELU, ELT_ADD, ELT_ADD_RELU, ELT_SCALE_SHIFT, ELT_SCALE_SHIFT_RELU = range(5)
 FLAG_ROUND_TF32 = 0x1
@@ -45,8 +45,9 @@ _c_vp = ctypes.c_void_p
 
 
 class ConvParams(ctypes.Structure):
-    """Mirror of ``neo_conv_params`` (ABI v2: leading struct_size, filled in
-    by the constructor and checked by the library)."""
+    """Mirror of ``neo_conv_params`` (ABI v3: leading struct_size, filled in
+    by the constructor and checked by the library; e4m3 storage scales at
+    the end)."""
 
     def __init__(self, *args, **kw):
         super().__init__(*args, **kw)
@@ -76,6 +77,8 @@ class ConvParams(ctypes.Structure):
         ("weight_stationary", _c_int),
         ("out2", _c_vp), ("k_split", _c_i64), ("relu2", _c_int),
         ("out2_cb_offset", _c_int), ("out2_cb_total", _c_int),
+        ("res_scale", ctypes.c_float), ("out_scale", ctypes.c_float),
+        ("out2_scale", ctypes.c_float),
     ]
 
 
@@ -92,12 +95,21 @@ SIGNATURES = {
                                     _c_int, _c_int, _c_vp]),
     "neo_pack_weights_umma": (_c_int, [_c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64,
                                        _c_int, _c_i64, _c_int, _c_vp]),
+    "neo_pack_weights_umma_fp8": (_c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
+                                           _c_int, _c_i64, _c_int, _c_vp]),
+    "neo_absmax": (_c_int, [_c_int, _c_vp, _c_i64, _c_vp, _c_vp]),
     "neo_stem_fold": (_c_int, [_c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
                                _c_int, _c_int, _c_i64, _c_int, _c_int, _c_vp]),
     "neo_stem_pack_weights": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp]),
     "neo_stem_weight_bytes": (_c_i64, []),
     "neo_stem_conv_pool": (_c_int, [_c_vp, _c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
                                     _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_vp]),
+    "neo_stem_conv_pool_q": (_c_int, [_c_vp, _c_int, _c_vp, _c_vp, _c_int, ctypes.c_float, _c_vp,
+                                      _c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
+                                      _c_int, _c_int, _c_vp]),
+    "neo_classifier_head_q": (_c_int, [_c_vp, _c_int, ctypes.c_float, _c_vp, _c_vp, _c_vp, _c_vp,
+                                       _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_int, _c_i64, _c_int,
+                                       _c_vp]),
     "neo_classifier_head": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
                                      _c_i64, _c_i64, _c_int, _c_i64, _c_int, _c_vp]),
     "neo_conv_umma_slices": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),

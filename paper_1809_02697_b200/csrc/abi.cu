@@ -24,8 +24,9 @@ extern "C" {
 const char* neo_last_error(void) { return g_err; }
 
 // v2: neo_conv_params gained a leading struct_size (checked by every entry
-// point that takes the struct)
-int neo_abi_version(void) { return 2; }
+// point that takes the struct); v3: NEO_MODE_FP8 / NEO_FP8 and the e4m3
+// storage scales at the end of neo_conv_params
+int neo_abi_version(void) { return 3; }
 
 int neo_conv_params_size(void) { return (int)sizeof(neo_conv_params); }
 
@@ -66,7 +67,8 @@ int neo_conv2d_nchwc_fused(const neo_conv_params* p, neo_stream_t stream) {
                     "the BN-ReLU prologue runs on the tensor-core path only");
       return neo_conv_simt_launch(p, st);
     case NEO_MODE_TF32:
-    case NEO_MODE_BF16: return neo_conv_tc_launch(p, st);
+    case NEO_MODE_BF16:
+    case NEO_MODE_FP8: return neo_conv_tc_launch(p, st);
     default: neo_set_error("unknown conv mode %d", p->mode); return NEO_ERR_INVALID_ARG;
   }
 }

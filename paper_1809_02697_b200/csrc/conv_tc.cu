@@ -1,7 +1,11 @@
 // K-CONV: NCHW[x]c convolution as a tcgen05/TMEM implicit GEMM.
 //
 // Replaces conv_blocked (reference kernels.py:250-303, hot loop _blocked_rows
-// :135-198) for NEO_MODE_BF16 / NEO_MODE_TF32.
+// :135-198) for NEO_MODE_BF16 / NEO_MODE_TF32 / NEO_MODE_FP8 (e4m3 x e4m3
+// through tcgen05 kind::f8f6f4: the same byte geometry as bf16 -- a K step
+// is 32 bytes of a 128-byte swizzled row either way -- so the operand
+// pipeline is shared and only the instruction kind and the epilogue's
+// storage conversion differ).
 //
 // GEMM view:  M = output pixels (n, oh, ow), N = output channels k,
 //             K = (r, s, c) reduction.
@@ -32,6 +36,10 @@
 namespace {
 
 constexpr int kMaxStages = 8;
+// operand kinds (template parameter KIND): tcgen05.mma .kind and idesc format
+enum { kKindBF16 = 0, kKindTF32 = 1, kKindFP8 = 2 };
+// epilogue storage types (template parameter OUT of epi_block_tma)
+enum { kOutBF16 = 0, kOutF32 = 1, kOutFP8 = 2 };
 constexpr int kThreads = 576;   // warp 0 TMA, warp 1 MMA, warps 2-17 epilogue (2 groups of 8)
 constexpr int kEpiWarps = 16;          // warps 2..17
 constexpr int kProWarps = 8;           // prologue mode: warps 10..17 rewrite A slices
@@ -70,6 +78,10 @@ struct ConvTCParams {
   int y, out_cb_off, out_cb_total, res_cb_off, res_cb_total;
   int relu, out_f32, round_tf32;
   int k_split, relu2, out2_cb_off;   // channels >= k_split -> tmO2 (0: one output)
+  int out_kind;       // kOutBF16 / kOutF32 / kOutFP8 (the residual has the same type)
+  // e4m3 storage: residual value = e4m3(q) * res_scale; stored output
+  // q = e4m3_rn_satfinite(v * out_qscale) (out2_qscale for the second output)
+  float res_scale, out_qscale, out2_qscale;
   int tma_epi;        // stage output blocks in smem and store them with TMA
   int rowb_out;       // y * sizeof(out elem) for the TMA epilogue
   uint32_t stage_out; // bytes of one staging buffer (128 rows * rowb_out)
@@ -275,14 +287,16 @@ constexpr int kParamFloats = 3 * 256;   // scale | shift | bias for BN <= 256
 
 // One output channel block (y columns) of one pixel row: TMEM -> registers ->
 // epilogue -> swizzled smem row (which already holds the residual block when
-// HAS_RES).  OUT_F32 selects f32 vs bf16 storage.
-template <bool OUT_F32, bool HAS_RES, bool AFFINE>
+// HAS_RES).  OUT selects f32 / bf16 / e4m3 storage (qs = 1 / output scale
+// for e4m3).
+template <int OUT, bool HAS_RES, bool AFFINE>
 __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int col0,
                                               int m, uint8_t* sbuf_gen, const float* par,
                                               float relu_floor, bool round, int c_begin,
-                                              int c_step) {
+                                              int c_step, float qs) {
+  constexpr bool OUT_F32 = OUT == kOutF32;
   const int nchunk = p.y / 16;  // 16-column TMEM loads
-  constexpr int kChunks16 = OUT_F32 ? 4 : 2;   // 16-byte pieces per 16 values
+  constexpr int kChunks16 = OUT_F32 ? 4 : OUT == kOutBF16 ? 2 : 1;   // 16-byte pieces per 16 values
   // swz_offset(m, chunk, rowb) hoisted: the row's base and its XOR pattern
   // are fixed per thread (chunk * 16 < rowb keeps o >> 7 == base >> 7)
   const uint32_t srow = (uint32_t)m * (uint32_t)p.rowb_out;
@@ -336,6 +350,34 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
           o[j] = round ? neo_round_tf32(t) : t;
         }
         *reinterpret_cast<float4*>(slot) = make_float4(o[0], o[1], o[2], o[3]);
+      } else if constexpr (OUT == kOutFP8) {
+        // e4m3 storage: residual bytes widened exactly (e4m3 -> f16 -> f32)
+        // and scaled (fma: one rounding, the scales are powers of two), the
+        // relu floor, then the output scale and ONE rounding to e4m3
+        if constexpr (HAS_RES) {
+          const uint4 rv = *slot;
+          const uint32_t* r = reinterpret_cast<const uint32_t*>(&rv);
+          const float rs = p.res_scale;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const __nv_fp8x2_storage_t pr = (__nv_fp8x2_storage_t)(r[j >> 1] >> (16 * (j & 1)));
+            const float2 rf = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(pr, __NV_E4M3)));
+            f[2 * j] = fmaf(rf.x, rs, f[2 * j]);
+            f[2 * j + 1] = fmaf(rf.y, rs, f[2 * j + 1]);
+          }
+        }
+        uint4 packed;
+        uint32_t* h = reinterpret_cast<uint32_t*>(&packed);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 a = make_float2(fmaxf(f[4 * j], relu_floor) * qs,
+                                       fmaxf(f[4 * j + 1], relu_floor) * qs);
+          const float2 b = make_float2(fmaxf(f[4 * j + 2], relu_floor) * qs,
+                                       fmaxf(f[4 * j + 3], relu_floor) * qs);
+          h[j] = (uint32_t)__nv_cvt_float2_to_fp8x2(a, __NV_SATFINITE, __NV_E4M3) |
+                 ((uint32_t)__nv_cvt_float2_to_fp8x2(b, __NV_SATFINITE, __NV_E4M3) << 16);
+        }
+        *slot = packed;
       } else {
         // bf16 output in the reference order (kernels.py:185-197): the
         // residual (bf16 -> f32 is exact) is added to the f32 conv result,
@@ -473,7 +515,7 @@ __device__ __forceinline__ void tl_stamp(const ConvTCParams& p, int ev) {
 // joined inside the asm, so the issuing loop only does 32-bit uniform adds
 // (64-bit loop-carried descriptors were kept in vector registers and moved
 // to uniform registers before every MMA, stalling the issue).
-template <bool TF32, bool PAIR>
+template <int KIND, bool PAIR>
 __device__ __forceinline__ void mma_issue(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo,
                                           uint32_t bhi, uint32_t idesc, uint32_t acc) {
 #define NEO_MMA_LO(CG, KIND)                                                                 \
@@ -485,24 +527,26 @@ __device__ __forceinline__ void mma_issue(uint32_t d, uint32_t alo, uint32_t ahi
                ::"r"(d), "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc)     \
                : "memory")
   if constexpr (PAIR) {
-    if constexpr (TF32) NEO_MMA_LO("2", "tf32");
+    if constexpr (KIND == kKindTF32) NEO_MMA_LO("2", "tf32");
+    else if constexpr (KIND == kKindFP8) NEO_MMA_LO("2", "f8f6f4");
     else NEO_MMA_LO("2", "f16");
   } else {
-    if constexpr (TF32) NEO_MMA_LO("1", "tf32");
+    if constexpr (KIND == kKindTF32) NEO_MMA_LO("1", "tf32");
+    else if constexpr (KIND == kKindFP8) NEO_MMA_LO("1", "f8f6f4");
     else NEO_MMA_LO("1", "f16");
   }
 #undef NEO_MMA_LO
 }
 // n slices (slice j at alo + j*a_step, blo + j*b_step), KPR K steps of 32
 // bytes (+2 in descriptor units) each; acc0 = accumulate flag of the first MMA
-template <bool TF32, bool PAIR, int KPR>
+template <int KIND, bool PAIR, int KPR>
 __device__ __forceinline__ void mma_slices(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo,
                                            uint32_t bhi, uint32_t a_step, uint32_t b_step, int n,
                                            uint32_t idesc, uint32_t acc0) {
   for (int j = 0; j < n; ++j) {
 #pragma unroll
     for (int kk = 0; kk < KPR; ++kk)
-      mma_issue<TF32, PAIR>(d, alo + 2u * kk, ahi, blo + 2u * kk, bhi, idesc, kk == 0 ? acc0 : 1u);
+      mma_issue<KIND, PAIR>(d, alo + 2u * kk, ahi, blo + 2u * kk, bhi, idesc, kk == 0 ? acc0 : 1u);
     acc0 = 1u;
     alo += a_step;
     blo += b_step;
@@ -519,10 +563,12 @@ enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst };
 //   Halo      one band per (r, channel block), S taps = shifted views
 //   HaloWst   weight-stationary halo: one band per channel block, R*S taps,
 //             weights at b_sub * (cb*R + r) in the resident image
-template <bool TF32, bool PAIR, int MODE>
+template <int KIND, bool PAIR, int MODE>
 __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint32_t tmem_base,
                                           uint32_t sA, uint32_t sB, uint32_t sBar) {
-  const uint32_t idesc = umma_idesc(TF32 ? 2u : 1u, PAIR ? 2 * kTileM : kTileM, p.BN);
+  // A/B format codes: kind::tf32 TF32 = 2, kind::f16 BF16 = 1, kind::f8f6f4 E4M3 = 0
+  const uint32_t idesc = umma_idesc(KIND == kKindTF32 ? 2u : KIND == kKindFP8 ? 0u : 1u,
+                                    PAIR ? 2 * kTileM : kTileM, p.BN);
   const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst;
   const uint64_t adesc0 = MODE == kMmaNarrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
                           : halo_mode        ? umma_smem_desc(sA, 16, 1024, 2)
@@ -574,20 +620,20 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
       if constexpr (MODE == kMmaHaloWst) {
         const uint32_t bw = b0lo + (uint32_t)ks * R * b_sub_u;
         for (int r = 0; r < R; ++r)
-          mma_slices<TF32, PAIR, 4>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi, 8u,
+          mma_slices<KIND, PAIR, 4>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi, 8u,
                                     b_tap_u, S, idesc, (acc0 | (uint32_t)r) ? 1u : 0u);
       } else if constexpr (MODE == kMmaHalo) {
         for (int g = 0; g < G; ++g)
-          mma_slices<TF32, PAIR, 4>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi, 8u,
+          mma_slices<KIND, PAIR, 4>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi, 8u,
                                     b_tap_u, S, idesc, (acc0 | (uint32_t)g) ? 1u : 0u);
       } else if constexpr (MODE == kMmaNarrow) {
         const int ksteps = G / 2;
         for (int k = 0; k < ksteps; ++k)
-          mma_issue<TF32, PAIR>(d_tmem, ad + 2u * k * a_sub_u, ahi, bd + 2u * k * b_sub_u, bhi,
+          mma_issue<KIND, PAIR>(d_tmem, ad + 2u * k * a_sub_u, ahi, bd + 2u * k * b_sub_u, bhi,
                                 idesc, k == 0 ? acc0 : 1u);
       } else {
         constexpr int KPR = MODE == kMmaK4 ? 4 : MODE == kMmaK2 ? 2 : 1;
-        mma_slices<TF32, PAIR, KPR>(d_tmem, ad, ahi, bd, bhi, a_sub_u, b_sub_u, G, idesc, acc0);
+        mma_slices<KIND, PAIR, KPR>(d_tmem, ad, ahi, bd, bhi, a_sub_u, b_sub_u, G, idesc, acc0);
       }
       if (prof) {
         const long long c = clock64();
@@ -625,8 +671,9 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
 // PAIR: CTA-pair (cta_group::2) instantiation, launched as 2-CTA clusters;
 // kernels containing cta_group::2 instructions cannot run unclustered, so
 // single-CTA tiles use the PAIR=false instantiation
-template <bool TF32, bool PAIR>
+template <int KIND, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvTCParams p) {
+  constexpr bool TF32 = KIND == kKindTF32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   long long dbg_t_entry = 0;
   if (p.dbg & 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t_entry));
@@ -869,12 +916,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                        : p.rowb >= 128 ? kMmaK4
                        : p.rowb == 64 ? kMmaK2 : kMmaK1;
       switch (mode) {
-        case kMmaK4: mma_tiles<TF32, PAIR, kMmaK4>(p, rank, tmem_base, sA, sB, sBar); break;
-        case kMmaK2: mma_tiles<TF32, PAIR, kMmaK2>(p, rank, tmem_base, sA, sB, sBar); break;
-        case kMmaK1: mma_tiles<TF32, PAIR, kMmaK1>(p, rank, tmem_base, sA, sB, sBar); break;
-        case kMmaNarrow: mma_tiles<TF32, PAIR, kMmaNarrow>(p, rank, tmem_base, sA, sB, sBar); break;
-        case kMmaHalo: mma_tiles<TF32, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
-        default: mma_tiles<TF32, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaK4: mma_tiles<KIND, PAIR, kMmaK4>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaK2: mma_tiles<KIND, PAIR, kMmaK2>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaK1: mma_tiles<KIND, PAIR, kMmaK1>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaNarrow: mma_tiles<KIND, PAIR, kMmaNarrow>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHalo: mma_tiles<KIND, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
+        default: mma_tiles<KIND, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
       }
       if (p.dbg & 256) tl_stamp(p, 3);
       if (p.dbg & 8) {
@@ -1146,6 +1193,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           if (leader) TRACE(28 + grp, t);
           const bool sec = p.k_split > 0 && k0 >= p.k_split;   // second output's tile
           const float floor_v = (sec ? p.relu2 : p.relu) ? 0.f : -INFINITY;
+          const float qs = sec ? p.out2_qscale : p.out_qscale;
           const bool rnd = p.round_tf32 != 0;
           // the two warps of a lane quarter split the chunk's work: whole
           // blocks when there are several, 16-column pieces of one block else
@@ -1157,25 +1205,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const uint32_t tcol = trow + (b0 + i) * p.y;
             const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
-#define NEO_EPI(F32, RES, AFF) \
-  epi_block_tma<F32, RES, AFF>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep)
-            if (affine) {
-              if (p.out_f32) {
-                if (has_res) NEO_EPI(true, true, true);
-                else NEO_EPI(true, false, true);
-              } else {
-                if (has_res) NEO_EPI(false, true, true);
-                else NEO_EPI(false, false, true);
-              }
+#define NEO_EPI(OUT, RES, AFF) \
+  epi_block_tma<OUT, RES, AFF>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep, qs)
+#define NEO_EPI_OUT(OUT)                       \
+  if (affine) {                                \
+    if (has_res) NEO_EPI(OUT, true, true);     \
+    else NEO_EPI(OUT, false, true);            \
+  } else {                                     \
+    if (has_res) NEO_EPI(OUT, true, false);    \
+    else NEO_EPI(OUT, false, false);           \
+  }
+            if (p.out_kind == kOutF32) {
+              NEO_EPI_OUT(kOutF32)
+            } else if (KIND == kKindFP8 && p.out_kind == kOutFP8) {
+              NEO_EPI_OUT(kOutFP8)
             } else {
-              if (p.out_f32) {
-                if (has_res) NEO_EPI(true, true, false);
-                else NEO_EPI(true, false, false);
-              } else {
-                if (has_res) NEO_EPI(false, true, false);
-                else NEO_EPI(false, false, false);
-              }
+              NEO_EPI_OUT(kOutBF16)
             }
+#undef NEO_EPI_OUT
 #undef NEO_EPI
           }
           if (b0 + cnt >= blk_hi && !helping) {   // accumulator read: release TMEM
@@ -1394,6 +1441,11 @@ int pick_slices_per_stage(int64_t nslices, int rowb, int bn) {
   return best;
 }
 
+// operand element bytes of a tensor-core mode
+int mode_elem_size(int mode) {
+  return mode == NEO_MODE_BF16 ? 2 : mode == NEO_MODE_FP8 ? 1 : 4;
+}
+
 }  // namespace
 
 // exported for layout.cu / the ABI
@@ -1423,7 +1475,7 @@ static int epi_groups(const neo_conv_params* p, int tile_n) {
 // the direct-store path must run: the block must be a 32/64/128-byte row of
 // whole 16-column chunks and every N tile must hold whole channel blocks.
 static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
-  const int out_es = p->out_dtype == NEO_F32 ? 4 : 2;
+  const int out_es = (int)neo_dtype_size(p->out_dtype);
   const int y = p->oc_bn;
   const int rowb_out = y * out_es;
   const bool ok = y % 16 == 0 && (rowb_out == 32 || rowb_out == 64 || rowb_out == 128) &&
@@ -1479,7 +1531,7 @@ int neo_conv_default_tiles(neo_conv_params* p) {
                 "neo_conv_params.struct_size %d != %d", p->struct_size,
                 (int)sizeof(neo_conv_params));
   if (p->mode == NEO_MODE_FP32) return NEO_OK;
-  const int es = p->mode == NEO_MODE_BF16 ? 2 : 4;
+  const int es = mode_elem_size(p->mode);
   const int rowb = p->ic_bn * es;
   const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
   const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
@@ -1526,8 +1578,10 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     const int widest = (halo || red_slices <= 8 || p->pro_scale) ? std::min(128, pick_tile_n(p->k))
                                                                  : pick_tile_n(p->k);
     p->tile_n = widest;
+    // the TMA-store epilogue needs whole output channel blocks per N tile
+    const int min_bn = (p->oc_bn % 16 == 0 && p->oc_bn <= widest) ? p->oc_bn : 16;
     for (int bn : {256, 128, 64}) {
-      if (bn > widest) continue;
+      if (bn > widest || bn < min_bn) continue;
       p->tile_n = bn;
       if (m_tiles * neo_ceil_div(p->k, bn) >= sm_count_of_current_device()) break;
     }
@@ -1550,8 +1604,9 @@ int neo_conv_default_tiles(neo_conv_params* p) {
                 neo_ceil_div(p->n, p->tile_img);
       if (auto_tn) {
         p->tile_n = pick_tile_n(p->k);
+        const int min_bn = (p->oc_bn % 16 == 0 && p->oc_bn <= p->tile_n) ? p->oc_bn : 16;
         for (int bn : {256, 128, 64}) {
-          if (bn > pick_tile_n(p->k)) continue;
+          if (bn > pick_tile_n(p->k) || bn < min_bn) continue;
           p->tile_n = bn;
           if (m_tiles * neo_ceil_div(p->k, bn) >= sm_count_of_current_device()) break;
         }
@@ -1691,13 +1746,25 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   if (st != NEO_OK) return st;
   const neo_conv_params* p = &pc;
   const bool tf32 = p->mode == NEO_MODE_TF32;
-  const int es = tf32 ? 4 : 2;
+  const bool fp8 = p->mode == NEO_MODE_FP8;
+  const int kind = tf32 ? kKindTF32 : fp8 ? kKindFP8 : kKindBF16;
+  const int es = mode_elem_size(p->mode);
   const int x = p->ic_bn;
   const int rowb = x * es;
   NEO_CHECK_ARG(rowb == 16 || rowb == 32 || rowb == 64 || rowb == 128, NEO_ERR_UNSUPPORTED,
                 "tensor-core conv needs ic_bn*sizeof in {16,32,64,128} bytes (ic_bn=%d, %s)", x,
-                tf32 ? "tf32" : "bf16");
+                tf32 ? "tf32" : fp8 ? "fp8" : "bf16");
   NEO_CHECK_ARG(p->out_dtype == NEO_F32 || !tf32, NEO_ERR_UNSUPPORTED, "tf32 mode writes f32");
+  NEO_CHECK_ARG(p->out_dtype != NEO_FP8 || fp8, NEO_ERR_UNSUPPORTED,
+                "e4m3 outputs come from NEO_MODE_FP8 convs");
+  NEO_CHECK_ARG(p->out_dtype == NEO_F32 || p->out_dtype == NEO_BF16 || p->out_dtype == NEO_FP8,
+                NEO_ERR_INVALID_ARG, "bad out_dtype %d", p->out_dtype);
+  if (fp8) {
+    // e4m3 tiles: unsplit reductions, no smem prologue (the split-K fixup
+    // and the BN-ReLU rewrite only know bf16 / f32 operands)
+    NEO_CHECK_ARG(p->pro_scale == nullptr, NEO_ERR_UNSUPPORTED, "no BN-ReLU prologue in fp8 mode");
+    NEO_CHECK_ARG(p->split_k <= 1, NEO_ERR_SCHEDULE_INVALID, "no split-K in fp8 mode");
+  }
   const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
   const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
   const int BW = p->tile_w, BH = p->tile_h, BNI = p->tile_img, BN = p->tile_n;
@@ -1750,8 +1817,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   memset(&kp, 0, sizeof(kp));
   auto encode = get_encode_fn();
   NEO_CHECK_ARG(encode != nullptr, NEO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const CUtensorMapDataType dt =
-      tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapDataType dt = tf32  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                       : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   {
     const char* base = static_cast<const char*>(p->x) + (size_t)p->x_cb_offset * p->h * p->w_in * rowb;
     cuuint64_t dims[5] = {(cuuint64_t)x, (cuuint64_t)p->w_in, (cuuint64_t)p->h, (cuuint64_t)Cb,
@@ -1907,6 +1975,13 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.out2_cb_off = p->out2_cb_offset;
   }
   kp.out_f32 = p->out_dtype == NEO_F32;
+  kp.out_kind = p->out_dtype == NEO_F32 ? kOutF32 : p->out_dtype == NEO_FP8 ? kOutFP8 : kOutBF16;
+  {
+    auto inv = [](float sc) { return sc > 0.f ? (float)(1.0 / (double)sc) : 1.f; };
+    kp.res_scale = p->res_scale > 0.f ? p->res_scale : 1.f;
+    kp.out_qscale = inv(p->out_scale);
+    kp.out2_qscale = inv(p->out2_scale);
+  }
   kp.round_tf32 = (p->flags & NEO_FLAG_ROUND_TF32) ? 1 : 0;
   kp.pro = p->pro_scale != nullptr;
   kp.pro_scale = p->pro_scale;
@@ -1926,6 +2001,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.nslot = (int)std::min<int64_t>(slots, (kp.res_pf ? 2 : 1) * per_tile);
   }
   kp.tma_epi = rb_out > 0 && kp.nslot >= 1;
+  NEO_CHECK_ARG(kp.tma_epi || p->out_dtype != NEO_FP8, NEO_ERR_UNSUPPORTED,
+                "e4m3 outputs need the TMA-store epilogue (oc_bn rows of 32/64/128 bytes, "
+                "whole channel blocks per N tile)");
   {
     static const bool no_share = getenv("NEOB200_NO_SHARE_LAST") != nullptr;
     kp.share_last = (!no_share && kp.tma_epi && kp.splits == 1 && !pair && !p->pro_scale &&
@@ -1938,8 +2016,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     kp.rowb_out = rb_out;
     kp.stage_out = (uint32_t)(kTileM * kp.rowb_out);
     kp.out_box_bytes = (uint32_t)(BW * BH * BNI * kp.rowb_out);
-    const CUtensorMapDataType odt =
-        kp.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const CUtensorMapDataType odt = kp.out_f32                  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                    : kp.out_kind == kOutFP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     cuuint32_t box[5] = {(cuuint32_t)y, (cuuint32_t)BW, (cuuint32_t)BH, 1u, (cuuint32_t)BNI};
     cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
     auto encode_fm = [&](CUtensorMap* map, const void* base, int64_t cb_total) {
@@ -1981,16 +2060,18 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                          : (int)std::min<int64_t>(kp.num_units, sms);
   // opt in to the large dynamic shared memory once per (device, kernel); the
   // attribute call is kept out of later launches so they can be graph-captured
-  static bool attr_set[64][4] = {};
+  static bool attr_set[64][6] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  bool& done = attr_set[dev & 63][(tf32 ? 1 : 0) + (pair ? 2 : 0)];
+  using KFn = void (*)(ConvTCParams);
+  static const KFn kfn[3][2] = {
+      {conv_tc_kernel<kKindBF16, false>, conv_tc_kernel<kKindBF16, true>},
+      {conv_tc_kernel<kKindTF32, false>, conv_tc_kernel<kKindTF32, true>},
+      {conv_tc_kernel<kKindFP8, false>, conv_tc_kernel<kKindFP8, true>}};
+  const KFn fn = kfn[kind][pair ? 1 : 0];
+  bool& done = attr_set[dev & 63][kind * 2 + (pair ? 1 : 0)];
   if (!done) {
-    const void* fn = tf32 ? (pair ? (const void*)conv_tc_kernel<true, true>
-                                  : (const void*)conv_tc_kernel<true, false>)
-                          : (pair ? (const void*)conv_tc_kernel<false, true>
-                                  : (const void*)conv_tc_kernel<false, false>);
-    NEO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NEO_CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemBudget));
     done = true;
   }
@@ -2009,12 +2090,9 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = neo_pdl_enabled() ? 2 : 1;
-    if (tf32) NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, true>, kp));
-    else NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, true>, kp));
-  } else if (tf32) {
-    neo_launch(conv_tc_kernel<true, false>, grid, kThreads, smem, stream, kp);
+    NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, kp));
   } else {
-    neo_launch(conv_tc_kernel<false, false>, grid, kThreads, smem, stream, kp);
+    neo_launch(fn, grid, kThreads, smem, stream, kp);
   }
   NEO_LAUNCH_CHECK();
   return NEO_OK;

@@ -30,6 +30,8 @@ struct HeadParams {
   int* bar;                 // 3 counters, zero between launches
   int N, C, HW, y, units, softmax;
   float div;                // window size (H*W), the reference divides by it
+  int x_fp8;                // x holds e4m3 bytes with per-tensor scale x_scale
+  float x_scale;
   int dbg;                  // NEOB200_HEAD_DBG: phase timestamps of CTA 0 -> neo_head_dbg
 };
 
@@ -84,10 +86,29 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const __grid_constant__ 
       const bool live = grp < groups;
       const int c0 = grp * 8;
       const int cb = c0 / p.y, l0 = c0 - cb * p.y;
-      const uint4* src = reinterpret_cast<const uint4*>(
-          p.x + ((size_t)(n * cb_total + (live ? cb : 0)) * p.HW) * p.y + l0);
+      const size_t eoff = ((size_t)(n * cb_total + (live ? cb : 0)) * p.HW) * p.y + l0;
+      const uint4* src = reinterpret_cast<const uint4*>(p.x + eoff);
+      // e4m3 input: 8 channels = 8 bytes per pixel, same pixel stride in uint2s
+      const uint2* src8 = reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(p.x) + eoff);
+      for (int t0 = slice; p.x_fp8 && live && t0 < p.HW; t0 += 32) {
+        uint2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = t0 + 4 * u < p.HW ? __ldg(src8 + (size_t)(t0 + 4 * u) * step) : make_uint2(0, 0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t w2[2] = {v[u].x, v[u].y};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_fp8x2_storage_t pr = (__nv_fp8x2_storage_t)(w2[e >> 1] >> (16 * (e & 1)));
+            const float2 f = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(pr, __NV_E4M3)));
+            acc[2 * e] += f.x;
+            acc[2 * e + 1] += f.y;
+          }
+        }
+      }
       // this slice's pixels t = slice + 4u: up to 8 loads in flight per batch
-      for (int t0 = slice; live && t0 < p.HW; t0 += 32) {
+      for (int t0 = slice; !p.x_fp8 && live && t0 < p.HW; t0 += 32) {
         uint4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -113,7 +134,8 @@ __global__ void __launch_bounds__(kThreads) head_kernel(const __grid_constant__ 
         uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float a = acc[2 * e] / p.div, b = acc[2 * e + 1] / p.div;
+          // e4m3: sum of the stored values, times the (power-of-two) scale
+          const float a = acc[2 * e] * p.x_scale / p.div, b = acc[2 * e + 1] * p.x_scale / p.div;
           asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(ow[e]) : "f"(a), "f"(b));
         }
         *reinterpret_cast<uint4*>(p.pooled + (size_t)n * p.C + c0) = o;
@@ -263,7 +285,18 @@ extern "C" int neo_classifier_head(const void* x, const void* w_bf16, const floa
                                    void* pooled, float* logits, float* out, int* bar, int64_t n,
                                    int64_t c, int64_t hw, int y, int64_t units, int softmax,
                                    neo_stream_t stream) {
+  return neo_classifier_head_q(x, NEO_BF16, 1.f, w_bf16, bias, pooled, logits, out, bar, n, c, hw,
+                               y, units, softmax, stream);
+}
+
+extern "C" int neo_classifier_head_q(const void* x, int x_dtype, float x_scale,
+                                     const void* w_bf16, const float* bias, void* pooled,
+                                     float* logits, float* out, int* bar, int64_t n, int64_t c,
+                                     int64_t hw, int y, int64_t units, int softmax,
+                                     neo_stream_t stream) {
   NEO_CHECK_ARG(x && w_bf16 && pooled && out && bar, NEO_ERR_INVALID_ARG, "null pointer");
+  NEO_CHECK_ARG(x_dtype == NEO_BF16 || (x_dtype == NEO_FP8 && x_scale > 0.f), NEO_ERR_INVALID_ARG,
+                "head input must be bf16 or e4m3 with a positive scale");
   NEO_CHECK_ARG(logits, NEO_ERR_INVALID_ARG, "head needs a 2*n*units logits scratch");
   NEO_CHECK_ARG(n >= 1 && hw >= 1 && units >= 1 && c >= 256 && c % 256 == 0,
                 NEO_ERR_SHAPE_MISMATCH, "head needs C a multiple of 256 (C=%lld)", (long long)c);
@@ -286,6 +319,8 @@ extern "C" int neo_classifier_head(const void* x, const void* w_bf16, const floa
   p.units = (int)units;
   p.softmax = softmax;
   p.div = (float)hw;
+  p.x_fp8 = x_dtype == NEO_FP8;
+  p.x_scale = p.x_fp8 ? x_scale : 1.f;
   {
     static const char* dbg = getenv("NEOB200_HEAD_DBG");
     p.dbg = dbg ? 1 : 0;

@@ -267,6 +267,51 @@ __global__ void weights_umma_kernel(const float* __restrict__ src, Td* __restric
   }
 }
 
+// e4m3 weight image (NEO_MODE_FP8): the slice-major layout of
+// weights_umma_kernel, value src / wscale[k] rounded RN (satfinite) to e4m3
+__global__ void weights_umma_fp8_kernel(const float* __restrict__ src, uint8_t* __restrict__ dst,
+                                        const float* __restrict__ wscale, int64_t K, int64_t C,
+                                        int64_t R, int64_t S, int x, int64_t slices,
+                                        int64_t nslices) {
+  neo_pdl_enter();
+  const int64_t Cb = (C + x - 1) / x;
+  const int64_t total = slices * K * x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int j = (int)(t % x);
+    t /= x;
+    const int64_t k = t % K;
+    const int64_t sl = t / K;
+    float v = 0.f;
+    if (sl < nslices) {
+      const int64_t cb = sl % Cb, rs = sl / Cb;
+      const int64_t s = rs % S, r = rs / S;
+      const int64_t ch = cb * x + j;
+      if (ch < C) v = __fdiv_rn(src[((k * C + ch) * R + r) * S + s], wscale[k]);
+    }
+    dst[i] = (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
+  }
+}
+
+// max |x|: grid-stride partial maxima, one atomicMax per warp on the float
+// bits (non-negative floats order like their bit patterns)
+template <int DT>
+__global__ void absmax_kernel(const void* __restrict__ x, int64_t n, float* __restrict__ out) {
+  neo_pdl_enter();
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v;
+    if constexpr (DT == NEO_F32) v = static_cast<const float*>(x)[i];
+    else if constexpr (DT == NEO_BF16) v = __bfloat162float(static_cast<const __nv_bfloat16*>(x)[i]);
+    else v = __half2float(__half(__nv_cvt_fp8_to_halfraw(static_cast<const uint8_t*>(x)[i], __NV_E4M3)));
+    m = fmaxf(m, fabsf(v));
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
+}
+
 int64_t grid_for(int64_t total) {
   return std::max<int64_t>(1, std::min<int64_t>(neo_ceil_div(total, 256), 148 * 32));
 }
@@ -358,6 +403,40 @@ extern "C" int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_d
   else
     neo_launch(weights_umma_kernel<float>, (unsigned)grid_for(total), 256, 0, st, 
         src_kcrs, static_cast<float*>(dst), k, c, r, s, x, slices_padded, nslices, round);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_pack_weights_umma_fp8(const float* src_kcrs, void* dst, const float* wscale,
+                                         int64_t k, int64_t c, int64_t r, int64_t s, int x,
+                                         int64_t slices_padded, int flags, neo_stream_t stream) {
+  NEO_CHECK_ARG(src_kcrs && dst && wscale, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(k >= 1 && c >= 1 && r >= 1 && s >= 1 && x >= 1, NEO_ERR_SHAPE_MISMATCH,
+                "non-positive dim");
+  const int64_t nslices = r * s * neo_ceil_div(c, x);
+  NEO_CHECK_ARG((flags & NEO_FLAG_PAD_CHANNELS) || c % x == 0, NEO_ERR_INDIVISIBLE_CHANNEL,
+                "C=%lld not divisible by x=%d", (long long)c, x);
+  if (slices_padded < nslices) slices_padded = nslices;
+  const int64_t total = slices_padded * k * x;
+  neo_launch(weights_umma_fp8_kernel, (unsigned)grid_for(total), 256, 0,
+             static_cast<cudaStream_t>(stream), src_kcrs, static_cast<uint8_t*>(dst), wscale, k,
+             c, r, s, x, slices_padded, nslices);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_absmax(int dtype, const void* x, int64_t n, float* out, neo_stream_t stream) {
+  NEO_CHECK_ARG(x && out && n >= 0, NEO_ERR_INVALID_ARG, "bad absmax arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NEO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float), st));
+  if (n == 0) return NEO_OK;
+  const unsigned grid = (unsigned)grid_for(n);
+  switch (dtype) {
+    case NEO_F32: neo_launch(absmax_kernel<NEO_F32>, grid, 256, 0, st, x, n, out); break;
+    case NEO_BF16: neo_launch(absmax_kernel<NEO_BF16>, grid, 256, 0, st, x, n, out); break;
+    case NEO_FP8: neo_launch(absmax_kernel<NEO_FP8>, grid, 256, 0, st, x, n, out); break;
+    default: neo_set_error("bad dtype %d", dtype); return NEO_ERR_INVALID_ARG;
+  }
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }

@@ -4,6 +4,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -78,7 +79,7 @@ inline void neo_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 #define NEO_LAUNCH_CHECK() NEO_CUDA_TRY(neo_consume_launch_error())
 
 static inline int64_t neo_ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-static inline size_t neo_dtype_size(int dt) { return dt == NEO_BF16 ? 2 : 4; }
+static inline size_t neo_dtype_size(int dt) { return dt == NEO_BF16 ? 2 : dt == NEO_FP8 ? 1 : 4; }
 
 // ---------------------------------------------------------------------------
 // element helpers

@@ -80,6 +80,8 @@ struct StemParams {
   int tiles_h, tiles_w, num_units;
   int y, out_cb_off, out_cb_total;
   int relu;
+  int out_fp8;              // store e4m3(pooled * out_qscale) bytes instead of bf16
+  float out_qscale;
   uint32_t raw_bytes;       // BoxOf<TX>::W * 37 * C * sizeof(TX)
   int raw_stages;           // f32 box ring depth (4, 3 for C = 4)
   int dbg;                  // NEOB200_STEM_DBG: 1 no MMAs, 2 no TMEM loads, 4 no TMA,
@@ -409,7 +411,24 @@ __global__ void __launch_bounds__(kThreads, 1) stem_conv_pool_kernel(const __gri
         const int kb = k / p.y, j0 = k - kb * p.y;
         const size_t off =
             ((((size_t)n * p.out_cb_total + p.out_cb_off + kb) * p.PH + P) * p.PW + Q) * p.y + j0;
-        *reinterpret_cast<uint4*>(p.out + off) = make_uint4(b0, b1, b2, b3);
+        if (p.out_fp8) {
+          // e4m3 output: the pooled bf16 value (exact in f32) times the
+          // output scale, rounded once (RN, satfinite)
+          const uint32_t bw[4] = {b0, b1, b2, b3};
+          uint32_t q[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float2 lo = make_float2(__uint_as_float(bw[2 * e] << 16) * p.out_qscale,
+                                          __uint_as_float(bw[2 * e] & 0xFFFF0000u) * p.out_qscale);
+            const float2 hi = make_float2(__uint_as_float(bw[2 * e + 1] << 16) * p.out_qscale,
+                                          __uint_as_float(bw[2 * e + 1] & 0xFFFF0000u) * p.out_qscale);
+            q[e] = (uint32_t)__nv_cvt_float2_to_fp8x2(lo, __NV_SATFINITE, __NV_E4M3) |
+                   ((uint32_t)__nv_cvt_float2_to_fp8x2(hi, __NV_SATFINITE, __NV_E4M3) << 16);
+          }
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(p.out) + off) = make_uint2(q[0], q[1]);
+        } else {
+          *reinterpret_cast<uint4*>(p.out + off) = make_uint4(b0, b1, b2, b3);
+        }
       }
       if (prof) { const long long t = clock64(); c_pool += t - t0; t0 = t; }
     }
@@ -474,7 +493,18 @@ extern "C" int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, 
                                   const float* scale, const float* shift, const float* bias,
                                   int relu, int64_t n, int64_t c, int64_t h, int64_t w, int y,
                                   int out_cb_offset, int out_cb_total, neo_stream_t stream) {
+  return neo_stem_conv_pool_q(x, x_dtype, wimg, out, NEO_BF16, 1.f, scale, shift, bias, relu, n,
+                              c, h, w, y, out_cb_offset, out_cb_total, stream);
+}
+
+extern "C" int neo_stem_conv_pool_q(const void* x, int x_dtype, const void* wimg, void* out,
+                                    int out_dtype, float out_scale, const float* scale,
+                                    const float* shift, const float* bias, int relu, int64_t n,
+                                    int64_t c, int64_t h, int64_t w, int y, int out_cb_offset,
+                                    int out_cb_total, neo_stream_t stream) {
   NEO_CHECK_ARG(x && wimg && out, NEO_ERR_INVALID_ARG, "null tensor pointer");
+  NEO_CHECK_ARG(out_dtype == NEO_BF16 || (out_dtype == NEO_FP8 && out_scale > 0.f),
+                NEO_ERR_INVALID_ARG, "stem output must be bf16 or e4m3 with a positive scale");
   NEO_CHECK_ARG(x_dtype == NEO_F32 || x_dtype == NEO_BF16, NEO_ERR_INVALID_ARG, "bad input dtype");
   const bool xbf = x_dtype == NEO_BF16;
   const int es = xbf ? 2 : 4, box_w = xbf ? BoxOf<__nv_bfloat16>::W : BoxOf<float>::W;
@@ -527,6 +557,8 @@ extern "C" int neo_stem_conv_pool(const void* x, int x_dtype, const void* wimg, 
   kp.out_cb_off = out_cb_offset;
   kp.out_cb_total = cbt;
   kp.relu = relu;
+  kp.out_fp8 = out_dtype == NEO_FP8;
+  kp.out_qscale = kp.out_fp8 ? (float)(1.0 / (double)out_scale) : 1.f;
   kp.raw_bytes = (uint32_t)(box_w * kBoxH * c * es);
   {
     static const char* dbg = getenv("NEOB200_STEM_DBG");

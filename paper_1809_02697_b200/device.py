@@ -12,7 +12,7 @@ import torch
 from . import _lib as L
 from . import errors as E
 
-_DT = {torch.float32: L.F32, torch.bfloat16: L.BF16}
+_DT = {torch.float32: L.F32, torch.bfloat16: L.BF16, torch.float8_e4m3fn: L.FP8}
 
 
 def dtype_code(t: torch.Tensor) -> int:
@@ -23,7 +23,7 @@ def dtype_code(t: torch.Tensor) -> int:
 
 
 def torch_dtype(code: int) -> torch.dtype:
-    return torch.bfloat16 if code == L.BF16 else torch.float32
+    return {L.BF16: torch.bfloat16, L.FP8: torch.float8_e4m3fn}.get(code, torch.float32)
 
 
 def _ptr(t) -> int | None:
@@ -93,12 +93,36 @@ def pack_weights_umma(w_kcrs: torch.Tensor, x: int, mode: int, pad_channels: boo
     return out
 
 
+def pack_weights_umma_fp8(w_kcrs: torch.Tensor, wscale: torch.Tensor, x: int,
+                          pad_channels: bool = False, stream=None) -> torch.Tensor:
+    """e4m3 tensor-core weight image: RN_e4m3(w[k] / wscale[k]) in the
+    slice-major layout (neo_pack_weights_umma_fp8)."""
+    if w_kcrs.dtype != torch.float32 or wscale.dtype != torch.float32:
+        raise E.InputMismatch("fp8 weight packing takes f32 KCRS and f32 scales")
+    k, c, r, s = w_kcrs.shape
+    slices = umma_slices(L.MODE_FP8, c, r, s, x)
+    out = torch.empty(slices * k * x, dtype=torch.float8_e4m3fn, device=w_kcrs.device)
+    flags = L.FLAG_PAD_CHANNELS if pad_channels else 0
+    L.call("neo_pack_weights_umma_fp8", _ptr(w_kcrs), _ptr(out), _ptr(wscale), k, c, r, s, x,
+           slices, flags, stream_handle(stream))
+    return out
+
+
+def absmax(t: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """max |t| into a one-element device f32 tensor (neo_absmax)."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.float32, device=t.device)
+    L.call("neo_absmax", dtype_code(t), _ptr(t), t.numel(), _ptr(out), stream_handle(stream))
+    return out
+
+
 def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 0), ic_bn=1,
                 oc_bn=1, scale=None, shift=None, bias=None, residual=None, relu=False,
                 x_cb=(0, 0), out_cb=(0, 0), res_cb=(0, 0), flags=0, tile=None,
-                prologue=None, second=None) -> L.ConvParams:
+                prologue=None, second=None, qscales=None) -> L.ConvParams:
     """``second`` = (out2, k_split, relu2, out2_cb): channels [k_split, k)
-    are written to out2 (two sibling convs as one launch)."""
+    are written to out2 (two sibling convs as one launch).  ``qscales`` =
+    (res_scale, out_scale, out2_scale) of e4m3 residual / outputs."""
     p = L.ConvParams()
     p.mode = mode
     p.x, p.w, p.out = _ptr(x), _ptr(w), _ptr(out)
@@ -124,6 +148,8 @@ def conv_params(mode, x, w, out, n, c, h, w_in, k, r, s, stride=(1, 1), pad=(0, 
         out2, k_split, relu2, out2_cb = second
         p.out2, p.k_split, p.relu2 = _ptr(out2), int(k_split), int(bool(relu2))
         p.out2_cb_offset, p.out2_cb_total = out2_cb
+    if qscales is not None:
+        p.res_scale, p.out_scale, p.out2_scale = (float(v or 0.0) for v in qscales)
     return p
 
 
@@ -276,15 +302,18 @@ def pack_stem_weights(w_kcrs: torch.Tensor, stream=None) -> torch.Tensor:
 
 def stem_conv_pool(x: torch.Tensor, wimg: torch.Tensor, out: torch.Tensor, n, c, h, w, y,
                    scale=None, shift=None, bias=None, relu=True, out_cb=(0, 0),
-                   stream=None) -> None:
+                   stream=None, out_scale: float = 1.0) -> None:
     """Fused stem: maxpool3x3/2(relu(conv7x7/2(x) * scale + shift + bias))
-    from NCHW f32 / bf16 straight into bf16 NCHW[y]c (neo_stem_conv_pool)."""
-    if x.dtype not in (torch.float32, torch.bfloat16) or out.dtype != torch.bfloat16:
-        raise E.InputMismatch("stem_conv_pool takes f32 or bf16 input and writes bf16")
+    from NCHW f32 / bf16 straight into bf16 NCHW[y]c (neo_stem_conv_pool),
+    or into e4m3 bytes of value / out_scale when ``out`` is float8_e4m3fn
+    (neo_stem_conv_pool_q)."""
+    if x.dtype not in (torch.float32, torch.bfloat16) or \
+            out.dtype not in (torch.bfloat16, torch.float8_e4m3fn):
+        raise E.InputMismatch("stem_conv_pool takes f32 or bf16 input and writes bf16 or e4m3")
     opt = lambda t: _ptr(t) if t is not None else None
-    L.call("neo_stem_conv_pool", _ptr(x), dtype_code(x), _ptr(wimg), _ptr(out), opt(scale), opt(shift),
-           opt(bias), int(bool(relu)), n, c, h, w, y, out_cb[0], out_cb[1],
-           stream_handle(stream))
+    L.call("neo_stem_conv_pool_q", _ptr(x), dtype_code(x), _ptr(wimg), _ptr(out), dtype_code(out),
+           float(out_scale), opt(scale), opt(shift), opt(bias), int(bool(relu)), n, c, h, w, y,
+           out_cb[0], out_cb[1], stream_handle(stream))
 
 
 class HeadScratch:
@@ -298,11 +327,15 @@ class HeadScratch:
 
 
 def classifier_head(x: torch.Tensor, w_bf16: torch.Tensor, bias, out: torch.Tensor, n, c, hw, y,
-                    units, softmax: bool, scratch: HeadScratch, stream=None) -> None:
+                    units, softmax: bool, scratch: HeadScratch, stream=None,
+                    x_scale: float = 1.0) -> None:
     """Global avg pool -> dense (+bias) -> optional softmax in one launch
-    (neo_classifier_head)."""
-    if x.dtype != torch.bfloat16 or w_bf16.dtype != torch.bfloat16 or out.dtype != torch.float32:
-        raise E.InputMismatch("classifier_head takes bf16 features / weights and writes f32")
-    L.call("neo_classifier_head", _ptr(x), _ptr(w_bf16), _ptr(bias) if bias is not None else None,
-           _ptr(scratch.pooled), _ptr(scratch.logits), _ptr(out), _ptr(scratch.bar), n, c, hw, y,
-           units, int(bool(softmax)), stream_handle(stream))
+    (neo_classifier_head; an e4m3 ``x`` is read with its scale ``x_scale``)."""
+    if x.dtype not in (torch.bfloat16, torch.float8_e4m3fn) or w_bf16.dtype != torch.bfloat16 \
+            or out.dtype != torch.float32:
+        raise E.InputMismatch("classifier_head takes bf16 / e4m3 features, bf16 weights and "
+                              "writes f32")
+    L.call("neo_classifier_head_q", _ptr(x), dtype_code(x), float(x_scale), _ptr(w_bf16),
+           _ptr(bias) if bias is not None else None, _ptr(scratch.pooled), _ptr(scratch.logits),
+           _ptr(out), _ptr(scratch.bar), n, c, hw, y, units, int(bool(softmax)),
+           stream_handle(stream))

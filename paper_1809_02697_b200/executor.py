@@ -15,8 +15,13 @@ compiles it once per (device, mode):
   planned arena);
 * the whole forward is captured once as a CUDA graph and replayed;
 * dtype rule: NCHW[x]c feature maps are stored in the mode's activation type
-  (bf16 in "bf16", tf32-rounded f32 in "tf32", f32 in "fp32"); everything
-  else (NCHW maps, matrices, logits, graph outputs) is f32;
+  (bf16 in "bf16", tf32-rounded f32 in "tf32", f32 in "fp32", e4m3 with a
+  static per-tensor scale in "fp8"); everything else (NCHW maps, matrices,
+  logits, graph outputs) is f32;
+* "fp8" (quantized inference, quant.py) covers graphs whose blocked maps are
+  all produced by tensor-core convs or the fused image stem and read by
+  tensor-core convs or the fused classifier head (the ResNet family); other
+  operators on e4m3 maps raise InputMismatch;
 * a 3-channel (or otherwise tensor-core-illegal) packed graph input that
   only feeds convs is physically packed with zero-padded lanes to the
   smallest legal block (8 bf16 / 4 tf32 lanes), so the stem runs on the
@@ -139,7 +144,10 @@ class DeviceProgram:
         self.mode = mode
         self.device = torch.device("cuda", device)
         self.keep = list(keep)
-        self.act_dtype = torch.bfloat16 if mode == "bf16" else torch.float32
+        self.act_dtype = {"bf16": torch.bfloat16, "fp8": torch.float8_e4m3fn}.get(mode, torch.float32)
+        # fp8: static e4m3 scale of every stored map (quant.py, node attr)
+        self.qscale = {nid: float(n.attrs["fp8_scale"]) for nid, n in self.g.nodes.items()
+                       if "fp8_scale" in n.attrs}
         self.round_flag = L.FLAG_ROUND_TF32 if mode == "tf32" else 0
         self.launches: list = []        # zero-arg callables, in order
         self.tc_params: list = []       # tensor-core conv params (split-K workspace)
@@ -233,7 +241,7 @@ class DeviceProgram:
         # 3-channel image stems: fold the kernel's horizontal taps into
         # channels (neo_stem_fold) so the first conv reads 64-byte rows
         self.stem_fold: dict[int, dict] = {}
-        if self.mode in ("bf16", "tf32"):
+        if self.mode in ("bf16", "tf32", "fp8"):
             for nid in order:
                 info = self._stem_fold_info(nid)
                 if info:
@@ -242,7 +250,7 @@ class DeviceProgram:
         # input) as one fused launch in bf16 mode: neither the packed input
         # nor the conv map is materialised (neo_stem_conv_pool)
         self.fused_stem: dict[int, tuple[int, int]] = {}   # pool id -> (conv, input)
-        if self.mode == "bf16" and not os.environ.get("NEOB200_NO_FUSED_STEM"):
+        if self.mode in ("bf16", "fp8") and not os.environ.get("NEOB200_NO_FUSED_STEM"):
             for t, info in list(self.stem_fold.items()):
                 found = self._fused_stem_info(t, info)
                 if found:
@@ -263,7 +271,7 @@ class DeviceProgram:
         # classifier head (global avg pool -> flatten -> dense -> softmax) as
         # one fused launch in bf16 mode (neo_classifier_head)
         self.fused_head: dict[int, dict] = {}    # anchor (softmax or dense) id -> info
-        if self.mode == "bf16" and not os.environ.get("NEOB200_NO_FUSED_HEAD"):
+        if self.mode in ("bf16", "fp8") and not os.environ.get("NEOB200_NO_FUSED_HEAD"):
             for nid in order:
                 info = self._fused_head_info(nid)
                 if info:
@@ -274,7 +282,7 @@ class DeviceProgram:
         # two-output launch over concatenated weights
         self.sibling: dict[int, tuple[int, int]] = {}   # first conv -> (second, tile_n)
         self.sibling_of: dict[int, int] = {}            # second -> first
-        if self.mode in ("bf16", "tf32") and not os.environ.get("NEOB200_NO_SIBLING"):
+        if self.mode in ("bf16", "tf32", "fp8") and not os.environ.get("NEOB200_NO_SIBLING"):
             groups: dict[int, list[int]] = {}
             for nid in order:
                 if self._sibling_eligible(nid):
@@ -915,8 +923,13 @@ class DeviceProgram:
         k, c = w.shape[0], w.shape[1]
         n, _, h, wd = self.specs[na.inputs[0][0]].logical_nchw
         ic_bn, oc_bn = data.px, oa.layout.x
-        mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
-        wdev = D.pack_weights_umma(self._upload(w), ic_bn, mode)
+        mode = self._lib_mode()
+        qscales = None
+        if self.mode == "fp8":
+            wdev, scale = self._pack_fp8(w, ic_bn, self._scale_of(na.inputs[0][0]), scale)
+            qscales = (0.0, self._scale_of(na.id), self._scale_of(nb.id))
+        else:
+            wdev = D.pack_weights_umma(self._upload(w), ic_bn, mode)
         self.weights.append(wdev)
         flags = self.round_flag | L.FLAG_STATIC_WEIGHTS
         p = D.conv_params(mode, data.tensor, wdev, oa.tensor, n, c, h, wd, k, 1, 1,
@@ -924,9 +937,10 @@ class DeviceProgram:
                           vec(shift), vec(bias), None, parts[0]["relu"],
                           x_cb=self._window(data), out_cb=self._window(oa), flags=flags,
                           tile={"tile_n": tile_n},
-                          second=(ob.tensor, ka, parts[1]["relu"], self._window(ob)))
+                          second=(ob.tensor, ka, parts[1]["relu"], self._window(ob)),
+                          qscales=qscales)
         self.tc_params.append(p)
-        es = 2 if self.mode == "bf16" else 4
+        es = bytes_per_elem(self.mode)
         fl, nbytes, desc = self._conv_work(n, c, h, wd, k, 1, 1, hw_pair(na.attrs["stride"]),
                                            (0, 0), es, kb=f"{ka}+{k - ka}")
         self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
@@ -1024,9 +1038,17 @@ class DeviceProgram:
         if fold is not None:      # tuned for the unfolded workload: let the kernel pick
             tile = {}
         if use_tc:
-            mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
-            wk = self._upload(kcrs)
-            wd = D.pack_weights_umma(wk, ic_bn, mode, pad_channels=pad_c)
+            mode = self._lib_mode()
+            qscales = None
+            if self.mode == "fp8":
+                wd, scale = self._pack_fp8(kcrs, ic_bn, self._scale_of(data_id), scale,
+                                           pad_channels=pad_c)
+                t_scale = vec(scale)
+                qscales = (self._scale_of(node.inputs[-1][0]) if res is not None else 0.0,
+                           self._scale_of(node.id), 0.0)
+            else:
+                wk = self._upload(kcrs)
+                wd = D.pack_weights_umma(wk, ic_bn, mode, pad_channels=pad_c)
             self.weights.append(wd)
             x_t, o_t = data.tensor, out.tensor
             r_t = None
@@ -1045,9 +1067,10 @@ class DeviceProgram:
                               ic_bn, oc_bn, t_scale, t_shift, t_bias, r_t,
                               bool(epi.get("relu")), x_cb=self._window(data),
                               out_cb=self._window(out), flags=flags,
-                              tile=tile if any(tile.values()) else None, prologue=pro)
+                              tile=tile if any(tile.values()) else None, prologue=pro,
+                              qscales=qscales)
             self.tc_params.append(p)
-            es = 2 if self.mode == "bf16" else 4
+            es = bytes_per_elem(self.mode)
             fl, nbytes, desc = self._conv_work(n, c, h, w, k, r, s, (sh, sw), (ph, pw), es,
                                                residual=res is not None)
             self._emit(f"conv{node.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
@@ -1078,8 +1101,41 @@ class DeviceProgram:
         if o_t is not out.tensor:
             self._emit_convert(o_t, out.tensor)
 
+    def _lib_mode(self) -> int:
+        from . import _lib as L
+        return {"bf16": L.MODE_BF16, "tf32": L.MODE_TF32, "fp8": L.MODE_FP8}[self.mode]
+
+    def _scale_of(self, nid: int) -> float:
+        """e4m3 scale of the map node ``nid`` stores (fp8 mode)."""
+        v = self._storage(nid)
+        key = v.nid if v is not None else nid
+        if key not in self.qscale:
+            raise InputMismatch(f"fp8 mode: node {key} has no e4m3 scale (compile the graph "
+                                f"with compile_graph(..., mode='fp8'))")
+        return self.qscale[key]
+
+    def _pack_fp8(self, kcrs, ic_bn: int, x_scale: float, bn_scale, pad_channels=False):
+        """e4m3 weight image (per-output-channel scales, quant.weight_scales)
+        and the epilogue scale vector x_scale * wscale[k] (* BN scale)."""
+        from . import device as D
+        from .quant import weight_scales
+        ws = weight_scales(kcrs)
+        wd = D.pack_weights_umma_fp8(self._upload(kcrs), self._upload(ws), ic_bn,
+                                     pad_channels=pad_channels)
+        sc = np.float32(x_scale) * ws
+        if bn_scale is not None:
+            sc = sc * np.asarray(bn_scale, np.float32)
+        return wd, sc.astype(np.float32)
+
+    def _no_fp8(self, what: str, *tensors):
+        import torch
+        if any(t is not None and t.dtype == torch.float8_e4m3fn for t in tensors):
+            raise InputMismatch(f"fp8 mode: {what} on e4m3 maps is not supported (the fp8 "
+                                f"mode covers conv / fused-stem / fused-head graphs)")
+
     def _as_f32(self, v: _Val):
         import torch
+        self._no_fp8("conversion to f32", v.tensor)
         if v.tensor.dtype == torch.float32:
             return v.tensor
         t = torch.empty(v.shape, dtype=torch.float32, device=self.device)
@@ -1090,6 +1146,7 @@ class DeviceProgram:
     def _emit_convert(self, src, dst):
         from . import _lib as L
         from . import device as D
+        self._no_fp8("dtype conversion", src, dst)
         numel = src.numel()
         self._emit("convert", lambda: L.call(
             "neo_layout_transform", D.dtype_code(src), D.dtype_code(dst), src.data_ptr(),
@@ -1126,8 +1183,10 @@ class DeviceProgram:
         kr, ks = w.shape[2], w.shape[3]
         fl, _, desc = self._conv_work(n, c, h, wd, w.shape[0], kr, ks,
                                       hw_pair(node.attrs["stride"]), hw_pair(node.attrs["pad"]), 2)
+        qs = self._scale_of(pool_node.id) if self.mode == "fp8" else 1.0
         self._emit(f"stem{cv_id}_pool{pool_node.id}", lambda: D.stem_conv_pool(
-            x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream),
+            x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream,
+            out_scale=qs),
             _nb(x_t) + _vb(out) + _nb(wimg), fl, desc + " + maxpool 3x3/2")
 
     def _bind_head(self, info: dict, out: _Val):
@@ -1137,7 +1196,8 @@ class DeviceProgram:
         from . import device as D
         g = self.g
         src = self.vals[info["src"]]
-        if src.win is not None or src.tensor.dtype != torch.bfloat16 or out.tensor.dtype != torch.float32:
+        if src.win is not None or src.tensor.dtype not in (torch.bfloat16, torch.float8_e4m3fn) \
+                or out.tensor.dtype != torch.float32:
             raise InputMismatch(f"fused head {info['anchor']}: unsupported operand storage")
         dn = g.nodes[info["dense"]]
         w = np.asarray(g.nodes[dn.inputs[1][0]].attrs["value"], np.float32)
@@ -1148,13 +1208,15 @@ class DeviceProgram:
         scratch = D.HeadScratch(n, c, units, self.device)
         self.weights.append(scratch)
         x_t, o_t, sm = src.tensor, out.tensor, info["softmax"]
+        xs = self._scale_of(info["src"]) if self.mode == "fp8" else 1.0
         self._emit(f"head{info['anchor']}", lambda: D.classifier_head(
-            x_t, w_t, b_t, o_t, n, c, h * wd, y, units, sm, scratch, self.stream),
+            x_t, w_t, b_t, o_t, n, c, h * wd, y, units, sm, scratch, self.stream, x_scale=xs),
             _nb(x_t) + _nb(w_t) + _nb(o_t), 2 * n * units * c,
             f"avgpool {h}x{wd} + dense {c}->{units}" + (" + softmax" if sm else "") + f" n{n}")
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
+        self._no_fp8("layout transform", src.tensor, out.tensor)
         from . import _lib as L
         from . import device as D
         if node.id in self.stem_fold:
@@ -1190,6 +1252,7 @@ class DeviceProgram:
         return 1, 1, 1, int(np.prod(v.shape)), 1
 
     def _bind_pool(self, node, src: _Val, out: _Val):
+        self._no_fp8("pooling", src.tensor, out.tensor)
         from . import device as D
         n, cb, h, w, x = self._geom(src)
         mode = "max" if node.kind == OpKind.MaxPool else "avg"
@@ -1206,6 +1269,7 @@ class DeviceProgram:
             s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream), nb)
 
     def _bind_eltwise(self, op, a: _Val, b: _Val | None, out: _Val):
+        self._no_fp8("elementwise op", a.tensor, b.tensor if b is not None else None, out.tensor)
         from . import device as D
         n, cb, h, w, x = self._geom(a)
         flags = self.round_flag if a.layout.tag == "NCHWc" else 0
@@ -1233,6 +1297,7 @@ class DeviceProgram:
         return np.asarray(scale, np.float32), np.asarray(shift, np.float32)
 
     def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
+        self._no_fp8("batch norm", src.tensor, out.tensor)
         from . import device as D
         from . import _lib as L
         scale, shift = self._bn_scale_shift(node)
@@ -1251,6 +1316,7 @@ class DeviceProgram:
             op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream), nb)
 
     def _bind_concat(self, node, ins, out: _Val):
+        self._no_fp8("concat", out.tensor, *[v.tensor for v in ins if v is not None])
         from . import device as D
         axis = node.attrs.get("axis", 1)
         done = self.concat_windowed.get(node.id, set())
@@ -1277,6 +1343,7 @@ class DeviceProgram:
             off += chunk
 
     def _bind_dense(self, node, src: _Val, out: _Val, relu: bool = False):
+        self._no_fp8("dense", src.tensor)
         import torch
         from . import _lib as L
         from . import device as D

@@ -146,7 +146,7 @@ class Epilogue:
 
 
 def bytes_per_elem(mode: str) -> int:
-    return 2 if mode == "bf16" else 4
+    return {"bf16": 2, "fp8": 1}.get(mode, 4)
 
 
 def vector_lane_width(mode: str = "bf16") -> int:
@@ -161,7 +161,7 @@ def vector_lane_width(mode: str = "bf16") -> int:
 
 def tc_legal_block(x: int, mode: str) -> bool:
     """Can the tensor-core conv consume NCHW[x]c input in ``mode``?"""
-    return mode in ("bf16", "tf32") and x * bytes_per_elem(mode) in (16, 32, 64, 128)
+    return mode in ("bf16", "tf32", "fp8") and x * bytes_per_elem(mode) in (16, 32, 64, 128)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,105 @@
+"""FP8 (e4m3) quantized inference: static per-tensor activation scales.
+
+The reference has no quantized mode (PAPER.md:433 names quantized inference
+as future work; its only dtype is f32, graph.py:20-21).  This module is the
+host half of the B200 FP8 conv mode:
+
+* weights: per output channel, ``wscale[k] = max_j |W[k, j]| / 448`` (f32)
+  and ``W_q = RN_e4m3(W / wscale[k])`` (neo_pack_weights_umma_fp8); the conv
+  folds ``x_scale * wscale[k]`` into its per-channel epilogue scale, which is
+  the reference Epilogue's scale slot (kernels.py:74-87, applied in the order
+  of :185-197);
+* activations: one power-of-two scale per stored NCHW[x]c map, chosen by
+  running the bf16 program once on calibration images (static calibration):
+  ``s = 2^ceil(log2(absmax * margin / 448))``.  Powers of two keep every
+  (de)quantization an exact multiply, so the only rounding an e4m3 map adds
+  is the one RN_e4m3 of each stored value.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .graph import Graph, OpKind
+
+E4M3_MAX = 448.0
+# headroom over the calibration absmax (inputs of the same distribution but
+# other images reach a little further)
+CALIB_MARGIN = 1.25
+
+
+def weight_scales(kcrs: np.ndarray) -> np.ndarray:
+    """Per-output-channel e4m3 weight scales (f32): absmax / 448 (1 for an
+    all-zero channel)."""
+    w = np.asarray(kcrs, np.float32)
+    amax = np.abs(w.reshape(w.shape[0], -1)).max(axis=1).astype(np.float32)
+    ws = (amax / np.float32(E4M3_MAX)).astype(np.float32)
+    ws[ws == 0] = np.float32(1.0)
+    return ws
+
+
+def act_scale(absmax: float, margin: float = CALIB_MARGIN) -> float:
+    """Power-of-two activation scale covering ``absmax * margin``."""
+    a = float(absmax) * margin
+    if not np.isfinite(a) or a <= 0:
+        return 1.0
+    return float(2.0 ** math.ceil(math.log2(a / E4M3_MAX)))
+
+
+def quantized_nodes(g: Graph) -> list[int]:
+    """Nodes whose outputs an fp8 program may store as e4m3 maps: convs and
+    pools (the fused stem's output is its max pool)."""
+    return [nid for nid, n in g.nodes.items()
+            if n.kind in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool)]
+
+
+def calibrate(g: Graph, feeds: dict | None = None, batch: int = 4, device: int = 0,
+              margin: float = CALIB_MARGIN) -> dict[int, float]:
+    """{node id: power-of-two e4m3 scale} from one bf16 forward of ``g``
+    (the uncompiled model graph) on ``feeds`` (default: a seeded N(0, 1)
+    batch of ``batch`` images, seed 7).  Node ids refer to the simplified
+    graph, which compile_graph produces identically in every mode."""
+    import torch
+    from . import device as D
+    from .executor import DeviceProgram, ExecutablePlan, with_batch
+    from .models import model_input
+    from .passes import compile_graph
+    if feeds is None:
+        gc = with_batch(g, batch)
+        feeds = model_input(gc, seed=7)
+    else:
+        n0 = next(iter(feeds.values())).shape[0]
+        gc = with_batch(g, n0)
+    cg = compile_graph(gc, mode="bf16")
+    keep = [nid for nid in quantized_nodes(cg) if nid not in cg.outputs]
+    prog = DeviceProgram(ExecutablePlan.compile(cg), device, "bf16", keep=keep, use_graph=False)
+    prog.set_inputs(feeds)
+    prog.launch()
+    scales = {}
+    tensors = prog.output_tensors()
+    amax = torch.empty(len(tensors), dtype=torch.float32, device=prog.device)
+    with torch.cuda.stream(prog.stream):
+        for i, t in enumerate(tensors):
+            D.absmax(t.contiguous(), amax[i:i + 1], stream=prog.stream)
+    prog.stream.synchronize()
+    host = amax.cpu().numpy()
+    ids = list(cg.outputs) + keep
+    for nid, a in zip(ids, host):
+        if nid in keep:
+            scales[nid] = act_scale(a, margin)
+    return scales
+
+
+def attach_scales(g: Graph, scales: dict[int, float]) -> Graph:
+    """Store the scales as ``fp8_scale`` attrs of the compiled graph's conv
+    and pool nodes (in place)."""
+    for nid in quantized_nodes(g):
+        if nid in scales:
+            g.nodes[nid].attrs["fp8_scale"] = float(scales[nid])
+    return g
+
+
+__all__ = ["E4M3_MAX", "weight_scales", "act_scale", "calibrate", "attach_scales",
+           "quantized_nodes"]

@@ -184,7 +184,7 @@ def test_native_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
     loaded = _lib.load()
-    assert loaded.neo_abi_version() == 2
+    assert loaded.neo_abi_version() == 3
     assert loaded.neo_last_error() is not None
     assert loaded.neo_conv_params_size() == ctypes.sizeof(_lib.ConvParams)
 
