@@ -492,7 +492,8 @@ def main():
         try:
             f8_peak = measure_fp8_peak(local)
             t_c = time.time()
-            fcg = compile_graph(g, mode="fp8")
+            fcg = compile_graph(g, mode="fp8", db=db)
+            tuned_f8 = db is not None and tuned_assignment(g, db, "fp8") is not None
             calib_s = time.time() - t_c
             fprog = DeviceProgram(ExecutablePlan.compile(fcg), local, "fp8")
             t_s = time_program(fprog, feeds, args.steps, args.warmup, flush)
@@ -507,7 +508,8 @@ def main():
                                    "bf16 calibration forward on 4 seeded images) x e4m3 weights "
                                    "(per-output-channel absmax/448); fp32 accumulation",
                    "calibration_s": calib_s,
-                   "schedules": "in-kernel default tiles",
+                   "schedules": "per-layer tuned fp8 tiles (schedules/b200.npsd)" if tuned_f8
+                                else "in-kernel default tiles",
                    "roofline": {k: froof[k] for k in ("bound", "achieved", "peak", "unit",
                                                       "frac", "conv_ms_per_step",
                                                       "peak_source", "per_layer_roofline_ms")},

@@ -13,7 +13,7 @@ from __future__ import annotations
 import os
 from dataclasses import dataclass, field
 
-MODES = ("fp32", "tf32", "bf16")
+MODES = ("fp32", "tf32", "bf16", "fp8")
 
 
 def default_mode() -> str:

@@ -97,7 +97,7 @@ def _conv(n, c, h, w, k, r, s, stride, pad, ic_bn, oc_bn, res, relu, seed=0, til
     (4, 256, 14, 14, 256, 3, 3, 1, 1, 128, 128, False, False),  # deep 3x3, no relu
     (2, 512, 28, 28, 256, 1, 1, 2, 0, 128, 128, False, True),   # stride 2
     (2, 512, 7, 7, 2048, 1, 1, 1, 0, 128, 128, True, True),     # 7x7 expand + residual
-    (1, 32, 17, 19, 48, 3, 3, 2, 1, 32, 16, False, True),       # ragged map, 32/16-byte rows
+    (1, 32, 17, 19, 64, 3, 3, 2, 1, 32, 32, False, True),       # ragged map, 32-byte rows
 ])
 def test_fp8_conv_matches_e4m3_model(cuda, case):
     got, ref = _conv(*case)
