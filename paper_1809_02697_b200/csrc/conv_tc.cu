@@ -554,7 +554,7 @@ __device__ __forceinline__ void mma_slices(uint32_t d, uint32_t alo, uint32_t ah
 }
 
 // MMA issue modes of mma_tiles
-enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst };
+enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst, kMmaHalo64, kMmaHaloWst64 };
 
 // The MMA issuer's tile loop.  Barrier map as in conv_tc_kernel.  Stage and
 // accumulator indices advance by counters; MODE fixes the operand layout:
@@ -563,25 +563,31 @@ enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst };
 //   Halo      one band per (r, channel block), S taps = shifted views
 //   HaloWst   weight-stationary halo: one band per channel block, R*S taps,
 //             weights at b_sub * (cb*R + r) in the resident image
+//   Halo64 / HaloWst64  the same over 64-byte rows (SWIZZLE_64B: e4m3 maps of
+//             64 channels, bf16 of 32); a tap shift is one 64-byte row
 template <int KIND, bool PAIR, int MODE>
 __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint32_t tmem_base,
                                           uint32_t sA, uint32_t sB, uint32_t sBar) {
   // A/B format codes: kind::tf32 TF32 = 2, kind::f16 BF16 = 1, kind::f8f6f4 E4M3 = 0
   const uint32_t idesc = umma_idesc(KIND == kKindTF32 ? 2u : KIND == kKindFP8 ? 0u : 1u,
                                     PAIR ? 2 * kTileM : kTileM, p.BN);
-  const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst;
+  constexpr bool halo64 = MODE == kMmaHalo64 || MODE == kMmaHaloWst64;
+  const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst || halo64;
+  // halo row: 128 bytes (SW128, 4 K steps per row) or 64 (SW64, 2 K steps)
+  constexpr uint32_t hrow_u = halo64 ? 4u : 8u;        // one row in descriptor units
+  constexpr int HKPR = halo64 ? 2 : 4;
   const uint64_t adesc0 = MODE == kMmaNarrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
-                          : halo_mode        ? umma_smem_desc(sA, 16, 1024, 2)
-                                             : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
+                          : halo_mode ? umma_smem_desc(sA, 16, halo64 ? 512 : 1024, halo64 ? 4 : 2)
+                                      : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
   const uint64_t bdesc0 = MODE == kMmaNarrow ? umma_smem_desc(sB, p.b_sub, 128, 0)
-                          : halo_mode        ? umma_smem_desc(sB, 16, 1024, 2)
-                                             : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
+                          : halo_mode ? umma_smem_desc(sB, 16, halo64 ? 512 : 1024, halo64 ? 4 : 2)
+                                      : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
   const uint32_t a0lo = (uint32_t)adesc0, ahi = (uint32_t)(adesc0 >> 32);
   const uint32_t b0lo = (uint32_t)bdesc0, bhi = (uint32_t)(bdesc0 >> 32);
   const uint32_t a_stage_u = p.a_stage >> 4, b_stage_u = p.b_stage >> 4;
   const uint32_t a_sub_u = p.a_sub >> 4, b_sub_u = p.b_sub >> 4;
-  const uint32_t b_tap_u = (uint32_t)(PAIR ? p.BN / 2 : p.BN) * 8u;   // halo: weight tap stride
-  const uint32_t band_r_u = (uint32_t)p.BW * 8u;                      // wst halo: kernel row stride
+  const uint32_t b_tap_u = (uint32_t)(PAIR ? p.BN / 2 : p.BN) * hrow_u;   // halo: weight tap stride
+  const uint32_t band_r_u = (uint32_t)p.BW * hrow_u;                      // wst halo: kernel row stride
   const uint32_t full0 = p.pro ? sBar + 384u : sBar;                 // xfull (prologue) or full
   const int nst = p.stages, ng = p.ngroups, G = p.G, S = p.S, R = p.R;
   const int kst = p.kstages;
@@ -617,15 +623,15 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
         c_x = c;
       }
       const uint32_t acc0 = ks != ks0 ? 1u : 0u;
-      if constexpr (MODE == kMmaHaloWst) {
+      if constexpr (MODE == kMmaHaloWst || MODE == kMmaHaloWst64) {
         const uint32_t bw = b0lo + (uint32_t)ks * R * b_sub_u;
         for (int r = 0; r < R; ++r)
-          mma_slices<KIND, PAIR, 4>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi, 8u,
-                                    b_tap_u, S, idesc, (acc0 | (uint32_t)r) ? 1u : 0u);
-      } else if constexpr (MODE == kMmaHalo) {
+          mma_slices<KIND, PAIR, HKPR>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi,
+                                       hrow_u, b_tap_u, S, idesc, (acc0 | (uint32_t)r) ? 1u : 0u);
+      } else if constexpr (MODE == kMmaHalo || MODE == kMmaHalo64) {
         for (int g = 0; g < G; ++g)
-          mma_slices<KIND, PAIR, 4>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi, 8u,
-                                    b_tap_u, S, idesc, (acc0 | (uint32_t)g) ? 1u : 0u);
+          mma_slices<KIND, PAIR, HKPR>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi,
+                                       hrow_u, b_tap_u, S, idesc, (acc0 | (uint32_t)g) ? 1u : 0u);
       } else if constexpr (MODE == kMmaNarrow) {
         const int ksteps = G / 2;
         for (int k = 0; k < ksteps; ++k)
@@ -911,7 +917,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
       }
       if (p.dbg & 256) tl_stamp(p, 2);
-      const int mode = p.halo ? (p.wst ? kMmaHaloWst : kMmaHalo)
+      const int mode = p.halo ? (p.rowb == 64 ? (p.wst ? kMmaHaloWst64 : kMmaHalo64)
+                                              : (p.wst ? kMmaHaloWst : kMmaHalo))
                        : p.rowb == 16 ? kMmaNarrow
                        : p.rowb >= 128 ? kMmaK4
                        : p.rowb == 64 ? kMmaK2 : kMmaK1;
@@ -921,6 +928,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         case kMmaK1: mma_tiles<KIND, PAIR, kMmaK1>(p, rank, tmem_base, sA, sB, sBar); break;
         case kMmaNarrow: mma_tiles<KIND, PAIR, kMmaNarrow>(p, rank, tmem_base, sA, sB, sBar); break;
         case kMmaHalo: mma_tiles<KIND, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHalo64: mma_tiles<KIND, PAIR, kMmaHalo64>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHaloWst64: mma_tiles<KIND, PAIR, kMmaHaloWst64>(p, rank, tmem_base, sA, sB, sBar); break;
         default: mma_tiles<KIND, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
       }
       if (p.dbg & 256) tl_stamp(p, 3);
@@ -1483,12 +1492,15 @@ static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
   return ok ? rowb_out : 0;
 }
 
-// stride-1 convs with a horizontal window, 128-byte rows (SW128 shifted
-// views) and a padded width that fits the 128-row M tile
+// stride-1 convs with a horizontal window, 128- or 64-byte rows (SW128 /
+// SW64 shifted views: the swizzle follows absolute shared-memory address
+// bits, so a view shifted by whole rows reads what TMA wrote) and a padded
+// width that fits the 128-row M tile
 static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
   static const bool disabled = getenv("NEOB200_NO_HALO") != nullptr;
-  return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 && rowb == 128 &&
-         OW + p->s - 1 <= kTileM;
+  static const bool no64 = getenv("NEOB200_NO_HALO64") != nullptr;
+  return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 &&
+         (rowb == 128 || (rowb == 64 && !no64)) && OW + p->s - 1 <= kTileM;
 }
 static int halo_a_rows(const neo_conv_params* p) {
   return (int)neo_ceil_div(kTileM + p->s - 1, 8) * 8;

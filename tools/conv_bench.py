@@ -46,8 +46,8 @@ def main():
     from paper_1809_02697_b200 import device as D
 
     dev = torch.device("cuda:0")
-    act = torch.bfloat16 if args.mode == "bf16" else torch.float32
-    lmode = L.MODE_BF16 if args.mode == "bf16" else L.MODE_TF32
+    act = {"bf16": torch.bfloat16, "fp8": torch.float8_e4m3fn}.get(args.mode, torch.float32)
+    lmode = {"bf16": L.MODE_BF16, "fp8": L.MODE_FP8}.get(args.mode, L.MODE_TF32)
     n, c, k, hw, r, st = args.n, args.c, args.k, args.hw, args.r, args.stride
     s_ = args.s or r
     H, W = args.h or hw, args.w or hw
@@ -58,9 +58,13 @@ def main():
     ow = (W + 2 * pw - s_) // sw + 1
     x = torch.randn((n, -(-c // args.x), H, W, args.x), device=dev).to(act)
     w = torch.randn((k, c, r, s_), device=dev) * 0.05
-    wd = D.pack_weights_umma(w, args.x, lmode, pad_channels=c % args.x != 0)
+    if args.mode == "fp8":
+        wd = D.pack_weights_umma_fp8(w, torch.full((k,), 0.05 / 8, device=dev), args.x,
+                                     pad_channels=c % args.x != 0)
+    else:
+        wd = D.pack_weights_umma(w, args.x, lmode, pad_channels=c % args.x != 0)
     out = torch.empty((n, k // args.y, oh, ow, args.y), dtype=act, device=dev)
-    res = torch.randn_like(out) if args.res else None
+    res = torch.randn(out.shape, device=dev).to(act) if args.res else None
     bias = torch.randn(k, device=dev)
     flops = 2 * n * k * c * r * s_ * oh * ow
     byts = (x.numel() + out.numel() * (2 if args.res else 1)) * x.element_size()
