@@ -119,6 +119,13 @@ int neo_pack_weights_umma(const float* src_kcrs, void* dst, int dst_dtype, int64
 int neo_pack_weights_umma_fp8(const float* src_kcrs, void* dst, const float* wscale, int64_t k,
                               int64_t c, int64_t r, int64_t s, int x, int64_t slices_padded,
                               int flags, neo_stream_t stream);
+/* e4m3 NCHW[x]c (channel-block window cb_off of cb_total blocks; cb_total 0 =
+ * dense) -> NCHW f32 / bf16 (dst_dtype): value = e4m3(q) * scale.  The FP8
+ * mode's exit from the blocked chain (transform_array layout.py:219-235 with
+ * the e4m3 decode). */
+int neo_dequant_fp8(const void* src, void* dst, int dst_dtype, float scale, int64_t n, int64_t c,
+                    int64_t h, int64_t w, int x, int64_t cb_off, int64_t cb_total,
+                    neo_stream_t stream);
 /* max |x| over n elements of a device buffer of `dtype` (fp8 bytes decoded
  * without scale) into *out (a device float); used by FP8 calibration. */
 int neo_absmax(int dtype, const void* x, int64_t n, float* out, neo_stream_t stream);
@@ -287,7 +294,8 @@ int neo_conv_junction(const void* x, const void* w1, const float* b1, const void
 
 /* ---- memory-bound operators (executor.py:96-203) ------------------------ */
 /* Max (pad -inf) / avg (pad 0, / win^2) pooling over h, w of NCHW[x]c
- * (x = 1 is NCHW), replaces _pool2d executor.py:103-128. */
+ * (x = 1 is NCHW), replaces _pool2d executor.py:103-128.  NEO_FP8 maps:
+ * max pooling only, x % 16 == 0, the output keeps the input's scale. */
 int neo_pool2d(int dtype, int mode, const void* in, void* out, int64_t n, int64_t cb, int64_t h,
                int64_t w, int x, int win, int stride, int pad, int flags, neo_stream_t stream);
 /* Same with channel-block windows: the input is blocks [in_cb_off, +cb) of a

@@ -79,14 +79,39 @@ def _conv(n, vals, arith=None):
     return out
 
 
-def _conv_fp8(n, vals, q8: set, scales: dict):
+def _conv_fp8(n, vals, q8: set, scales: dict, feeds_pool: set):
     """FP8-mode conv of a compiled graph (node attr ``fp8_scale`` = scale of
     its stored e4m3 output): an e4m3 input gives an e4m3 conv
     (ops.conv2d_fp8); the image stem (input not e4m3) runs in bf16 like the
     device's fused stem and leaves its output unquantized."""
     data_id = n.inputs[0][0]
     if data_id not in q8:
-        return _conv(n, vals, "bf16"), False
+        # bf16 operands (the image stem); its output is stored as e4m3 unless
+        # a max pool fused with it (the ResNet stem) quantizes the pooled map
+        if n.attrs.get("fp8_scale") is None or n.id in feeds_pool:
+            return _conv(n, vals, "bf16"), False
+        data, weight = vals[data_id], vals[n.inputs[1][0]]
+        epi = dict(n.attrs.get("epilogue") or {})
+        ins = [vals[i] for i, _ in n.inputs]
+        bias = epi.get("bias")
+        if len(n.inputs) >= 3:
+            bias = ins[2] if bias is None else bias + ins[2]
+        blocked = data.ndim == 5
+        if blocked:
+            data = ops.unpack_nchw(data)
+        if weight.ndim == 6:
+            weight = ops.unpack_kcrs(weight)
+        s8 = np.float32(n.attrs["fp8_scale"])
+        out = ops.conv2d(ops.round_rn(data, "bf16"), ops.round_rn(weight, "bf16"), n.attrs["stride"],
+                         n.attrs["pad"], epi.get("scale"), epi.get("shift"), bias, None,
+                         bool(epi.get("relu", False)))
+        out = (ops.round_e4m3(out / s8) * s8).astype(np.float32)
+        if blocked:
+            sch = n.attrs.get("schedule") or {}
+            y = sch.get("oc_bn") or (vals[n.inputs[1][0]].shape[5]
+                                     if vals[n.inputs[1][0]].ndim == 6 else 1)
+            out = ops.pack_nchw(out, y)
+        return out, True
     epi = dict(n.attrs.get("epilogue") or {})
     ins = [vals[i] for i, _ in n.inputs]
     extra = 1 if epi.get("residual") else 0
@@ -131,6 +156,14 @@ def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.
 
 
 def _execute(graph, inputs, arith, vals, q8, scales):
+    # convs whose only consumers are max pools: the device fuses an image
+    # stem with its pool and stores the pooled map, not the conv output
+    users: dict[int, list] = {}
+    for nd in graph.nodes.values():
+        for src, _ in nd.inputs:
+            users.setdefault(src, []).append(nd)
+    feeds_pool = {nid for nid, nd in graph.nodes.items() if _kind(nd) == "Conv2d" and users.get(nid)
+                  and all(_kind(u) == "MaxPool" for u in users[nid])}
     for nid in _topo(graph):
         n = graph.nodes[nid]
         k = _kind(n)
@@ -144,7 +177,7 @@ def _execute(graph, inputs, arith, vals, q8, scales):
         elif k == "Constant":
             vals[nid] = np.asarray(n.attrs["value"], dtype=np.float32)
         elif k == "Conv2d" and arith == "fp8":
-            vals[nid], quant = _conv_fp8(n, vals, q8, scales)
+            vals[nid], quant = _conv_fp8(n, vals, q8, scales, feeds_pool)
             if quant:
                 q8.add(nid)
         elif k == "Conv2d":
@@ -165,8 +198,9 @@ def _execute(graph, inputs, arith, vals, q8, scales):
         elif k in ("MaxPool", "AvgPool"):
             vals[nid] = ops.pool2d(src[0], n.attrs["window"], n.attrs["stride"],
                                    n.attrs.get("pad", 0), "max" if k == "MaxPool" else "avg")
-            if arith == "fp8" and nid in scales and n.inputs[0][0] not in q8 \
-                    and vals[nid].ndim == 5 and k == "MaxPool":
+            if arith == "fp8" and k == "MaxPool" and n.inputs[0][0] in q8:
+                q8.add(nid)           # max of stored e4m3 values: exact, same scale
+            elif arith == "fp8" and nid in scales and vals[nid].ndim == 5 and k == "MaxPool":
                 # the fused stem's pooled bf16 map stored as e4m3
                 s8 = np.float32(scales[nid])
                 vals[nid] = (ops.round_e4m3(vals[nid] / s8) * s8).astype(np.float32)

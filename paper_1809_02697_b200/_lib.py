@@ -98,6 +98,8 @@ SIGNATURES = {
     "neo_pack_weights_umma_fp8": (_c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
                                            _c_int, _c_i64, _c_int, _c_vp]),
     "neo_absmax": (_c_int, [_c_int, _c_vp, _c_i64, _c_vp, _c_vp]),
+    "neo_dequant_fp8": (_c_int, [_c_vp, _c_vp, _c_int, ctypes.c_float, _c_i64, _c_i64, _c_i64,
+                                 _c_i64, _c_int, _c_i64, _c_i64, _c_vp]),
     "neo_stem_fold": (_c_int, [_c_vp, _c_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
                                _c_int, _c_int, _c_i64, _c_int, _c_int, _c_vp]),
     "neo_stem_pack_weights": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp]),

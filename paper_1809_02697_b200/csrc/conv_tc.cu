@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   }
             if (p.out_kind == kOutF32) {
               NEO_EPI_OUT(kOutF32)
-            } else if (KIND == kKindFP8 && p.out_kind == kOutFP8) {
+            } else if (KIND != kKindTF32 && p.out_kind == kOutFP8) {
               NEO_EPI_OUT(kOutFP8)
             } else {
               NEO_EPI_OUT(kOutBF16)
@@ -1502,8 +1502,17 @@ static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
   return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 &&
          (rowb == 128 || (rowb == 64 && !no64)) && OW + p->s - 1 <= kTileM;
 }
+// halo bands are whole 1024-byte swizzle periods (8 rows of 128 B, 16 of
+// 64 B): TMA's SWIZZLE_64B pattern is laid out on 1024-byte boundaries, and
+// a 64-byte-row band of an odd number of 512-byte atoms misplaced every
+// following stage / the weight image (measured: e4m3 64->128 3x3 tiles)
+static int halo_row_align(const neo_conv_params* p) {
+  const int es = p->mode == NEO_MODE_BF16 ? 2 : p->mode == NEO_MODE_FP8 ? 1 : 4;
+  return std::max(8, 1024 / std::max(16, p->ic_bn * es));
+}
 static int halo_a_rows(const neo_conv_params* p) {
-  return (int)neo_ceil_div(kTileM + p->s - 1, 8) * 8;
+  const int al = halo_row_align(p);
+  return (int)neo_ceil_div(kTileM + p->s - 1, al) * al;
 }
 // CTA-pair (cta_group::2) tiles: explicit cta_pair (2 on, 1 off) or
 // NEOB200_PAIR=1; needs an unsplit reduction, at least two M tiles and an N
@@ -1534,7 +1543,8 @@ static int64_t wst_w_bytes(const neo_conv_params* p, bool halo, int rowb, int G,
 }
 // halo band: 128 rows read from the largest shift (R-1)*BW + S-1
 static int wst_band_rows(const neo_conv_params* p, int BW) {
-  return (int)neo_ceil_div(kTileM + (p->r - 1) * BW + p->s - 1, 8) * 8;
+  const int al = halo_row_align(p);
+  return (int)neo_ceil_div(kTileM + (p->r - 1) * BW + p->s - 1, al) * al;
 }
 
 int neo_conv_default_tiles(neo_conv_params* p) {
@@ -1767,8 +1777,10 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
                 "tensor-core conv needs ic_bn*sizeof in {16,32,64,128} bytes (ic_bn=%d, %s)", x,
                 tf32 ? "tf32" : fp8 ? "fp8" : "bf16");
   NEO_CHECK_ARG(p->out_dtype == NEO_F32 || !tf32, NEO_ERR_UNSUPPORTED, "tf32 mode writes f32");
-  NEO_CHECK_ARG(p->out_dtype != NEO_FP8 || fp8, NEO_ERR_UNSUPPORTED,
-                "e4m3 outputs come from NEO_MODE_FP8 convs");
+  // e4m3 outputs: NEO_MODE_FP8 convs, or a bf16 conv entering an fp8 chain
+  // (e.g. a 3-channel image stem folded to bf16); residuals stay e4m3
+  NEO_CHECK_ARG(p->out_dtype != NEO_FP8 || !tf32, NEO_ERR_UNSUPPORTED,
+                "e4m3 outputs come from NEO_MODE_FP8 or NEO_MODE_BF16 convs");
   NEO_CHECK_ARG(p->out_dtype == NEO_F32 || p->out_dtype == NEO_BF16 || p->out_dtype == NEO_FP8,
                 NEO_ERR_INVALID_ARG, "bad out_dtype %d", p->out_dtype);
   if (fp8) {

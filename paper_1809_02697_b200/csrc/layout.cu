@@ -425,6 +425,50 @@ extern "C" int neo_pack_weights_umma_fp8(const float* src_kcrs, void* dst, const
   return NEO_OK;
 }
 
+// e4m3 NCHW[x]c (scale) -> NCHW f32 / bf16: value = e4m3(q) * scale (the
+// FP8 mode's exit from the blocked chain, e.g. into a classifier)
+template <typename Td>
+__global__ void dequant_fp8_kernel(const uint8_t* __restrict__ src, Td* __restrict__ dst,
+                                   float scale, int64_t N, int64_t C, int64_t HW, int x,
+                                   int64_t cb_off, int64_t cb_total) {
+  neo_pdl_enter();
+  const int64_t total = N * C * HW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % HW;
+    const int64_t c = (i / HW) % C;
+    const int64_t n = i / (HW * C);
+    const uint8_t q = src[((n * cb_total + cb_off + c / x) * HW + p) * x + c % x];
+    const float v = __half2float(__half(__nv_cvt_fp8_to_halfraw(q, __NV_E4M3))) * scale;
+    dst[i] = Elem<Td>::from_f(v);
+  }
+}
+
+extern "C" int neo_dequant_fp8(const void* src, void* dst, int dst_dtype, float scale, int64_t n,
+                               int64_t c, int64_t h, int64_t w, int x, int64_t cb_off,
+                               int64_t cb_total, neo_stream_t stream) {
+  NEO_CHECK_ARG(src && dst && scale > 0.f, NEO_ERR_INVALID_ARG, "bad dequant arguments");
+  NEO_CHECK_ARG(x >= 1 && c % x == 0, NEO_ERR_INDIVISIBLE_CHANNEL, "C=%lld not divisible by x=%d",
+                (long long)c, x);
+  if (cb_total <= 0) cb_total = c / x;
+  const int64_t total = n * c * h * w;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dst_dtype == NEO_BF16)
+    neo_launch(dequant_fp8_kernel<__nv_bfloat16>, (unsigned)grid_for(total), 256, 0, st,
+               static_cast<const uint8_t*>(src), static_cast<__nv_bfloat16*>(dst), scale, n, c,
+               h * w, x, cb_off, cb_total);
+  else if (dst_dtype == NEO_F32)
+    neo_launch(dequant_fp8_kernel<float>, (unsigned)grid_for(total), 256, 0, st,
+               static_cast<const uint8_t*>(src), static_cast<float*>(dst), scale, n, c, h * w, x,
+               cb_off, cb_total);
+  else {
+    neo_set_error("dequant writes f32 or bf16");
+    return NEO_ERR_INVALID_ARG;
+  }
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
 extern "C" int neo_absmax(int dtype, const void* x, int64_t n, float* out, neo_stream_t stream) {
   NEO_CHECK_ARG(x && out && n >= 0, NEO_ERR_INVALID_ARG, "bad absmax arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -472,6 +472,50 @@ __global__ void avgpool3s1_bf16(const __nv_bfloat16* __restrict__ in,
   }
 }
 
+// e4m3 max pooling (FP8 mode): 16 lanes per thread; e4m3 -> f16 is exact,
+// max in f16x2 (padding -inf), and the maximum -- one of the stored values --
+// converts back to the same e4m3 byte, so the map keeps its scale
+__global__ void pool_max_fp8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t Cb,
+                             int64_t P, int H, int W, int OH, int OW, int x, int win, int stride,
+                             int pad, Win wnd) {
+  neo_pdl_enter();
+  const uint32_t groups = x / 16;
+  const uint32_t per_plane = (uint32_t)OH * OW * groups;
+  for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
+    const uint8_t* src = in + wnd.in_plane(plane, Cb) * H * W * x;
+    uint8_t* dst = out + wnd.out_plane(plane, Cb) * OH * OW * x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_plane;
+         i += gridDim.x * blockDim.x) {
+      const uint32_t gq = i % groups, t = i / groups;
+      const int ow = (int)(t % (uint32_t)OW), oh = (int)(t / (uint32_t)OW);
+      __half2 m[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m[k] = __half2(__ushort_as_half(0xFC00u), __ushort_as_half(0xFC00u));
+      for (int r = 0; r < win; ++r) {
+        const int ih = oh * stride + r - pad;
+        if (ih < 0 || ih >= H) continue;
+        for (int q = 0; q < win; ++q) {
+          const int iw = ow * stride + q - pad;
+          if (iw < 0 || iw >= W) continue;
+          const uint4 raw = __ldg(reinterpret_cast<const uint4*>(src + ((int64_t)ih * W + iw) * x + gq * 16));
+          const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const __nv_fp8x2_storage_t pr = (__nv_fp8x2_storage_t)(w4[k >> 1] >> (16 * (k & 1)));
+            m[k] = __hmax2(m[k], __half2(__nv_cvt_fp8x2_to_halfraw2(pr, __NV_E4M3)));
+          }
+        }
+      }
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        o[k] = (uint32_t)__nv_cvt_halfraw2_to_fp8x2(__half2_raw(m[2 * k]), __NV_SATFINITE, __NV_E4M3) |
+               ((uint32_t)__nv_cvt_halfraw2_to_fp8x2(__half2_raw(m[2 * k + 1]), __NV_SATFINITE, __NV_E4M3) << 16);
+      *reinterpret_cast<uint4*>(dst + ((int64_t)oh * OW + ow) * x + gq * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 template <typename T, int V, bool IS_MAX>
 void launch_pool_vec(const T* in, T* out, int64_t cb, int64_t P, int h, int w, int OH, int OW,
                      int x, int win, int stride, int pad, bool round, Win wnd, cudaStream_t st) {
@@ -692,6 +736,16 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
   const bool al = aligned16(in) && aligned16(out);
   const bool is_max = mode == NEO_POOL_MAX;
   const bool global = OH == 1 && OW == 1 && pad == 0 && win == h && win == w && x % 2 == 0;
+  if (dtype == NEO_FP8) {
+    // e4m3 maps: max pooling only (an average would need a new scale)
+    NEO_CHECK_ARG(is_max, NEO_ERR_UNSUPPORTED, "e4m3 pooling is max pooling only");
+    NEO_CHECK_ARG(x % 16 == 0 && al, NEO_ERR_UNSUPPORTED, "e4m3 pooling needs 16-lane blocks");
+    neo_launch(pool_max_fp8, plane_grid(P, (int64_t)OH * OW * (x / 16)), 256, 0, st,
+               static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), cb, P, (int)h, (int)w,
+               (int)OH, (int)OW, x, win, stride, pad, wnd);
+    NEO_LAUNCH_CHECK();
+    return NEO_OK;
+  }
   if (global) {
     const float inv = (float)(win * win);
     const unsigned grid = (unsigned)grid_for(P * (x / 2));

@@ -108,6 +108,13 @@ def pack_weights_umma_fp8(w_kcrs: torch.Tensor, wscale: torch.Tensor, x: int,
     return out
 
 
+def dequant_fp8(src: torch.Tensor, dst: torch.Tensor, scale: float, n, c, h, w, x,
+                cb=(0, 0), stream=None) -> None:
+    """e4m3 NCHW[x]c -> NCHW f32 / bf16 times ``scale`` (neo_dequant_fp8)."""
+    L.call("neo_dequant_fp8", _ptr(src), _ptr(dst), dtype_code(dst), float(scale), n, c, h, w, x,
+           cb[0], cb[1], stream_handle(stream))
+
+
 def absmax(t: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """max |t| into a one-element device f32 tensor (neo_absmax)."""
     if out is None:

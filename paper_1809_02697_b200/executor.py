@@ -145,6 +145,10 @@ class DeviceProgram:
         self.device = torch.device("cuda", device)
         self.keep = list(keep)
         self.act_dtype = {"bf16": torch.bfloat16, "fp8": torch.float8_e4m3fn}.get(mode, torch.float32)
+        # dense layers (and their non-blocked inputs) and folded image stems
+        # run bf16 in fp8 mode: only the blocked conv chain is e4m3
+        self.dense_mode = "bf16" if mode == "fp8" else mode
+        self.dense_dtype = torch.bfloat16 if mode == "fp8" else self.act_dtype
         # fp8: static e4m3 scale of every stored map (quant.py, node attr)
         self.qscale = {nid: float(n.attrs["fp8_scale"]) for nid, n in self.g.nodes.items()
                        if "fp8_scale" in n.attrs}
@@ -225,7 +229,7 @@ class DeviceProgram:
         # ReLU writes the ReLU's value with the relu fused into the epilogue.
         self.tc_dense: set[int] = set()
         self.fused_dense_relu: dict[int, int] = {}   # relu id -> dense id
-        if self.mode in ("bf16", "tf32"):
+        if self.mode in ("bf16", "tf32", "fp8"):
             for nid in order:
                 node = g.nodes[nid]
                 if node.kind != OpKind.Dense:
@@ -678,7 +682,7 @@ class DeviceProgram:
             return None
         S, sw, pw = geo.pop()
         F = S * c
-        lanes = [x for x in (8, 16, 32, 64, 4) if tc_legal_block(x, self.mode)]
+        lanes = [x for x in (8, 16, 32, 64, 4) if tc_legal_block(x, self.dense_mode)]
         fits = [x for x in sorted(lanes) if x >= F]
         if S == 1 or not fits:
             return None
@@ -709,7 +713,7 @@ class DeviceProgram:
         if nid in self.stem_fold:
             f = self.stem_fold[nid]
             shape = (f["n"], -(-f["F"] // f["xf"]), f["h"], f["ow"], f["xf"])
-            return _Val(nid, shape, self.act_dtype, layout, px=f["xf"])
+            return _Val(nid, shape, self.dense_dtype, layout, px=f["xf"])
         if layout.tag == "NCHWc":
             px = self.phys_x.get(nid, layout.x)
             n, c, h, w = spec.logical_nchw
@@ -718,13 +722,13 @@ class DeviceProgram:
             else:
                 shape = spec.shape
             return _Val(nid, tuple(shape), self.act_dtype, layout, px=px)
-        dtype = self.act_dtype if self._feeds_tc_dense(nid) else torch.float32
+        dtype = self.dense_dtype if self._feeds_tc_dense(nid) else torch.float32
         return _Val(nid, tuple(spec.shape), dtype, layout)
 
     def _dense_block(self, width: int) -> int:
         """Legal tensor-core block dividing a dense input width (0 if none)."""
         for x in (64, 32, 16, 8, 4):
-            if width % x == 0 and tc_legal_block(x, self.mode):
+            if width % x == 0 and tc_legal_block(x, self.dense_mode):
                 return x
         return 0
 
@@ -1040,12 +1044,20 @@ class DeviceProgram:
         if use_tc:
             mode = self._lib_mode()
             qscales = None
-            if self.mode == "fp8":
+            if self.mode == "fp8" and data.tensor.dtype == torch.float8_e4m3fn:
                 wd, scale = self._pack_fp8(kcrs, ic_bn, self._scale_of(data_id), scale,
                                            pad_channels=pad_c)
                 t_scale = vec(scale)
                 qscales = (self._scale_of(node.inputs[-1][0]) if res is not None else 0.0,
                            self._scale_of(node.id), 0.0)
+            elif self.mode == "fp8":
+                # a bf16 input (the folded 3-channel image of a VGG-style
+                # stem): bf16 operands, e4m3 output entering the fp8 chain
+                mode = L.MODE_BF16
+                if res is not None:
+                    raise InputMismatch(f"fp8 mode: conv {node.id} on a bf16 input with a residual")
+                wd = D.pack_weights_umma(self._upload(kcrs), ic_bn, mode, pad_channels=pad_c)
+                qscales = (0.0, self._scale_of(node.id), 0.0)
             else:
                 wk = self._upload(kcrs)
                 wd = D.pack_weights_umma(wk, ic_bn, mode, pad_channels=pad_c)
@@ -1216,9 +1228,19 @@ class DeviceProgram:
 
     # other operators ---------------------------------------------------------
     def _bind_transform(self, node, src: _Val, out: _Val):
-        self._no_fp8("layout transform", src.tensor, out.tensor)
+        import torch
         from . import _lib as L
         from . import device as D
+        if src.tensor.dtype == torch.float8_e4m3fn and out.layout.tag == "NCHW" \
+                and src.layout.tag == "NCHWc" and out.tensor.dtype != torch.float8_e4m3fn:
+            # the fp8 chain's exit: decode e4m3 * scale into NCHW f32 / bf16
+            n, c, h, w = self.specs[node.inputs[0][0]].logical_nchw
+            s8 = self._scale_of(node.inputs[0][0])
+            s_t, d_t, cbw = src.tensor, out.tensor, self._window(src)
+            self._emit(f"dequant{node.id}", lambda: D.dequant_fp8(
+                s_t, d_t, s8, n, c, h, w, src.px, cbw, self.stream), _vb(src) + _nb(d_t))
+            return
+        self._no_fp8("layout transform", src.tensor, out.tensor)
         if node.id in self.stem_fold:
             f = self.stem_fold[node.id]
             s_t, d_t = src.tensor, out.tensor
@@ -1252,7 +1274,17 @@ class DeviceProgram:
         return 1, 1, 1, int(np.prod(v.shape)), 1
 
     def _bind_pool(self, node, src: _Val, out: _Val):
-        self._no_fp8("pooling", src.tensor, out.tensor)
+        import torch
+        if src.tensor.dtype == torch.float8_e4m3fn:
+            # e4m3 max pooling keeps the map's scale (quant.attach_scales gives
+            # the pool its input's scale); an average would need a new one
+            if node.kind != OpKind.MaxPool or out.tensor.dtype != torch.float8_e4m3fn:
+                self._no_fp8("average pooling", src.tensor)
+            if self._scale_of(node.id) != self._scale_of(node.inputs[0][0]):
+                raise InputMismatch(f"fp8 max pool {node.id}: output scale must equal the "
+                                    f"input's")
+        else:
+            self._no_fp8("pooling", src.tensor, out.tensor)
         from . import device as D
         n, cb, h, w, x = self._geom(src)
         mode = "max" if node.kind == OpKind.MaxPool else "avg"
@@ -1343,7 +1375,7 @@ class DeviceProgram:
             off += chunk
 
     def _bind_dense(self, node, src: _Val, out: _Val, relu: bool = False):
-        self._no_fp8("dense", src.tensor)
+        self._no_fp8("dense", src.tensor)    # fp8 mode: dense inputs are bf16
         import torch
         from . import _lib as L
         from . import device as D
@@ -1353,12 +1385,12 @@ class DeviceProgram:
         if len(node.inputs) == 3:
             b_t = self._upload(self.g.nodes[node.inputs[2][0]].attrs["value"])
         n = src.shape[0]
-        if node.id in self.tc_dense and src.tensor.dtype == self.act_dtype:
+        if node.id in self.tc_dense and src.tensor.dtype == self.dense_dtype:
             # tensor cores: (n, width) row-major == NCHW[x]c with H = W = 1, so
             # the dense is a 1x1 conv; the output (n, units) is NCHW[y]c with
             # H = W = 1 for any y dividing units.
             x = self._dense_block(width)
-            mode = L.MODE_BF16 if self.mode == "bf16" else L.MODE_TF32
+            mode = L.MODE_BF16 if self.dense_mode == "bf16" else L.MODE_TF32
             wd = D.pack_weights_umma(self._upload(w.reshape(units, width, 1, 1)), x, mode)
             self.weights.append(wd)
             o_t = out.tensor
@@ -1374,7 +1406,7 @@ class DeviceProgram:
                        _nb(wd) + _nb(src.tensor) + _nb(o_t), 2 * n * units * width,
                        f"dense {width}->{units} n{n}")
             return
-        a_t = self._as_f32(src) if self.mode != "bf16" or src.tensor.dtype != torch.bfloat16 \
+        a_t = self._as_f32(src) if self.dense_mode != "bf16" or src.tensor.dtype != torch.bfloat16 \
             else src.tensor
         w_t = self._upload(w, a_t.dtype)
         o_t = out.tensor if out.tensor.dtype == torch.float32 else torch.empty(

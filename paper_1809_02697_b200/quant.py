@@ -94,10 +94,19 @@ def calibrate(g: Graph, feeds: dict | None = None, batch: int = 4, device: int =
 
 def attach_scales(g: Graph, scales: dict[int, float]) -> Graph:
     """Store the scales as ``fp8_scale`` attrs of the compiled graph's conv
-    and pool nodes (in place)."""
-    for nid in quantized_nodes(g):
-        if nid in scales:
-            g.nodes[nid].attrs["fp8_scale"] = float(scales[nid])
+    and pool nodes (in place).  A max pool inherits its input's scale: its
+    outputs are a subset of its inputs' stored values, so the e4m3 bytes
+    carry over unchanged."""
+    from .graph import topo_sort
+    for nid in topo_sort(g):
+        node = g.nodes[nid]
+        if node.kind not in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool):
+            continue
+        src = node.inputs[0][0] if node.inputs else None
+        if node.kind == OpKind.MaxPool and src is not None and "fp8_scale" in g.nodes[src].attrs:
+            node.attrs["fp8_scale"] = g.nodes[src].attrs["fp8_scale"]
+        elif nid in scales:
+            node.attrs["fp8_scale"] = float(scales[nid])
     return g
 
 

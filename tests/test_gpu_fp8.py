@@ -15,9 +15,15 @@ order scale -> bias -> residual -> relu (kernels.py:185-197), one RN
   at most 1e-3 of the outputs, each within one e4m3 step;
 * fused stem / head: bit-identical to the bf16 kernels followed by / fed
   with the documented e4m3 conversion;
-* whole networks: logits within 5e-2 (rel_err, reference
-  tests/test_kernels.py:31-32) of the e4m3 model of the same compiled graph
-  and scales; the model's own distance to the f32 oracle is reported."""
+* whole networks: logits of the device within 1e-1 (rel_err, reference
+  tests/test_kernels.py:31-32: max|a-b| / max|b|) and 2e-2 in RMS of the
+  e4m3 model of the same compiled graph and scales.  One e4m3 step at the
+  largest stored values is 1/16 = 6%, and a single accumulation-order tie
+  flip upstream moves later maps by about one step (tools/fp8_layer_diff.py:
+  VGG-16's maps are identical to the model up to conv 21, then differ by one
+  step at a few values), so the max-norm bound admits ~1.5 steps; the RMS
+  bound is what pins the bulk.  The model's own distance to the f32 oracle
+  is reported beside it."""
 
 import numpy as np
 import pytest
@@ -29,7 +35,14 @@ from oracle.ops import (conv2d_fp8, e4m3_from_bytes, e4m3_to_bytes, fp8_weight_s
 pytestmark = pytest.mark.gpu
 
 MISMATCH_FRAC = 1e-3      # fraction of stored values that may differ by one e4m3 step
-NET_TOL = 5e-2            # network logits vs the e4m3 model
+NET_TOL = 1e-1            # network logits vs the e4m3 model (max norm, ~1.5 e4m3 steps)
+NET_RMS = 2e-2            # ... and in RMS
+
+
+def _rms(a, b) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.sqrt(np.mean((a - b) ** 2)) / max(1e-30, np.sqrt(np.mean(b ** 2))))
 
 
 def _to_dev(vals, x):
@@ -98,6 +111,9 @@ def _conv(n, c, h, w, k, r, s, stride, pad, ic_bn, oc_bn, res, relu, seed=0, til
     (2, 512, 28, 28, 256, 1, 1, 2, 0, 128, 128, False, True),   # stride 2
     (2, 512, 7, 7, 2048, 1, 1, 1, 0, 128, 128, True, True),     # 7x7 expand + residual
     (1, 32, 17, 19, 64, 3, 3, 2, 1, 32, 32, False, True),       # ragged map, 32-byte rows
+    (2, 64, 32, 32, 128, 3, 3, 1, 1, 64, 128, False, True),     # 64-byte-row halo, N=128,
+    (1, 64, 56, 56, 128, 3, 3, 1, 1, 64, 128, True, True),      # weight-stationary bands
+    (2, 64, 20, 20, 128, 3, 3, 1, 1, 64, 128, False, True),
 ])
 def test_fp8_conv_matches_e4m3_model(cuda, case):
     got, ref = _conv(*case)
@@ -128,11 +144,15 @@ def test_fp8_rejects_unsupported(cuda):
                       tile={"split_k": 2})
     with pytest.raises(ScheduleInvalid):
         D.conv2d(p)
-    xb = torch.zeros((1, 1, 8, 8, 64), dtype=torch.bfloat16, device="cuda")
-    wb = torch.zeros(64 * 64, dtype=torch.bfloat16, device="cuda")
-    p = D.conv_params(L.MODE_BF16, xb, wb, out, 1, 64, 8, 8, 64, 1, 1, ic_bn=64, oc_bn=64)
+    xf = torch.zeros((1, 2, 8, 8, 32), dtype=torch.float32, device="cuda")
+    wf = torch.zeros(64 * 64, dtype=torch.float32, device="cuda")
+    p = D.conv_params(L.MODE_TF32, xf, wf, out, 1, 64, 8, 8, 64, 1, 1, ic_bn=32, oc_bn=64)
     with pytest.raises(DeviceError):
-        D.conv2d(p)                     # e4m3 output from a bf16-mode conv
+        D.conv2d(p)                     # e4m3 output from a tf32-mode conv
+    p = D.conv_params(L.MODE_FP8, x, w, out, 1, 64, 8, 8, 64, 1, 1, ic_bn=64, oc_bn=64,
+                      prologue=(torch.ones(64, device="cuda"), torch.zeros(64, device="cuda"), True))
+    with pytest.raises(DeviceError):
+        D.conv2d(p)                     # no BN-ReLU prologue on e4m3 tiles
 
 
 def test_fp8_stem_and_head_kernels(cuda):
@@ -176,7 +196,7 @@ def test_fp8_stem_and_head_kernels(cuda):
     assert torch.equal(outs[0], outs[1])
 
 
-def _net(model, batch, image=None, seed_idx=None):
+def _net(model, batch, image=None):
     from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, build_model, compile_graph,
                                        model_input)
     kw = {"softmax": False}
@@ -189,21 +209,28 @@ def _net(model, batch, image=None, seed_idx=None):
     return g, cg, prog, feeds
 
 
-@pytest.mark.parametrize("model,batch", [("resnet18", 2), ("resnet50", 2)])
-def test_fp8_network_vs_e4m3_model(cuda, model, batch):
-    """Whole ResNet forwards in fp8 (fused stem, e4m3 convs incl. two-output
-    siblings, fused head) against the e4m3 model of the same compiled graph
-    and calibration scales."""
-    g, cg, prog, feeds = _net(model, batch)
+@pytest.mark.parametrize("model,batch,image", [("resnet18", 2, None), ("resnet50", 2, None),
+                                               ("vgg16", 2, 64)])
+def test_fp8_network_vs_e4m3_model(cuda, model, batch, image):
+    """Whole forwards in fp8 against the e4m3 model of the same compiled
+    graph and calibration scales: ResNets (fused stem, e4m3 convs incl.
+    two-output siblings, fused head) and VGG-16 (bf16-operand first conv
+    writing e4m3, e4m3 max pools, e4m3 -> bf16 exit into the dense
+    classifier)."""
+    g, cg, prog, feeds = _net(model, batch, image)
     names = prog.launch_names
-    assert any(n.startswith("stem") for n in names) and any(n.startswith("head") for n in names)
+    if model.startswith("resnet"):
+        assert any(n.startswith("stem") for n in names) and any(n.startswith("head") for n in names)
+    else:
+        assert any(n.startswith("maxpool") for n in names) and any(n.startswith("dequant") for n in names)
     got = prog.run(feeds)[0]
     model8 = oracle.execute_reference(cg, feeds, arith="fp8")[0]
     ref = oracle.execute_reference(g, feeds)[0]
     err = oracle.rel_err(got, model8)
-    print(f"{model} fp8: device vs e4m3 model {err:.3e}, model vs f32 oracle "
+    rms = _rms(got, model8)
+    print(f"{model} fp8: device vs e4m3 model {err:.3e} (RMS {rms:.3e}), model vs f32 oracle "
           f"{oracle.rel_err(model8, ref):.3e}, device vs f32 {oracle.rel_err(got, ref):.3e}")
-    assert err <= NET_TOL, err
+    assert err <= NET_TOL and rms <= NET_RMS, (err, rms)
 
 
 def test_fp8_bench_program(cuda):
@@ -218,8 +245,30 @@ def test_fp8_bench_program(cuda):
     cg3 = with_batch(cg, 3)
     model8 = oracle.execute_reference(cg3, sub, arith="fp8")[0]
     err = oracle.rel_err(got[idx], model8)
-    assert err <= NET_TOL, err
+    assert err <= NET_TOL and _rms(got[idx], model8) <= NET_RMS, err
     assert np.isfinite(got).all()
+
+
+def test_fp8_max_pool_and_dequant_kernels(cuda):
+    """e4m3 max pooling returns the stored bytes of the window maximum (the
+    map keeps its scale); the dequant exit is e4m3(q) * scale exactly."""
+    import torch
+    from paper_1809_02697_b200 import device as D
+    rng = np.random.default_rng(5)
+    n, c, h, w, x = 2, 256, 14, 14, 128
+    q = round_e4m3(rng.standard_normal((n, c, h, w)).astype(np.float32) * 30)
+    src = _to_dev(q, x)
+    for win, st, pad in ((2, 2, 0), (3, 2, 1), (3, 1, 1)):
+        oh = (h + 2 * pad - win) // st + 1
+        out = torch.empty((n, c // x, oh, oh, x), dtype=torch.float8_e4m3fn, device="cuda")
+        D.pool2d(src, out, n, c // x, h, w, x, win, st, pad, "max")
+        torch.cuda.synchronize()
+        assert np.array_equal(_from_dev(out), oracle.ops.pool2d(q, win, st, pad, "max"))
+    for dt in (torch.float32, torch.bfloat16):
+        dst = torch.empty((n, c, h, w), dtype=dt, device="cuda")
+        D.dequant_fp8(src, dst, 2.0 ** -3, n, c, h, w, x)
+        torch.cuda.synchronize()
+        assert np.array_equal(dst.float().cpu().numpy(), q * np.float32(2.0 ** -3))
 
 
 def test_fp8_rejects_graphs_outside_the_mode(cuda):
