@@ -36,3 +36,59 @@ def test_conv2d_rounded_is_the_rounded_conv(rng):
         want = ops.round_rn(ops.conv2d(ops.round_rn(x, kind), ops.round_rn(w, kind), 1, 1), kind)
         assert np.array_equal(ops.conv2d_rounded(kind, x, w, 1, 1), want)
     assert oracle.rel_err(ops.conv2d_rounded("tf32", x, w, 1, 1), ops.conv2d(x, w, 1, 1)) < 3e-3
+
+
+# --- e4m3 (FP8 mode) ------------------------------------------------------
+
+def test_round_e4m3_matches_torch_float8(rng):
+    """oracle.ops.round_e4m3 == torch's float8_e4m3fn conversion (RN-even)
+    on 10^6 values over the whole normal / subnormal range, and the byte
+    codecs round-trip every finite code."""
+    import torch
+    x = (rng.standard_normal(1_000_000) * np.exp(rng.uniform(-12, 7, 1_000_000))).astype(np.float32)
+    x = np.clip(x, -448, 448)
+    x[:6] = [0.0, -0.0, 2.0 ** -9, 2.0 ** -10, 1.0625, 1.1875]      # subnormal / ties
+    want = torch.from_numpy(x).to(torch.float8_e4m3fn).float().numpy()
+    got = ops.round_e4m3(x)
+    assert np.array_equal(got, want)
+    codes = np.arange(256, dtype=np.uint8)
+    vals = ops.e4m3_from_bytes(codes)
+    ref = torch.from_numpy(codes).view(torch.float8_e4m3fn).float().numpy()
+    fin = ~np.isnan(ref)
+    assert np.array_equal(vals[fin], ref[fin]) and np.isnan(vals[~fin]).all()
+    assert np.array_equal(ops.e4m3_from_bytes(ops.e4m3_to_bytes(vals[fin])), vals[fin])
+
+
+def test_round_e4m3_saturates():
+    """satfinite: everything past 448 (in magnitude) stores as +-448."""
+    x = np.array([448.0, 460.0, 464.0, 1e6, -1e6, -500.0], np.float32)
+    assert np.array_equal(ops.round_e4m3(x), np.array([448, 448, 448, 448, -448, -448], np.float32))
+
+
+def test_fp8_scales_rules():
+    """Weight scales absmax/448 per output channel (1 for zero channels) in
+    the product and the oracle are the same numbers; activation scales are
+    powers of two covering the margin."""
+    from paper_1809_02697_b200 import quant
+    w = np.random.default_rng(3).standard_normal((8, 4, 3, 3)).astype(np.float32)
+    w[5] = 0
+    assert np.array_equal(quant.weight_scales(w), ops.fp8_weight_scales(w))
+    assert quant.weight_scales(w)[5] == 1.0
+    for a in (1e-3, 0.5, 7.0, 300.0, 448.0, 1e4):
+        s = quant.act_scale(a)
+        assert s == 2.0 ** round(np.log2(s)) and a * quant.CALIB_MARGIN / s <= 448.0
+        assert a * quant.CALIB_MARGIN / s > 224.0
+    assert quant.act_scale(0.0) == 1.0
+
+
+def test_conv2d_fp8_model_is_exact_on_representable_data(rng):
+    """With e4m3 inputs and weights already representable and scales 1, the
+    model's only rounding is the final RN_e4m3 of the f32 epilogue."""
+    x = ops.round_e4m3(rng.standard_normal((1, 8, 6, 6)).astype(np.float32))
+    w = ops.round_e4m3(rng.standard_normal((4, 8, 3, 3)).astype(np.float32))
+    ws = ops.fp8_weight_scales(w)
+    got = ops.conv2d_fp8(x, w, 1.0, None, 1, 1)
+    wq = ops.round_e4m3(w / ws.reshape(-1, 1, 1, 1))
+    want = ops.conv2d(x, wq, 1, 1, ws, None, None, None, False)
+    assert np.array_equal(got, want)
+    assert np.array_equal(ops.conv2d_fp8(x, w, 1.0, 2.0, 1, 1), ops.round_e4m3(want / 2))
