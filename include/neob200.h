@@ -305,6 +305,14 @@ int neo_pool2d_window(int dtype, int mode, const void* in, void* out, int64_t n,
                       int64_t h, int64_t w, int x, int win, int stride, int pad,
                       int64_t in_cb_off, int64_t in_cb_total, int64_t out_cb_off,
                       int64_t out_cb_total, int flags, neo_stream_t stream);
+/* e4m3 pooling with scales (FP8 mode): max or avg (reference order, /win^2)
+ * of the dequantized inputs e4m3(q) * in_scale, stored as
+ * e4m3_rn_satfinite(v / out_scale); windows as neo_pool2d_window; x % 16 == 0.
+ * A max pool with out_scale == in_scale copies the winning bytes. */
+int neo_pool2d_q(int mode, const void* in, void* out, int64_t n, int64_t cb, int64_t h, int64_t w,
+                 int x, int win, int stride, int pad, int64_t in_cb_off, int64_t in_cb_total,
+                 int64_t out_cb_off, int64_t out_cb_total, float in_scale, float out_scale,
+                 neo_stream_t stream);
 /* elementwise ops over (n, cb, hw, x) (x = 1 is NCHW); scale/shift indexed by
  * channel cb*x+lane.  Replaces executor.py:165-190 (ReLU, BatchNorm with
  * _channel_broadcast :96-100, ElementwiseAdd). */
@@ -317,6 +325,13 @@ int neo_eltwise_window(int dtype, int op, const void* a, const void* b, void* ou
                        const float* scale, const float* shift, int64_t n, int64_t cb, int64_t hw,
                        int x, int64_t a_cb_off, int64_t a_cb_total, int64_t out_cb_off,
                        int64_t out_cb_total, int flags, neo_stream_t stream);
+/* e4m3 relu / scale-shift / scale-shift-relu (FP8 mode; BN = a*scale+shift as
+ * two rounded f32 ops on a = e4m3(q) * a_scale), stored as
+ * e4m3_rn_satfinite(v / out_scale); channel-block windows on a and out. */
+int neo_eltwise_q(int op, const void* a, void* out, const float* scale, const float* shift,
+                  int64_t n, int64_t cb, int64_t hw, int x, int64_t a_cb_off, int64_t a_cb_total,
+                  int64_t out_cb_off, int64_t out_cb_total, float a_scale, float out_scale,
+                  neo_stream_t stream);
 /* strided copy for np.concatenate (executor.py:191-193): src viewed as
  * (outer, chunk) elements is copied into dst viewed as (outer, dst_row) at
  * column dst_off.  Concat of k inputs = k calls. */

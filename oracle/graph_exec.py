@@ -128,17 +128,25 @@ def _conv_fp8(n, vals, q8: set, scales: dict, feeds_pool: set):
         weight = ops.unpack_kcrs(weight)
     xs = np.float32(scales[data_id])
     out_scale = n.attrs["fp8_scale"]
-    stored = ops.conv2d_fp8(data / xs, weight, xs, out_scale, n.attrs["stride"], n.attrs["pad"],
-                            epi.get("scale"), epi.get("shift"), bias, residual,
-                            bool(epi.get("relu", False)))
-    out = (stored * np.float32(out_scale)).astype(np.float32)
+    sch = n.attrs.get("schedule") or {}
+    bf16_out = (sch.get("oc_bn") or 16) < 16      # rows under 16 bytes: stored bf16
+    stored = ops.conv2d_fp8(data / xs, weight, xs, None if bf16_out else out_scale,
+                            n.attrs["stride"], n.attrs["pad"], epi.get("scale"), epi.get("shift"),
+                            bias, residual, bool(epi.get("relu", False)))
+    out = ops.round_rn(stored, "bf16") if bf16_out else \
+        (stored * np.float32(out_scale)).astype(np.float32)
     if vals[data_id].ndim == 5:
         sch = n.attrs.get("schedule") or {}
         y = sch.get("oc_bn") or (vals[n.inputs[1][0]].shape[5]
                                  if vals[n.inputs[1][0]].ndim == 6 else 1)
         out = ops.pack_nchw(out, y)
-    return out, True
+    return out, not bf16_out
 
+
+def _q8(a, scale) -> np.ndarray:
+    """Store f32 values as e4m3 at ``scale`` (the dequantized result)."""
+    s8 = np.float32(scale)
+    return (ops.round_e4m3(np.asarray(a, np.float32) / s8) * s8).astype(np.float32)
 
 
 def execute_reference(graph, inputs: dict, arith: str | None = None) -> list[np.ndarray]:
@@ -184,6 +192,9 @@ def _execute(graph, inputs, arith, vals, q8, scales):
             vals[nid] = _conv(n, vals, arith)
         elif k == "ReLU":
             vals[nid] = ops.relu(src[0])
+            if arith == "fp8" and nid in scales:
+                vals[nid] = _q8(vals[nid], scales[nid])       # e4m3 BN-ReLU output
+                q8.add(nid)
         elif k == "Softmax":
             vals[nid] = ops.softmax(src[0])
         elif k == "BatchNorm":
@@ -198,17 +209,17 @@ def _execute(graph, inputs, arith, vals, q8, scales):
         elif k in ("MaxPool", "AvgPool"):
             vals[nid] = ops.pool2d(src[0], n.attrs["window"], n.attrs["stride"],
                                    n.attrs.get("pad", 0), "max" if k == "MaxPool" else "avg")
-            if arith == "fp8" and k == "MaxPool" and n.inputs[0][0] in q8:
-                q8.add(nid)           # max of stored e4m3 values: exact, same scale
-            elif arith == "fp8" and nid in scales and vals[nid].ndim == 5 and k == "MaxPool":
-                # the fused stem's pooled bf16 map stored as e4m3
-                s8 = np.float32(scales[nid])
-                vals[nid] = (ops.round_e4m3(vals[nid] / s8) * s8).astype(np.float32)
+            if arith == "fp8" and nid in scales and vals[nid].ndim == 5:
+                # e4m3 pooled map (a max pool at its input's scale is exact;
+                # the fused stem's pooled bf16 maxima and averages round once)
+                vals[nid] = _q8(vals[nid], scales[nid])
                 q8.add(nid)
         elif k == "ElementwiseAdd":
             vals[nid] = ops.add(src[0], src[1])
         elif k == "Concat":
             vals[nid] = ops.concat(src, n.attrs.get("axis", 1))
+            if arith == "fp8" and all(i in q8 for i, _ in n.inputs):
+                q8.add(nid)           # members share the group's scale: exact
         elif k == "Flatten":
             vals[nid] = ops.flatten(src[0])
         elif k == "Dense":

@@ -127,6 +127,12 @@ SIGNATURES = {
     "neo_pool2d_window": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64,
                                    _c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_i64,
                                    _c_int, _c_vp]),
+    "neo_pool2d_q": (_c_int, [_c_int, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
+                              _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_i64,
+                              ctypes.c_float, ctypes.c_float, _c_vp]),
+    "neo_eltwise_q": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,
+                               _c_int, _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_float,
+                               ctypes.c_float, _c_vp]),
     "neo_eltwise_window": (_c_int, [_c_int, _c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64,
                                     _c_i64, _c_i64, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_int,
                                     _c_vp]),

@@ -1487,8 +1487,11 @@ static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
   const int out_es = (int)neo_dtype_size(p->out_dtype);
   const int y = p->oc_bn;
   const int rowb_out = y * out_es;
-  const bool ok = y % 16 == 0 && (rowb_out == 32 || rowb_out == 64 || rowb_out == 128) &&
-                  tile_n % y == 0 && !getenv("NEOB200_DIRECT_EPILOGUE");
+  // 16-byte rows (unswizzled staging): e4m3 blocks of 16 channels only (the
+  // direct epilogue has no e4m3 store)
+  const bool rows_ok = rowb_out == 32 || rowb_out == 64 || rowb_out == 128 ||
+                       (rowb_out == 16 && p->out_dtype == NEO_FP8);
+  const bool ok = y % 16 == 0 && rows_ok && tile_n % y == 0 && !getenv("NEOB200_DIRECT_EPILOGUE");
   return ok ? rowb_out : 0;
 }
 
@@ -1616,7 +1619,10 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     auto fits = [&]() {
       return 2 * halo_pair_bytes(p, rowb, m_tiles) + staging_of(p->tile_n) <= budget;
     };
-    while (!fits() && auto_tn && p->tile_n > 32) p->tile_n /= 2;
+    // (never below one output channel block: the TMA-store epilogue -- the
+    // only e4m3 store -- needs whole blocks per N tile)
+    const int floor_tn = (p->oc_bn % 16 == 0 && p->oc_bn > 32) ? p->oc_bn : 32;
+    while (!fits() && auto_tn && p->tile_n > floor_tn) p->tile_n /= 2;
     if (!fits() && auto_geom) {
       p->tile_w = g0.BW;
       p->tile_h = g0.BH;

@@ -472,15 +472,38 @@ __global__ void avgpool3s1_bf16(const __nv_bfloat16* __restrict__ in,
   }
 }
 
-// e4m3 max pooling (FP8 mode): 16 lanes per thread; e4m3 -> f16 is exact,
-// max in f16x2 (padding -inf), and the maximum -- one of the stored values --
-// converts back to the same e4m3 byte, so the map keeps its scale
-__global__ void pool_max_fp8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t Cb,
-                             int64_t P, int H, int W, int OH, int OW, int x, int win, int stride,
-                             int pad, Win wnd) {
+// e4m3 pooling (FP8 mode), 16 lanes per thread.  Max: e4m3 -> f16 is exact,
+// the maximum in f16x2 (padding -inf) is one of the stored values; avg: the
+// reference's sum order (first tap, then + each tap r-major, padding +0)
+// of the dequantized values in f32, / win^2 (count_include_pad).  The result
+// times in_scale / out_scale (powers of two: exact) is rounded once to e4m3
+// -- a max pool with out_scale == in_scale returns the winning bytes.
+__device__ __forceinline__ void e4m3x16_to_f32(const uint4& raw, float* v) {
+  const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __nv_fp8x2_storage_t pr = (__nv_fp8x2_storage_t)(w4[k >> 1] >> (16 * (k & 1)));
+    const float2 f = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(pr, __NV_E4M3)));
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ uint4 f32x16_to_e4m3(const float* v) {
+  uint32_t o[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    o[k] = (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(v[4 * k], v[4 * k + 1]), __NV_SATFINITE, __NV_E4M3) |
+           ((uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(v[4 * k + 2], v[4 * k + 3]), __NV_SATFINITE, __NV_E4M3) << 16);
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__global__ void pool_fp8(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t Cb,
+                         int64_t P, int H, int W, int OH, int OW, int x, int win, int stride,
+                         int pad, bool is_max, float in_scale, float qs, Win wnd) {
   neo_pdl_enter();
   const uint32_t groups = x / 16;
   const uint32_t per_plane = (uint32_t)OH * OW * groups;
+  const float inv = (float)(win * win);
   for (int64_t plane = blockIdx.y; plane < P; plane += gridDim.y) {
     const uint8_t* src = in + wnd.in_plane(plane, Cb) * H * W * x;
     uint8_t* dst = out + wnd.out_plane(plane, Cb) * OH * OW * x;
@@ -488,31 +511,66 @@ __global__ void pool_max_fp8(const uint8_t* __restrict__ in, uint8_t* __restrict
          i += gridDim.x * blockDim.x) {
       const uint32_t gq = i % groups, t = i / groups;
       const int ow = (int)(t % (uint32_t)OW), oh = (int)(t / (uint32_t)OW);
-      __half2 m[8];
+      float acc[16];
+      bool first = true;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) m[k] = __half2(__ushort_as_half(0xFC00u), __ushort_as_half(0xFC00u));
+      for (int k = 0; k < 16; ++k) acc[k] = is_max ? -INFINITY : 0.f;
       for (int r = 0; r < win; ++r) {
         const int ih = oh * stride + r - pad;
-        if (ih < 0 || ih >= H) continue;
         for (int q = 0; q < win; ++q) {
           const int iw = ow * stride + q - pad;
-          if (iw < 0 || iw >= W) continue;
-          const uint4 raw = __ldg(reinterpret_cast<const uint4*>(src + ((int64_t)ih * W + iw) * x + gq * 16));
-          const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+          const bool inb = ih >= 0 && ih < H && iw >= 0 && iw < W;
+          if (!inb && is_max) continue;                 // -inf padding
+          float v[16];                                  // avg: +0 padding taps
+          if (inb)
+            e4m3x16_to_f32(__ldg(reinterpret_cast<const uint4*>(src + ((int64_t)ih * W + iw) * x + gq * 16)), v);
+          else
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const __nv_fp8x2_storage_t pr = (__nv_fp8x2_storage_t)(w4[k >> 1] >> (16 * (k & 1)));
-            m[k] = __hmax2(m[k], __half2(__nv_cvt_fp8x2_to_halfraw2(pr, __NV_E4M3)));
+            for (int k = 0; k < 16; ++k) v[k] = 0.f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            if (is_max) acc[k] = fmaxf(acc[k], v[k]);
+            else acc[k] = first ? v[k] * in_scale : __fadd_rn(acc[k], v[k] * in_scale);
           }
+          first = false;
         }
       }
-      uint32_t o[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        o[k] = (uint32_t)__nv_cvt_halfraw2_to_fp8x2(__half2_raw(m[2 * k]), __NV_SATFINITE, __NV_E4M3) |
-               ((uint32_t)__nv_cvt_halfraw2_to_fp8x2(__half2_raw(m[2 * k + 1]), __NV_SATFINITE, __NV_E4M3) << 16);
-      *reinterpret_cast<uint4*>(dst + ((int64_t)oh * OW + ow) * x + gq * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int k = 0; k < 16; ++k)
+        acc[k] = is_max ? acc[k] * in_scale * qs : __fdiv_rn(acc[k], inv) * qs;
+      *reinterpret_cast<uint4*>(dst + ((int64_t)oh * OW + ow) * x + gq * 16) = f32x16_to_e4m3(acc);
     }
+  }
+}
+
+// e4m3 elementwise (FP8 mode): relu / scale-shift(-relu) (BN, executor.py:
+// 174-181, a * scale + shift as two rounded ops) of the dequantized values,
+// then one rounding to e4m3 at the output's scale; 16 lanes per thread
+__global__ void eltwise_fp8(const uint8_t* __restrict__ a, uint8_t* __restrict__ out,
+                            const float* __restrict__ scale, const float* __restrict__ shift,
+                            int64_t Cb, int64_t P, int64_t HW, int x, int op, float a_scale,
+                            float qs, Win wnd) {
+  neo_pdl_enter();
+  const int64_t groups = HW * (x / 16);
+  const int64_t total = P * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t plane = i / groups, g = i % groups;
+    const int lane0 = (int)(g % (x / 16)) * 16;
+    const int64_t cb = plane % Cb;
+    float v[16];
+    e4m3x16_to_f32(__ldg(reinterpret_cast<const uint4*>(a + wnd.in_plane(plane, Cb) * HW * x + g * 16)), v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float y = v[k] * a_scale;
+      if (op == NEO_ELT_SCALE_SHIFT || op == NEO_ELT_SCALE_SHIFT_RELU) {
+        const int64_t ch = cb * x + lane0 + k;
+        y = __fadd_rn(__fmul_rn(y, __ldg(scale + ch)), __ldg(shift + ch));
+      }
+      if (op != NEO_ELT_SCALE_SHIFT) y = fmaxf(y, 0.f);
+      v[k] = y * qs;
+    }
+    *reinterpret_cast<uint4*>(out + wnd.out_plane(plane, Cb) * HW * x + g * 16) = f32x16_to_e4m3(v);
   }
 }
 
@@ -737,14 +795,11 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
   const bool is_max = mode == NEO_POOL_MAX;
   const bool global = OH == 1 && OW == 1 && pad == 0 && win == h && win == w && x % 2 == 0;
   if (dtype == NEO_FP8) {
-    // e4m3 maps: max pooling only (an average would need a new scale)
-    NEO_CHECK_ARG(is_max, NEO_ERR_UNSUPPORTED, "e4m3 pooling is max pooling only");
-    NEO_CHECK_ARG(x % 16 == 0 && al, NEO_ERR_UNSUPPORTED, "e4m3 pooling needs 16-lane blocks");
-    neo_launch(pool_max_fp8, plane_grid(P, (int64_t)OH * OW * (x / 16)), 256, 0, st,
-               static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), cb, P, (int)h, (int)w,
-               (int)OH, (int)OW, x, win, stride, pad, wnd);
-    NEO_LAUNCH_CHECK();
-    return NEO_OK;
+    // e4m3 maps without scales: max pooling (the map keeps its scale); an
+    // average needs neo_pool2d_q's output scale
+    NEO_CHECK_ARG(is_max, NEO_ERR_UNSUPPORTED, "e4m3 average pooling needs neo_pool2d_q");
+    return neo_pool2d_q(mode, in, out, n, cb, h, w, x, win, stride, pad, in_cb_off, in_cb_total,
+                        out_cb_off, out_cb_total, 1.f, 1.f, stream);
   }
   if (global) {
     const float inv = (float)(win * win);
@@ -801,6 +856,57 @@ extern "C" int neo_pool2d_window(int dtype, int mode, const void* in, void* out,
     neo_launch(pool_kernel<float>, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const float*>(in), static_cast<float*>(out), n, cb, (int)h, (int)w, (int)OH,
         (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, round, wnd);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_pool2d_q(int mode, const void* in, void* out, int64_t n, int64_t cb, int64_t h,
+                            int64_t w, int x, int win, int stride, int pad, int64_t in_cb_off,
+                            int64_t in_cb_total, int64_t out_cb_off, int64_t out_cb_total,
+                            float in_scale, float out_scale, neo_stream_t stream) {
+  NEO_CHECK_ARG(in && out && in_scale > 0.f && out_scale > 0.f, NEO_ERR_INVALID_ARG,
+                "bad e4m3 pool arguments");
+  NEO_CHECK_ARG(win >= 1 && stride >= 1 && pad >= 0 && pad < win, NEO_ERR_INVALID_ARG,
+                "bad pool window/stride/pad");
+  NEO_CHECK_ARG(in_cb_off >= 0 && in_cb_off + cb <= in_cb_total && out_cb_off >= 0 &&
+                    out_cb_off + cb <= out_cb_total,
+                NEO_ERR_SHAPE_MISMATCH, "channel-block window out of range");
+  NEO_CHECK_ARG(x % 16 == 0 && aligned16(in) && aligned16(out), NEO_ERR_UNSUPPORTED,
+                "e4m3 pooling needs 16-lane blocks");
+  const int64_t OH = (h + 2 * pad - win) / stride + 1, OW = (w + 2 * pad - win) / stride + 1;
+  NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "pool has empty output");
+  const Win wnd{in_cb_off, in_cb_total, out_cb_off, out_cb_total};
+  const int64_t P = n * cb;
+  neo_launch(pool_fp8, plane_grid(P, OH * OW * (x / 16)), 256, 0, static_cast<cudaStream_t>(stream),
+             static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out), cb, P, (int)h, (int)w,
+             (int)OH, (int)OW, x, win, stride, pad, mode == NEO_POOL_MAX, in_scale,
+             (float)(1.0 / (double)out_scale), wnd);
+  NEO_LAUNCH_CHECK();
+  return NEO_OK;
+}
+
+extern "C" int neo_eltwise_q(int op, const void* a, void* out, const float* scale,
+                             const float* shift, int64_t n, int64_t cb, int64_t hw, int x,
+                             int64_t a_cb_off, int64_t a_cb_total, int64_t out_cb_off,
+                             int64_t out_cb_total, float a_scale, float out_scale,
+                             neo_stream_t stream) {
+  NEO_CHECK_ARG(a && out && a_scale > 0.f && out_scale > 0.f, NEO_ERR_INVALID_ARG,
+                "bad e4m3 eltwise arguments");
+  NEO_CHECK_ARG(op == NEO_ELT_RELU || op == NEO_ELT_SCALE_SHIFT || op == NEO_ELT_SCALE_SHIFT_RELU,
+                NEO_ERR_UNSUPPORTED, "e4m3 eltwise: relu / scale-shift(-relu) only (op %d)", op);
+  NEO_CHECK_ARG(op == NEO_ELT_RELU || (scale && shift), NEO_ERR_INVALID_ARG,
+                "scale/shift needs both vectors");
+  NEO_CHECK_ARG(a_cb_off >= 0 && a_cb_off + cb <= a_cb_total && out_cb_off >= 0 &&
+                    out_cb_off + cb <= out_cb_total,
+                NEO_ERR_SHAPE_MISMATCH, "channel-block window out of range");
+  NEO_CHECK_ARG(x % 16 == 0 && aligned16(a) && aligned16(out), NEO_ERR_UNSUPPORTED,
+                "e4m3 eltwise needs 16-lane blocks");
+  const Win wnd{a_cb_off, a_cb_total, out_cb_off, out_cb_total};
+  const int64_t P = n * cb;
+  neo_launch(eltwise_fp8, (unsigned)grid_for(P * hw * (x / 16)), 256, 0,
+             static_cast<cudaStream_t>(stream), static_cast<const uint8_t*>(a),
+             static_cast<uint8_t*>(out), scale, shift, cb, P, hw, x, op, a_scale,
+             (float)(1.0 / (double)out_scale), wnd);
   NEO_LAUNCH_CHECK();
   return NEO_OK;
 }
@@ -881,6 +987,10 @@ extern "C" int neo_concat_copy(int dtype, const void* src, void* dst, int64_t ou
     neo_launch(concat_kernel_v4, (unsigned)grid_for(total), 256, 0, st, 
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), outer, chunk / per,
         dst_row / per, dst_off / per);
+  } else if (es == 1) {
+    neo_launch(concat_kernel<uint8_t>, (unsigned)grid_for(outer * chunk), 256, 0, st,
+        static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), outer, chunk, dst_row,
+        dst_off);
   } else if (es == 2) {
     neo_launch(concat_kernel<uint16_t>, (unsigned)grid_for(outer * chunk), 256, 0, st, 
         static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), outer, chunk, dst_row,

@@ -206,6 +206,22 @@ def pool2d_window(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, in_win,
            out_win[0], out_win[1], flags, stream_handle(stream))
 
 
+def pool2d_q(inp, out, n, cb, h, w, x, win, stride, pad, mode: str, in_win, out_win,
+             in_scale: float, out_scale: float, stream=None):
+    """e4m3 pooling with requantization (neo_pool2d_q)."""
+    L.call("neo_pool2d_q", L.POOL_MAX if mode == "max" else L.POOL_AVG, _ptr(inp), _ptr(out), n,
+           cb, h, w, x, win, stride, pad, in_win[0], in_win[1], out_win[0], out_win[1],
+           float(in_scale), float(out_scale), stream_handle(stream))
+
+
+def eltwise_q(op: int, a, out, n, cb, hw, x, a_win, out_win, a_scale: float, out_scale: float,
+              scale=None, shift=None, stream=None):
+    """e4m3 relu / scale-shift(-relu) with requantization (neo_eltwise_q)."""
+    L.call("neo_eltwise_q", op, _ptr(a), _ptr(out), _ptr(scale), _ptr(shift), n, cb, hw, x,
+           a_win[0], a_win[1], out_win[0], out_win[1], float(a_scale), float(out_scale),
+           stream_handle(stream))
+
+
 def eltwise_window(op: int, a, out, n, cb, hw, x, a_win, out_win, scale=None, shift=None,
                    flags=0, stream=None):
     L.call("neo_eltwise_window", dtype_code(a), op, _ptr(a), None, _ptr(out), _ptr(scale),

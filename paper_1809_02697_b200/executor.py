@@ -721,7 +721,12 @@ class DeviceProgram:
                 shape = (n, -(-c // px), h, w, px)
             else:
                 shape = spec.shape
-            return _Val(nid, tuple(shape), self.act_dtype, layout, px=px)
+            dtype = self.act_dtype
+            if self.mode == "fp8" and px < 16:
+                # an e4m3 row under 16 bytes has no TMA store: such maps (the
+                # SSD heads' 2-8 channel blocks) are kept in bf16
+                dtype = torch.bfloat16
+            return _Val(nid, tuple(shape), dtype, layout, px=px)
         dtype = self.dense_dtype if self._feeds_tc_dense(nid) else torch.float32
         return _Val(nid, tuple(spec.shape), dtype, layout)
 
@@ -1118,9 +1123,13 @@ class DeviceProgram:
         return {"bf16": L.MODE_BF16, "tf32": L.MODE_TF32, "fp8": L.MODE_FP8}[self.mode]
 
     def _scale_of(self, nid: int) -> float:
-        """e4m3 scale of the map node ``nid`` stores (fp8 mode)."""
+        """e4m3 scale of the map node ``nid`` stores (fp8 mode); a concat
+        window stores at its buffer's scale (quant.attach_scales gives every
+        member of a concat group the group's scale)."""
         v = self._storage(nid)
         key = v.nid if v is not None else nid
+        if v is not None and v.win is not None:
+            key = v.win[0]
         if key not in self.qscale:
             raise InputMismatch(f"fp8 mode: node {key} has no e4m3 scale (compile the graph "
                                 f"with compile_graph(..., mode='fp8'))")
@@ -1275,17 +1284,23 @@ class DeviceProgram:
 
     def _bind_pool(self, node, src: _Val, out: _Val):
         import torch
-        if src.tensor.dtype == torch.float8_e4m3fn:
-            # e4m3 max pooling keeps the map's scale (quant.attach_scales gives
-            # the pool its input's scale); an average would need a new one
-            if node.kind != OpKind.MaxPool or out.tensor.dtype != torch.float8_e4m3fn:
-                self._no_fp8("average pooling", src.tensor)
-            if self._scale_of(node.id) != self._scale_of(node.inputs[0][0]):
-                raise InputMismatch(f"fp8 max pool {node.id}: output scale must equal the "
-                                    f"input's")
-        else:
-            self._no_fp8("pooling", src.tensor, out.tensor)
         from . import device as D
+        if src.tensor.dtype == torch.float8_e4m3fn:
+            # e4m3 pooling: dequantize, pool (max / reference-order average),
+            # requantize at the output's scale (a max pool that keeps its
+            # input's scale copies the winning bytes)
+            if out.tensor.dtype != torch.float8_e4m3fn:
+                self._no_fp8("pooling into a non-e4m3 map", src.tensor)
+            n, cb, h, w, x = self._geom(src)
+            mode = "max" if node.kind == OpKind.MaxPool else "avg"
+            win, st, pad = node.attrs["window"], node.attrs["stride"], node.attrs.get("pad", 0)
+            s_t, d_t, iw, ow = src.tensor, out.tensor, self._window(src), self._window(out)
+            si, so = self._scale_of(src.nid), self._scale_of(node.id)
+            self._emit(f"{mode}pool{node.id}", lambda: D.pool2d_q(
+                s_t, d_t, n, cb, h, w, x, win, st, pad, mode, iw, ow, si, so, self.stream),
+                _vb(src) + _vb(out))
+            return
+        self._no_fp8("pooling", src.tensor, out.tensor)
         n, cb, h, w, x = self._geom(src)
         mode = "max" if node.kind == OpKind.MaxPool else "avg"
         win, st, pad = node.attrs["window"], node.attrs["stride"], node.attrs.get("pad", 0)
@@ -1301,8 +1316,18 @@ class DeviceProgram:
             s_t, d_t, n, cb, h, w, x, win, st, pad, mode, flags, self.stream), nb)
 
     def _bind_eltwise(self, op, a: _Val, b: _Val | None, out: _Val):
-        self._no_fp8("elementwise op", a.tensor, b.tensor if b is not None else None, out.tensor)
+        import torch
         from . import device as D
+        if a.tensor.dtype == torch.float8_e4m3fn and b is None and op == D_ELT_RELU \
+                and out.tensor.dtype == torch.float8_e4m3fn:
+            n, cb, h, w, x = self._geom(a)
+            a_t, o_t, aw, ow = a.tensor, out.tensor, self._window(a), self._window(out)
+            sa, so = self._scale_of(a.nid), self._scale_of(out.nid)
+            self._emit(f"relu{out.nid}", lambda: D.eltwise_q(
+                D_ELT_RELU, a_t, o_t, n, cb, h * w, x, aw, ow, sa, so, stream=self.stream),
+                _vb(a) + _vb(out))
+            return
+        self._no_fp8("elementwise op", a.tensor, b.tensor if b is not None else None, out.tensor)
         n, cb, h, w, x = self._geom(a)
         flags = self.round_flag if a.layout.tag == "NCHWc" else 0
         a_t, b_t, o_t = a.tensor, (b.tensor if b is not None else None), out.tensor
@@ -1329,13 +1354,23 @@ class DeviceProgram:
         return np.asarray(scale, np.float32), np.asarray(shift, np.float32)
 
     def _bind_scale_shift(self, node, src: _Val, out: _Val, relu: bool):
-        self._no_fp8("batch norm", src.tensor, out.tensor)
+        import torch
         from . import device as D
         from . import _lib as L
         scale, shift = self._bn_scale_shift(node)
         t_scale, t_shift = self._upload(scale), self._upload(shift)
         n, cb, h, w, x = self._geom(src)
         op = L.ELT_SCALE_SHIFT_RELU if relu else L.ELT_SCALE_SHIFT
+        if src.tensor.dtype == torch.float8_e4m3fn and out.tensor.dtype == torch.float8_e4m3fn:
+            # e4m3 BN(-ReLU), e.g. DenseNet's pre-activations over a concat
+            # window: dequantize, a*scale+shift, relu, requantize
+            a_t, o_t, aw, ow = src.tensor, out.tensor, self._window(src), self._window(out)
+            sa, so = self._scale_of(src.nid), self._scale_of(out.nid)
+            self._emit(f"bn{node.id}{'_relu' if relu else ''}", lambda: D.eltwise_q(
+                op, a_t, o_t, n, cb, h * w, x, aw, ow, sa, so, t_scale, t_shift, self.stream),
+                _vb(src) + _vb(out))
+            return
+        self._no_fp8("batch norm", src.tensor, out.tensor)
         flags = self.round_flag if src.layout.tag == "NCHWc" else 0
         a_t, o_t = src.tensor, out.tensor
         nb = _vb(src) + _vb(out)
@@ -1348,8 +1383,15 @@ class DeviceProgram:
             op, a_t, None, o_t, n, cb, h * w, x, t_scale, t_shift, flags, self.stream), nb)
 
     def _bind_concat(self, node, ins, out: _Val):
-        self._no_fp8("concat", out.tensor, *[v.tensor for v in ins if v is not None])
+        import torch
         from . import device as D
+        if out.tensor.dtype == torch.float8_e4m3fn:
+            # e4m3 concat: every input is stored at the concat group's scale
+            # (quant.attach_scales), so copies are byte copies
+            so = self._scale_of(node.id)
+            for (src, _), v in zip(node.inputs, ins):
+                if self._scale_of(src) != so:
+                    raise InputMismatch(f"fp8 concat {node.id}: input {src} has another scale")
         axis = node.attrs.get("axis", 1)
         done = self.concat_windowed.get(node.id, set())
         dst = out
@@ -1452,8 +1494,14 @@ class DeviceProgram:
         return [v.tensor for v in self.out_vals]
 
     def _launch_all(self):
-        for fn in self.launches:
-            fn()
+        for i, fn in enumerate(self.launches):
+            try:
+                fn()
+            except Exception as exc:
+                # name the launch ("conv123", "bn45_relu", ...) in the error
+                exc.args = (f"{self.launch_names[i]} [{self.launch_desc[i]}]: "
+                            f"{exc.args[0] if exc.args else exc}",) + tuple(exc.args[1:])
+                raise
 
     def launch(self):
         """Run the forward on ``self.stream`` (inputs already in place)."""

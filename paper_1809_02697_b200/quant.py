@@ -48,11 +48,28 @@ def act_scale(absmax: float, margin: float = CALIB_MARGIN) -> float:
     return float(2.0 ** math.ceil(math.log2(a / E4M3_MAX)))
 
 
+def _global_pool(g: Graph, nid: int) -> bool:
+    """A global average pool the fused classifier head absorbs (C % 256 ==
+    0, executor._fused_head_info): the head pools the e4m3 map at its
+    input's scale, so the pool itself stores nothing and needs no scale."""
+    from .graph import hw_pair, infer_shapes
+    n = g.nodes[nid]
+    if n.kind != OpKind.AvgPool:
+        return False
+    spec = infer_shapes(g)[n.inputs[0][0]]
+    _, c, h, w = spec.logical_nchw
+    return (hw_pair(n.attrs["window"]) == (h, w) and hw_pair(n.attrs.get("pad", 0)) == (0, 0)
+            and c % 256 == 0)
+
+
 def quantized_nodes(g: Graph) -> list[int]:
-    """Nodes whose outputs an fp8 program may store as e4m3 maps: convs and
-    pools (the fused stem's output is its max pool)."""
+    """Nodes whose outputs an fp8 program may store as e4m3 maps: convs,
+    pools (the fused stem's output is its max pool; global average pools
+    feed the classifier head, which reads its input map's scale) and ReLUs
+    (DenseNet's BN-ReLU pre-activations)."""
     return [nid for nid, n in g.nodes.items()
-            if n.kind in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool)]
+            if n.kind in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool, OpKind.ReLU)
+            and not _global_pool(g, nid)]
 
 
 def calibrate(g: Graph, feeds: dict | None = None, batch: int = 4, device: int = 0,
@@ -93,20 +110,51 @@ def calibrate(g: Graph, feeds: dict | None = None, batch: int = 4, device: int =
 
 
 def attach_scales(g: Graph, scales: dict[int, float]) -> Graph:
-    """Store the scales as ``fp8_scale`` attrs of the compiled graph's conv
-    and pool nodes (in place).  A max pool inherits its input's scale: its
-    outputs are a subset of its inputs' stored values, so the e4m3 bytes
-    carry over unchanged."""
+    """Store the scales as ``fp8_scale`` attrs of the compiled graph's conv,
+    pool and ReLU nodes (in place).
+
+    * A max pool inherits its input's scale: its outputs are a subset of its
+      inputs' stored values, so the e4m3 bytes carry over unchanged.
+    * Channel concats are done in place (producers write windows of one
+      buffer), so a concat and all its inputs -- transitively, through nested
+      concats -- form one group stored at one scale: the largest of the
+      members' calibrated scales (a power of two covering every member)."""
     from .graph import topo_sort
+    quant = set(quantized_nodes(g))
     for nid in topo_sort(g):
         node = g.nodes[nid]
-        if node.kind not in (OpKind.Conv2d, OpKind.MaxPool, OpKind.AvgPool):
+        if nid not in quant:
             continue
         src = node.inputs[0][0] if node.inputs else None
         if node.kind == OpKind.MaxPool and src is not None and "fp8_scale" in g.nodes[src].attrs:
             node.attrs["fp8_scale"] = g.nodes[src].attrs["fp8_scale"]
         elif nid in scales:
             node.attrs["fp8_scale"] = float(scales[nid])
+    parent: dict[int, int] = {}
+
+    def find(a: int) -> int:
+        parent.setdefault(a, a)
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    concats = [nid for nid, n in g.nodes.items()
+               if n.kind == OpKind.Concat and n.attrs.get("axis", 1) == 1]
+    for c in concats:
+        for src, _ in g.nodes[c].inputs:
+            parent[find(src)] = find(c)
+    groups: dict[int, list[int]] = {}
+    for m in list(parent):
+        groups.setdefault(find(m), []).append(m)
+    for members in groups.values():
+        sc = [g.nodes[m].attrs["fp8_scale"] for m in members if "fp8_scale" in g.nodes[m].attrs]
+        if not sc:
+            continue
+        top = max(sc)
+        for m in members:
+            if m in quant or g.nodes[m].kind == OpKind.Concat:
+                g.nodes[m].attrs["fp8_scale"] = top
     return g
 
 

@@ -14,13 +14,19 @@ from oracle.ops import unpack_nchw
 
 def main():
     model = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
+    batch = 1 if model.startswith("ssd") else 2
     image = int(sys.argv[2]) if len(sys.argv) > 2 else 64
     from paper_1809_02697_b200 import (DeviceProgram, ExecutablePlan, build_model, compile_graph,
                                        model_input)
     from paper_1809_02697_b200.graph import OpKind, topo_sort
-    g = build_model(model, batch=2, image=image, softmax=False)
+    g = build_model(model, batch=batch, image=image, **({} if model.startswith("ssd") else {"softmax": False}))
     cg = compile_graph(g, mode="fp8")
-    ids = [nid for nid in topo_sort(cg) if cg.nodes[nid].kind in (OpKind.Conv2d, OpKind.MaxPool)]
+    users = cg.consumers()
+    # (a conv feeding only a max pool is the fused image stem: keeping it
+    # would unfuse the stem and change the program)
+    ids = [nid for nid in topo_sort(cg) if cg.nodes[nid].kind in (OpKind.Conv2d, OpKind.MaxPool)
+           and not (cg.nodes[nid].kind == OpKind.Conv2d and users.get(nid)
+                    and all(cg.nodes[u].kind == OpKind.MaxPool for u in users[nid]))]
     prog = DeviceProgram(ExecutablePlan.compile(cg), 0, "fp8", keep=ids)
     feeds = model_input(g)
     outs = prog.run(feeds)
