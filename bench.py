@@ -495,8 +495,21 @@ def main():
             fcg = compile_graph(g, mode="fp8", db=db)
             tuned_f8 = db is not None and tuned_assignment(g, db, "fp8") is not None
             calib_s = time.time() - t_c
-            fprog = DeviceProgram(ExecutablePlan.compile(fcg), local, "fp8")
+            fprog = DeviceProgram(ExecutablePlan.compile(fcg), local, "fp8",
+                                  host_round=upload == "bf16")
             t_s = time_program(fprog, feeds, args.steps, args.warmup, flush)
+            # end to end through the same public API as the bf16 e2e
+            fo = fprog.output_tensors()[0]
+            fouts = [torch.empty(fo.shape, dtype=fo.dtype).pin_memory()
+                     for _ in range(args.steps + args.warmup)]
+            fprog.pipeline(rot(args.warmup), fouts[:args.warmup])
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(fprog._copy_stream)
+            fprog.pipeline(rot(args.steps), fouts[args.warmup:])
+            f1.record(fprog.stream)
+            f1.synchronize()
+            f_e2e_s = f0.elapsed_time(f1) * 1e-3
             pk8 = f8_peak if f8_peak else 2.0 * float(pk.get("bf16_tflops", 1643.1))
             froof, _ = conv_roofline(fprog, 3, flops_step, pk, pk_kind, flush=flush,
                                      peak_tflops=pk8,
@@ -504,6 +517,9 @@ def main():
                                      else "fp8 = 2 x bf16 burst (no fp8 GEMM to measure)")
             fp8 = {"value": args.batch * args.steps / t_s, "unit": "images/s",
                    "ms_per_step": 1e3 * t_s / args.steps,
+                   "e2e": {"value": args.batch * args.steps / f_e2e_s, "unit": "images/s",
+                           "h2d_bytes_per_step": fprog.upload_bytes(),
+                           "d2h_bytes_per_step": int(fo.numel() * fo.element_size())},
                    "quantization": "e4m3 activations (static power-of-two per-tensor scales, "
                                    "bf16 calibration forward on 4 seeded images) x e4m3 weights "
                                    "(per-output-channel absmax/448); fp32 accumulation",
