@@ -518,7 +518,7 @@ def main():
             fp8 = {"value": args.batch * args.steps / t_s, "unit": "images/s",
                    "ms_per_step": 1e3 * t_s / args.steps,
                    "e2e": {"value": args.batch * args.steps / f_e2e_s, "unit": "images/s",
-                           "h2d_bytes_per_step": fprog.upload_bytes(),
+                           "h2d_bytes_per_step": int(fprog.upload_bytes),
                            "d2h_bytes_per_step": int(fo.numel() * fo.element_size())},
                    "quantization": "e4m3 activations (static power-of-two per-tensor scales, "
                                    "bf16 calibration forward on 4 seeded images) x e4m3 weights "
