@@ -163,6 +163,14 @@ class DeviceProgram:
         self.weights: list = []         # device tensors kept alive
         self._pinned_inputs: dict = {}  # input id -> (pinned staging, upload-done event)
         self.graph_exec = None
+        # serving input slots: slot 0 is each input's own buffer, slot 1 an
+        # alternate buffer pipeline() uploads into while slot 0 is read;
+        # launches reading a graph input resolve it at launch time, and one
+        # CUDA graph is captured per slot (no device-side staging copy)
+        self._input_slot = 0
+        self._alt_inputs: dict = {}
+        self._graphs: dict = {}
+        self.input_readers: dict = {}   # input nid -> launch names reading it
         self.use_graph = use_graph and not os.environ.get("NEOB200_NO_GRAPH")
         self.host_round = (os.environ.get("NEOB200_HOST_ROUND", "1") != "0") if host_round is None \
             else bool(host_round)
@@ -1201,13 +1209,14 @@ class DeviceProgram:
         y = out.layout.x
         cb = self._window(out)
         relu = bool(epi.get("relu"))
+        self.input_readers.setdefault(src_id, []).append("stem")
         kr, ks = w.shape[2], w.shape[3]
         fl, _, desc = self._conv_work(n, c, h, wd, w.shape[0], kr, ks,
                                       hw_pair(node.attrs["stride"]), hw_pair(node.attrs["pad"]), 2)
         qs = self._scale_of(pool_node.id) if self.mode == "fp8" else 1.0
         self._emit(f"stem{cv_id}_pool{pool_node.id}", lambda: D.stem_conv_pool(
-            x_t, wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias, relu, cb, self.stream,
-            out_scale=qs),
+            self._input_of(src_id, x_t), wimg, o_t, n, c, h, wd, y, t_scale, t_shift, t_bias,
+            relu, cb, self.stream, out_scale=qs),
             _nb(x_t) + _vb(out) + _nb(wimg), fl, desc + " + maxpool 3x3/2")
 
     def _bind_head(self, info: dict, out: _Val):
@@ -1493,6 +1502,13 @@ class DeviceProgram:
     def output_tensors(self) -> list:
         return [v.tensor for v in self.out_vals]
 
+    def _input_of(self, nid: int, default):
+        """The buffer a launch reads graph input ``nid`` from in the active
+        input slot (resolved when the launch is issued or captured)."""
+        if self._input_slot:
+            return self._alt_inputs[nid]
+        return default
+
     def _launch_all(self):
         for i, fn in enumerate(self.launches):
             try:
@@ -1507,14 +1523,16 @@ class DeviceProgram:
         """Run the forward on ``self.stream`` (inputs already in place)."""
         import torch
         from . import device as D
-        if self.use_graph and self.graph_exec is None:
+        if self.use_graph and self._graphs.get(self._input_slot) is None:
             with torch.cuda.device(self.device):
                 self._launch_all()                 # warm-up: sets kernel attributes
                 self.stream.synchronize()
                 with torch.cuda.stream(self.stream):
-                    self.graph_exec = D.capture(self._launch_all, self.stream)
-        if self.graph_exec is not None:
-            self.graph_exec.launch(self.stream)
+                    self._graphs[self._input_slot] = D.capture(self._launch_all, self.stream)
+            if self._input_slot == 0:
+                self.graph_exec = self._graphs[0]
+        if self.use_graph:
+            self._graphs[self._input_slot].launch(self.stream)
         else:
             with torch.cuda.device(self.device):
                 self._launch_all()
@@ -1588,7 +1606,7 @@ class DeviceProgram:
 
     def pipeline(self, batches, outputs):
         """Serving loop over pinned host batches: the upload of batch i+1 (a
-        separate copy stream into a double-buffered device staging area)
+        separate copy stream into the other of two device input buffers)
         overlaps the forward of batch i; each forward's first-output tensor
         is read back into ``outputs[i]`` (pinned host tensors).  Every copy
         is part of the loop; returns after all work is enqueued.  Inputs must
@@ -1596,19 +1614,37 @@ class DeviceProgram:
         stored as bf16 (read only by fused stems), each batch is rounded to
         bf16 on the host into a pinned buffer before its upload.
 
-        ``upload_bytes`` is the host->device byte count per batch."""
+        When the input is read only by fused stems (which resolve their input
+        buffer at launch time), the two input buffers are the graph's own
+        inputs -- one captured CUDA graph per buffer -- so no device-side
+        staging copy runs; the result is copied to a small device staging
+        buffer on the compute stream and read back on a third stream, off the
+        forward's critical path.  ``upload_bytes`` is the host->device byte
+        count per batch."""
         import torch
         if len(self.plan.input_ids) != 1:
             raise InputMismatch("pipeline() needs a single-input graph")
-        dst = self.vals[self.plan.input_ids[0]].tensor
+        in_id = self.plan.input_ids[0]
+        dst = self.vals[in_id].tensor
+        zero_copy = (self.use_graph and bool(self.input_readers.get(in_id))
+                     and all(u in self.skip for u in self.users[in_id]))
         if not hasattr(self, "_staging"):
-            self._staging = [torch.empty_like(dst) for _ in range(2)]
+            if zero_copy:
+                self._alt_inputs[in_id] = torch.empty_like(dst)
+                self._staging = [dst, self._alt_inputs[in_id]]
+            else:
+                self._staging = [torch.empty_like(dst) for _ in range(2)]
             self._copy_stream = torch.cuda.Stream(self.device)
+            self._d2h_stream = torch.cuda.Stream(self.device)
             self._copied = [torch.cuda.Event() for _ in range(2)]
             self._consumed = [torch.cuda.Event() for _ in range(2)]
-            for ev in self._consumed:
+            self._out_ready = [torch.cuda.Event() for _ in range(2)]
+            self._out_read = [torch.cuda.Event() for _ in range(2)]
+            for ev in self._consumed + self._out_read:
                 ev.record(self.stream)
         out_dev = self.output_tensors()[0]
+        if not hasattr(self, "_out_stage"):
+            self._out_stage = [torch.empty_like(out_dev) for _ in range(2)]
         convert = dst.dtype != torch.float32
         if convert and not hasattr(self, "_host_stage"):
             # f32 host batch -> pinned bf16 (RN, multi-threaded on the host)
@@ -1626,12 +1662,13 @@ class DeviceProgram:
         gc_was = gc.isenabled()
         gc.disable()
         try:
-            self._pipeline_loop(batches, outputs, dst, out_dev, convert, chunks)
+            self._pipeline_loop(batches, outputs, dst, out_dev, convert, chunks, zero_copy)
         finally:
+            self._input_slot = 0
             if gc_was:
                 gc.enable()
 
-    def _pipeline_loop(self, batches, outputs, dst, out_dev, convert, chunks):
+    def _pipeline_loop(self, batches, outputs, dst, out_dev, convert, chunks, zero_copy):
         import torch
         for i, host in enumerate(batches):
             slot = i & 1
@@ -1657,11 +1694,22 @@ class DeviceProgram:
                 self._copied[slot].record(self._copy_stream)
             with torch.cuda.stream(self.stream):
                 self.stream.wait_event(self._copied[slot])
-                dst.copy_(self._staging[slot], non_blocking=True)
-                self._consumed[slot].record(self.stream)
+                if zero_copy:
+                    self._input_slot = slot            # the graph reading this buffer
+                else:
+                    dst.copy_(self._staging[slot], non_blocking=True)
             self.launch()
             with torch.cuda.stream(self.stream):
-                outputs[i].copy_(out_dev, non_blocking=True)
+                self._consumed[slot].record(self.stream)
+                # result -> small device stage (its previous readback done),
+                # read back on the third stream while the next forward runs
+                self.stream.wait_event(self._out_read[slot])
+                self._out_stage[slot].copy_(out_dev, non_blocking=True)
+                self._out_ready[slot].record(self.stream)
+            with torch.cuda.stream(self._d2h_stream):
+                self._d2h_stream.wait_event(self._out_ready[slot])
+                outputs[i].copy_(self._out_stage[slot], non_blocking=True)
+                self._out_read[slot].record(self._d2h_stream)
 
 
 # ---------------------------------------------------------------------------
