@@ -967,42 +967,61 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           if (sl >= p.nslices) continue;              // padding slice: zeros x zero weights
           const int cbase = (sl % p.Cb) * (p.rowb / (TF32 ? 4 : 2));
           uint8_t* slice = a_gen + g * p.a_sub;
+          if constexpr (!TF32) {
+            // bf16: a thread always rewrites the same 16-byte chunk column
+            // of the slice (256 threads, chunks_row | 256), so its 8
+            // channels' scale / shift are loaded once per slice; multiply
+            // and add as the reference's two rounded ops (executor.py:
+            // 180-181), relu, one bf16 conversion per pair -- the rewrite
+            // must keep pace with the MMAs
+            const int ch = ptid & (chunks_row - 1);
+            const int c0 = cbase + ch * 8;
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0 + 4));
+            const float4 t0 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
+            const float4 t1 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0 + 4));
+            const float2 sc2[4] = {make_float2(s0.x, s0.y), make_float2(s0.z, s0.w),
+                                   make_float2(s1.x, s1.y), make_float2(s1.z, s1.w)};
+            const float2 sh2[4] = {make_float2(t0.x, t0.y), make_float2(t0.z, t0.w),
+                                   make_float2(t1.x, t1.y), make_float2(t1.z, t1.w)};
+            const int row_step = (kProWarps * 32) / chunks_row;
+            for (int row = ptid / chunks_row; row < kTileM; row += row_step) {
+              uint4* ptr = reinterpret_cast<uint4*>(slice + swz_offset(row, ch, p.rowb));
+              uint4 v = *ptr;
+              uint32_t* h = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x2 = make_float2(__uint_as_float(h[e] << 16),
+                                              __uint_as_float(h[e] & 0xFFFF0000u));
+                // scalar _rn ops: nvcc contracts __fmul2_rn + __fadd2_rn into
+                // one FFMA2 (one rounding), which would break the reference's
+                // two-rounding BN and the bit-identity with the unfused path
+                float2 y2 = make_float2(__fadd_rn(__fmul_rn(x2.x, sc2[e].x), sh2[e].x),
+                                        __fadd_rn(__fmul_rn(x2.y, sc2[e].y), sh2[e].y));
+                if (p.pro_relu) {          // fmaxf like the unfused BN-ReLU (bit-identical)
+                  y2.x = fmaxf(y2.x, 0.f);
+                  y2.y = fmaxf(y2.y, 0.f);
+                }
+                asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h[e]) : "f"(y2.x), "f"(y2.y));
+              }
+              *ptr = v;
+            }
+            continue;
+          }
           for (int idx = ptid; idx < per_slice; idx += kProWarps * 32) {
             const int row = idx / chunks_row, ch = idx - row * chunks_row;
             uint4* ptr = reinterpret_cast<uint4*>(slice + swz_offset(row, ch, p.rowb));
             uint4 v = *ptr;
-            if constexpr (TF32) {
-              float* f = reinterpret_cast<float*>(&v);
-              const int c0 = cbase + ch * 4;
-              const float4 sc = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
-              const float4 sh = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
-              const float scv[4] = {sc.x, sc.y, sc.z, sc.w}, shv[4] = {sh.x, sh.y, sh.z, sh.w};
+            float* f = reinterpret_cast<float*>(&v);
+            const int c0 = cbase + ch * 4;
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
+            const float4 sh = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
+            const float scv[4] = {sc.x, sc.y, sc.z, sc.w}, shv[4] = {sh.x, sh.y, sh.z, sh.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float y = __fadd_rn(__fmul_rn(f[e], scv[e]), shv[e]);
-                if (p.pro_relu) y = fmaxf(y, 0.f);
-                f[e] = neo_round_tf32(y);
-              }
-            } else {
-              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
-              const int c0 = cbase + ch * 8;
-              const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0));
-              const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.pro_scale + c0 + 4));
-              const float4 t0 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0));
-              const float4 t1 = __ldg(reinterpret_cast<const float4*>(p.pro_shift + c0 + 4));
-              const float scv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-              const float shv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 x2 = __bfloat1622float2(h[e]);
-                float a = __fadd_rn(__fmul_rn(x2.x, scv[2 * e]), shv[2 * e]);
-                float b = __fadd_rn(__fmul_rn(x2.y, scv[2 * e + 1]), shv[2 * e + 1]);
-                if (p.pro_relu) {
-                  a = fmaxf(a, 0.f);
-                  b = fmaxf(b, 0.f);
-                }
-                h[e] = __floats2bfloat162_rn(a, b);
-              }
+            for (int e = 0; e < 4; ++e) {
+              float y = __fadd_rn(__fmul_rn(f[e], scv[e]), shv[e]);
+              if (p.pro_relu) y = fmaxf(y, 0.f);
+              f[e] = neo_round_tf32(y);
             }
             *ptr = v;
           }

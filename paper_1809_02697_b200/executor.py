@@ -203,9 +203,11 @@ class DeviceProgram:
         # tensor cores can become the conv's shared-memory prologue (DenseNet
         # pre-activation; neither the BN nor the ReLU value is materialised).
         # Opt-in (NEOB200_PROLOGUE=1): on B200 the in-smem rewrite sits on the
-        # critical path of every pipeline stage and cost more (DenseNet-201
-        # b32 2.9 -> 5.2 ms) than the HBM-speed scale-shift-relu launches it
-        # removes.
+        # critical path of every pipeline stage and costs more than the
+        # HBM-speed scale-shift-relu launches it removes (DenseNet-201 b32:
+        # 2.75 ms without, 4.25 ms with the round-2 rewrite -- per-slice
+        # parameters in registers, bit-identical to the unfused path; 5.2 ms
+        # with the round-1 rewrite).
         self.prologue: dict[int, int] = {}       # conv id -> bn id
         self.pro_src: dict[int, int] = {}        # relu id -> the BN's input value
         import os
