@@ -267,3 +267,43 @@ def test_pool_division_by_constant_is_correctly_rounded():
         rem = _rn_f32(F(x) - F(d) * F(q))
         q1 = _rn_f32(F(rem) * F(r) + F(q))
         assert q1 == float(np.float32(x) / np.float32(d)), x
+
+
+def test_fp8_scale_groups_and_pools():
+    """quant.attach_scales (host logic, no GPU): a max pool keeps its
+    input's scale, every member of an in-place concat group (transitively
+    through nested concats) takes the group's largest scale, and a global
+    average pool the fused head absorbs gets none."""
+    from paper_1809_02697_b200.graph import OpKind
+    from paper_1809_02697_b200.models import NetBuilder
+    from paper_1809_02697_b200.passes import compile_graph
+    from paper_1809_02697_b200.quant import attach_scales, quantized_nodes
+    b = NetBuilder("groups", 1, 3, 32)
+    x = b.conv_bn_relu(b.data, 3, 64, 3)
+    p = b.maxpool(x, 2, 2)
+    c1 = b.conv_bn_relu(p, 64, 64, 1)
+    c2 = b.conv_bn_relu(p, 64, 64, 3)
+    cat1 = b.concat([p, c1])
+    cat2 = b.concat([cat1, c2])
+    head = b.avgpool(b.conv_bn_relu(cat2, 192, 256, 1), 16, 1)
+    b.g.outputs = [b.classifier(head, 256, 10, softmax=False)]
+    cg = compile_graph(b.g, mode="bf16")
+    q = quantized_nodes(cg)
+    kinds = {cg.nodes[n].kind for n in q}
+    assert OpKind.Conv2d in kinds and OpKind.MaxPool in kinds
+    assert not any(cg.nodes[n].kind == OpKind.AvgPool for n in q)   # global, C % 256 == 0
+    scales = {n: 2.0 ** (i % 5 - 2) for i, n in enumerate(sorted(q))}
+    attach_scales(cg, scales)
+    sc = lambda n: cg.nodes[n].attrs.get("fp8_scale")
+    pools = [n for n in q if cg.nodes[n].kind == OpKind.MaxPool]
+    cats = [n for n, nd in cg.nodes.items() if nd.kind == OpKind.Concat]
+    assert len(pools) == 1 and len(cats) == 2
+    members = set(cats)
+    for c in cats:
+        members |= {s for s, _ in cg.nodes[c].inputs}
+    group = {sc(m) for m in members}
+    assert len(group) == 1 and None not in group            # one scale for the group
+    top = group.pop()
+    assert top == max(scales[m] for m in members if m in scales)
+    # the pool is a group member: its scale was raised to the group's
+    assert sc(pools[0]) == top
