@@ -65,7 +65,7 @@ def main():
     mus = sum(r["us"] for r in mem)
     mb = sum(r["bytes"] for r in mem)
     print(f"# {args.title}: per-launch ncu times (cold cache, serialised) vs algorithmic bytes\n")
-    print(f"HBM peak: {hbm:.0f} GB/s measured copy (MEASURED_PEAKS.json); bf16 tensor peak "
+    print(f"HBM peak: {hbm:.0f} GB/s measured copy (MEASURED_PEAKS.json); tensor peak "
           f"{tpk:.0f} TFLOP/s.  {len(mem)} memory-bound launches, {mus:.1f} us = "
           f"{100 * mus / tot:.1f}% of {tot:.1f} us; aggregate {mb / mus / 1e3:.0f} GB/s = "
           f"{mb / mus / 1e3 / hbm:.2f} of HBM.\n")
