@@ -7,7 +7,9 @@ Python and allocates every intermediate in NumPy; here ``DeviceProgram``
 compiles it once per (device, mode):
 
 * every operator becomes one pre-bound libneob200 launch (conv with fused
-  epilogue, pool, eltwise, concat copy, dense, softmax, layout transform);
+  epilogue, pool, eltwise, concat copy, dense, softmax, layout transform),
+  except where fusion.py's plan merges several into one launch (image stem,
+  classifier head, sibling 1x1 convs, BN-ReLU, Dense-ReLU);
 * standalone BatchNorm followed by its only consumer ReLU runs as one fused
   scale-shift-relu launch (DenseNet's pre-activations);
 * all intermediates live in one static arena with liveness-based reuse
@@ -41,6 +43,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .errors import InputMismatch, ShapeMismatch
+from .fusion import FusionOptions, conv_kcrs, dense_block, plan_fusions
 from .graph import Graph, OpKind, hw_pair, infer_shapes, topo_sort, validate
 from .kernels import bytes_per_elem, tc_legal_block
 from .layout import Layout, host_unpack_kcrs
@@ -128,12 +131,15 @@ class DeviceProgram:
     """One compiled forward of ``plan`` on ``device`` in ``mode``."""
 
     def __init__(self, plan: ExecutablePlan, device: int = 0, mode: str = "bf16",
-                 keep=(), use_graph: bool = True, host_round: bool | None = None):
+                 keep=(), use_graph: bool = True, host_round: bool | None = None,
+                 fusion: FusionOptions | None = None):
         """``host_round``: an image read only by fused stems is uploaded as
         bf16 rounded on the host (half the PCIe bytes, host CPU work per
         batch) when True (default), or as f32 and rounded by the stem's
         loader (bit-identical, no host compute: what several ranks sharing one
-        host want) when False; NEOB200_HOST_ROUND=0 flips the default."""
+        host want) when False; NEOB200_HOST_ROUND=0 flips the default.
+        ``fusion``: fusion planner switches (fusion.FusionOptions; default
+        the shipped configuration with the NEOB200_* experiment overrides)."""
         import torch
         from . import _lib as L
         L.load()
@@ -174,6 +180,8 @@ class DeviceProgram:
         self.use_graph = use_graph and not os.environ.get("NEOB200_NO_GRAPH")
         self.host_round = (os.environ.get("NEOB200_HOST_ROUND", "1") != "0") if host_round is None \
             else bool(host_round)
+        self.fusion_options = fusion if fusion is not None else \
+            FusionOptions.from_env(host_round=self.host_round)
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
             self._lower()
@@ -183,178 +191,22 @@ class DeviceProgram:
 
     # -- analysis ------------------------------------------------------------
     def _lower(self):
-        import torch
         g = self.g
         self.specs = infer_shapes(g)
         self.users = g.consumers()
         order = self.plan.order
         self.step = {nid: i for i, nid in enumerate(order)}
-        self.fused_bn_relu: dict[int, int] = {}   # relu id -> bn id
-        self.skip: set[int] = set()
-        for nid in order:
-            node = g.nodes[nid]
-            if node.kind == OpKind.BatchNorm and len(node.inputs) == 1:
-                us = self.users[nid]
-                if (len(us) == 1 and g.nodes[us[0]].kind == OpKind.ReLU
-                        and nid not in g.outputs and nid not in self.keep):
-                    self.fused_bn_relu[us[0]] = nid
-                    self.skip.add(nid)
-        # BN -> ReLU feeding only the data input of an unpadded 1x1 conv on the
-        # tensor cores can become the conv's shared-memory prologue (DenseNet
-        # pre-activation; neither the BN nor the ReLU value is materialised).
-        # Opt-in (NEOB200_PROLOGUE=1): on B200 the in-smem rewrite sits on the
-        # critical path of every pipeline stage and costs more than the
-        # HBM-speed scale-shift-relu launches it removes (DenseNet-201 b32:
-        # 2.75 ms without, 4.25 ms with the round-2 rewrite -- per-slice
-        # parameters in registers, bit-identical to the unfused path; 5.2 ms
-        # with the round-1 rewrite).
-        self.prologue: dict[int, int] = {}       # conv id -> bn id
-        self.pro_src: dict[int, int] = {}        # relu id -> the BN's input value
-        import os
-        if self.mode in ("bf16", "tf32") and os.environ.get("NEOB200_PROLOGUE"):
-            for relu, bn in list(self.fused_bn_relu.items()):
-                us = self.users[relu]
-                if len(us) != 1 or relu in g.outputs or relu in self.keep:
-                    continue
-                cv = g.nodes[us[0]]
-                if cv.kind != OpKind.Conv2d or cv.inputs[0][0] != relu:
-                    continue
-                if any(s == relu for s, _ in cv.inputs[1:]):
-                    continue
-                wt = g.nodes[cv.inputs[1][0]].attrs["value"]
-                kh, kw = (wt.shape[2], wt.shape[3]) if wt.ndim == 4 else (wt.shape[2], wt.shape[3])
-                spec = self.specs[relu]
-                if (kh, kw) != (1, 1) or hw_pair(cv.attrs["pad"]) != (0, 0):
-                    continue
-                if spec.layout.tag != "NCHWc" or not tc_legal_block(spec.layout.x, self.mode):
-                    continue
-                if spec.logical_nchw[1] % spec.layout.x:
-                    continue
-                self.prologue[cv.id] = bn
-                self.pro_src[relu] = g.nodes[bn].inputs[0][0]
-                self.skip.add(relu)
-                del self.fused_bn_relu[relu]
-        # Dense layers run as 1x1 tensor-core convs over their row-major input
-        # ((N, F) == NCHW[x]c with H = W = 1); a Dense whose only consumer is a
-        # ReLU writes the ReLU's value with the relu fused into the epilogue.
-        self.tc_dense: set[int] = set()
-        self.fused_dense_relu: dict[int, int] = {}   # relu id -> dense id
-        if self.mode in ("bf16", "tf32", "fp8"):
-            for nid in order:
-                node = g.nodes[nid]
-                if node.kind != OpKind.Dense:
-                    continue
-                width = g.nodes[node.inputs[1][0]].attrs["value"].shape[1]
-                if self._dense_block(width):
-                    self.tc_dense.add(nid)
-                us = self.users[nid]
-                if (len(us) == 1 and g.nodes[us[0]].kind == OpKind.ReLU
-                        and nid not in g.outputs and nid not in self.keep):
-                    self.fused_dense_relu[us[0]] = nid
-                    self.skip.add(nid)
-        # 3-channel image stems: fold the kernel's horizontal taps into
-        # channels (neo_stem_fold) so the first conv reads 64-byte rows
-        self.stem_fold: dict[int, dict] = {}
-        if self.mode in ("bf16", "tf32", "fp8"):
-            for nid in order:
-                info = self._stem_fold_info(nid)
-                if info:
-                    self.stem_fold[nid] = info
-        # image stem (7x7/2 conv + relu + 3x3/2 max pool over a <=4-channel
-        # input) as one fused launch in bf16 mode: neither the packed input
-        # nor the conv map is materialised (neo_stem_conv_pool)
-        self.fused_stem: dict[int, tuple[int, int]] = {}   # pool id -> (conv, input)
-        if self.mode in ("bf16", "fp8") and not os.environ.get("NEOB200_NO_FUSED_STEM"):
-            for t, info in list(self.stem_fold.items()):
-                found = self._fused_stem_info(t, info)
-                if found:
-                    cv, mp, src = found
-                    self.fused_stem[mp] = (cv, src)
-                    self.skip.update((t, cv))
-                    del self.stem_fold[t]
-        # a graph input read only by fused stems is stored as bf16: the stem
-        # rounds it RN to bf16 anyway, so rounding on the host before the
-        # upload gives identical results with half the host->device bytes
-        self.bf16_inputs: set[int] = set()
-        stem_srcs = {src for _, src in self.fused_stem.values()} if self.host_round else set()
-        for src in stem_srcs:
-            if all(u in self.skip for u in self.users[src]) and src not in g.outputs \
-                    and g.nodes[src].attrs.get("layout", "NCHW") == "NCHW" \
-                    and self.specs[src].logical_nchw[3] % 8 == 0:
-                self.bf16_inputs.add(src)
-        # classifier head (global avg pool -> flatten -> dense -> softmax) as
-        # one fused launch in bf16 mode (neo_classifier_head)
-        self.fused_head: dict[int, dict] = {}    # anchor (softmax or dense) id -> info
-        if self.mode in ("bf16", "fp8") and not os.environ.get("NEOB200_NO_FUSED_HEAD"):
-            for nid in order:
-                info = self._fused_head_info(nid)
-                if info:
-                    self.fused_head[info["anchor"]] = info
-                    self.skip.update(info["skip"])
-        # sibling 1x1 convs over one input (a bottleneck's reduce conv and its
-        # projection shortcut, Inception's branch reducers) run as one
-        # two-output launch over concatenated weights
-        self.sibling: dict[int, tuple[int, int]] = {}   # first conv -> (second, tile_n)
-        self.sibling_of: dict[int, int] = {}            # second -> first
-        if self.mode in ("bf16", "tf32", "fp8") and not os.environ.get("NEOB200_NO_SIBLING"):
-            groups: dict[int, list[int]] = {}
-            for nid in order:
-                if self._sibling_eligible(nid):
-                    groups.setdefault(g.nodes[nid].inputs[0][0], []).append(nid)
-            for convs in groups.values():
-                convs = list(convs)
-                while len(convs) >= 2:
-                    a = convs.pop(0)
-                    pick = None
-                    for b in convs:
-                        tn = self._sibling_tile(a, b)
-                        if tn:
-                            pick = (b, tn)
-                            break
-                    if pick:
-                        convs.remove(pick[0])
-                        self.sibling[a] = pick
-                        self.sibling_of[pick[0]] = a
-        # junctions between bottleneck blocks: an expand conv (1x1, fused
-        # shortcut) and the next block's reduce conv (1x1) reading its output
-        # run as one neo_conv_junction launch; the reduce conv takes the
-        # expand's output from shared memory (both maps are still written).
-        # Opt-in (NEOB200_JUNCTION=1): bit-identical and faster per launch
-        # in isolation, but measured slower inside the graphed ResNet-50 b64
-        # step (1.190 vs 1.183 ms with only the 56x56 junctions, 1.235 ms with
-        # all): one tile in flight per SM drains its chunks serially, while the
-        # two tuned stand-alone convs overlap tiles and neighbouring launches
-        self.junction: dict[int, int] = {}       # expand conv -> reduce conv
-        self.junction_of: dict[int, int] = {}    # reduce conv -> expand conv
-        if self.mode == "bf16" and os.environ.get("NEOB200_JUNCTION") == "1":
-            for nid in order:
-                r = self._junction_partner(nid)
-                if r is not None and r not in self.junction_of and nid not in self.junction_of:
-                    self.junction[nid] = r
-                    self.junction_of[r] = nid
-        # physical block size for tensor-core-illegal packed inputs
-        self.phys_x: dict[int, int] = {}
-        if self.mode in ("bf16", "tf32"):
-            min_lanes = 16 // bytes_per_elem(self.mode)
-            for nid in order:
-                node = g.nodes[nid]
-                if node.kind != OpKind.LayoutTransform:
-                    continue
-                dst = Layout.parse(node.attrs["dst_layout"])
-                if dst.tag != "NCHWc" or tc_legal_block(dst.x, self.mode):
-                    continue
-                src_layout = Layout.parse(node.attrs["src_layout"])
-                us = self.users[nid]
-                if nid in self.stem_fold:
-                    continue
-                if (src_layout.tag == "NCHW" and us and nid not in g.outputs
-                        and all(g.nodes[u].kind == OpKind.Conv2d and g.nodes[u].inputs[0][0] == nid
-                                for u in us)):
-                    px = min_lanes
-                    while px < dst.x:
-                        px *= 2
-                    if tc_legal_block(px, self.mode):
-                        self.phys_x[nid] = px
+        # which operators share a launch: fusion.py owns the decisions
+        self.fusion = fp = plan_fusions(g, self.mode, self.keep, self.fusion_options,
+                                        specs=self.specs, users=self.users, order=order)
+        self.skip = fp.skip
+        self.fused_bn_relu, self.prologue, self.pro_src = fp.fused_bn_relu, fp.prologue, fp.pro_src
+        self.tc_dense, self.fused_dense_relu = fp.tc_dense, fp.fused_dense_relu
+        self.stem_fold, self.fused_stem, self.bf16_inputs = fp.stem_fold, fp.fused_stem, fp.bf16_inputs
+        self.fused_head = fp.fused_head
+        self.sibling, self.sibling_of = fp.sibling, fp.sibling_of
+        self.junction, self.junction_of = fp.junction, fp.junction_of
+        self.phys_x = fp.phys_x
         for nid in order:
             if nid in self.skip:
                 continue
@@ -491,214 +343,8 @@ class DeviceProgram:
             return 0, v.shape[1]
         return v.win[1], self.vals[v.win[0]].shape[1]
 
-    def _fused_stem_info(self, t: int, info: dict):
-        """(conv, pool, input) if stem transform ``t`` feeds exactly one
-        7x7/2 pad-3 conv with 64 outputs and no residual whose only consumer
-        is a 3x3/2 pad-1 max pool writing NCHW[y]c."""
-        g = self.g
-        if info["S"] != 7 or info["sw"] != 2 or info["pw"] != 3 or info["w"] % 4:
-            return None
-        us = self.users[t]
-        if len(us) != 1:
-            return None
-        cv = g.nodes[us[0]]
-        wt = g.nodes[cv.inputs[1][0]].attrs["value"]
-        if wt.ndim == 6:                    # pre-packed KCRS[x]c[y]k
-            wt = host_unpack_kcrs(wt)
-        epi = cv.attrs.get("epilogue") or {}
-        if (wt.ndim != 4 or tuple(wt.shape) != (64, info["C"], 7, 7) or epi.get("residual")
-                or len(cv.inputs) > 3 or hw_pair(cv.attrs["stride"]) != (2, 2)
-                or hw_pair(cv.attrs["pad"]) != (3, 3)):
-            return None
-        cus = self.users[cv.id]
-        if len(cus) != 1 or cv.id in g.outputs or cv.id in self.keep:
-            return None
-        mp = g.nodes[cus[0]]
-        if (mp.kind != OpKind.MaxPool or hw_pair(mp.attrs["window"]) != (3, 3)
-                or hw_pair(mp.attrs["stride"]) != (2, 2)
-                or hw_pair(mp.attrs.get("pad", 0)) != (1, 1)):
-            return None
-        lay = self.specs[mp.id].layout
-        if lay.tag != "NCHWc" or lay.x not in (8, 16, 32, 64):
-            return None
-        return cv.id, mp.id, g.nodes[t].inputs[0][0]
-
     def _conv_kcrs(self, nid: int) -> np.ndarray:
-        wv = self.g.nodes[self.g.nodes[nid].inputs[1][0]].attrs["value"]
-        return host_unpack_kcrs(wv) if wv.ndim == 6 else np.asarray(wv, np.float32)
-
-    def _sibling_eligible(self, nid: int) -> bool:
-        """Unpadded 1x1 tensor-core conv without residual or prologue over a
-        blocked input, writing a blocked map whose rows suit the TMA-store
-        epilogue."""
-        g = self.g
-        node = g.nodes[nid]
-        if node.kind != OpKind.Conv2d or nid in self.prologue or nid in self.skip:
-            return False
-        epi = node.attrs.get("epilogue") or {}
-        if epi.get("residual") or hw_pair(node.attrs["pad"]) != (0, 0):
-            return False
-        src = node.inputs[0][0]
-        if src in self.stem_fold or src in self.skip:
-            return False
-        k, c, r, s = self._conv_kcrs(nid).shape
-        if (r, s) != (1, 1):
-            return False
-        dl, ol = self.specs[src].layout, self.specs[nid].layout
-        if dl.tag != "NCHWc" or ol.tag != "NCHWc" or not tc_legal_block(dl.x, self.mode):
-            return False
-        if c % dl.x or k % ol.x or (ol.x * bytes_per_elem(self.mode)) not in (32, 64, 128):
-            return False
-        return True
-
-    def _junction_conv_ok(self, nid: int, residual: bool) -> bool:
-        """Unpadded stride-1 1x1 bf16 conv over NCHW[64]c into NCHW[64]c,
-        bias-only epilogue (BN folded), with / without a fused residual."""
-        g = self.g
-        node = g.nodes[nid]
-        if node.kind != OpKind.Conv2d or nid in self.skip or nid in self.prologue:
-            return False
-        if nid in self.sibling or nid in self.sibling_of or nid in self.stem_fold:
-            return False
-        epi = node.attrs.get("epilogue") or {}
-        if bool(epi.get("residual")) != residual or epi.get("scale") is not None \
-                or epi.get("shift") is not None:
-            return False
-        if hw_pair(node.attrs["stride"]) != (1, 1) or hw_pair(node.attrs["pad"]) != (0, 0):
-            return False
-        k, c, r, s_ = self._conv_kcrs(nid).shape
-        src = node.inputs[0][0]
-        dl, ol = self.specs[src].layout, self.specs[nid].layout
-        if (r, s_) != (1, 1) or dl.tag != "NCHWc" or ol.tag != "NCHWc":
-            return False
-        if dl.x != 64 or ol.x != 64 or c % 64 or k % 64 or src in self.stem_fold:
-            return False
-        if residual and self.specs[node.inputs[-1][0]].layout.x != 64:
-            return False
-        return True
-
-    def _junction_partner(self, nid: int) -> int | None:
-        """Reduce conv R that can share a launch with expand conv ``nid``."""
-        if not self._junction_conv_ok(nid, residual=True):
-            return None
-        n1 = self._conv_kcrs(nid).shape[0]
-        if n1 % 128:
-            return None
-        _, _, h, w = self.specs[nid].logical_nchw
-        if h * w < int(os.environ.get("NEOB200_JUNCTION_MIN_HW", "0")):
-            return None
-        for u in self.users[nid]:
-            if u == nid or self.g.nodes[u].inputs[0][0] != nid:
-                continue
-            if not self._junction_conv_ok(u, residual=False):
-                continue
-            if self.pro_src.get(nid) is not None:
-                continue
-            n2 = self._conv_kcrs(u).shape[0]
-            if n2 <= 256:
-                return u
-        return None
-
-    def _sibling_tile(self, a: int, b: int) -> int:
-        """N tile of the merged launch (k_split = K of ``a`` must be a whole
-        number of tiles), or 0 when the pair should not merge."""
-        g = self.g
-        na, nb = g.nodes[a], g.nodes[b]
-        if hw_pair(na.attrs["stride"]) != hw_pair(nb.attrs["stride"]):
-            return 0
-        if self.specs[a].layout.x != self.specs[b].layout.x:
-            return 0
-        ka, kb = self._conv_kcrs(a).shape[0], self._conv_kcrs(b).shape[0]
-        # measured (B200, b64): merging pays when both halves fill 128-256
-        # wide N tiles; 64-wide tiles (the 56x56 64 -> 64 reducer) lose
-        for tn in (256, 128):
-            if ka % tn == 0 and kb >= tn:
-                return tn
-        return 0
-
-    def _fused_head_info(self, nid: int) -> dict | None:
-        """Chain global AvgPool -> (NCHW transform) -> Flatten -> Dense ->
-        (Softmax) with single consumers, over a bf16 NCHW[y]c map."""
-        g = self.g
-        node = g.nodes[nid]
-        if node.kind != OpKind.AvgPool or hw_pair(node.attrs.get("pad", 0)) != (0, 0):
-            return None
-        src = node.inputs[0][0]
-        sspec = self.specs[src]
-        n, c, h, w = sspec.logical_nchw
-        if hw_pair(node.attrs["window"]) != (h, w) or sspec.layout.tag != "NCHWc":
-            return None
-        if sspec.layout.x % 8 or c % 256 or c % sspec.layout.x:
-            return None
-        chain, cur = [nid], nid
-        protected = set(g.outputs) | set(self.keep)
-        while True:
-            us = self.users[cur]
-            if len(us) != 1 or cur in protected:
-                break
-            nxt = g.nodes[us[0]]
-            if nxt.kind in (OpKind.LayoutTransform, OpKind.Flatten) and len(chain) < 3:
-                chain.append(nxt.id)
-                cur = nxt.id
-                continue
-            if nxt.kind == OpKind.Dense and nxt.inputs[0][0] == cur:
-                if nxt.id in self.skip or nxt.id in self.fused_dense_relu.values():
-                    return None       # the Dense is already fused into its ReLU
-                chain.append(nxt.id)
-                cur = nxt.id
-                if len(self.users[cur]) == 1 and cur not in protected:
-                    sm = g.nodes[self.users[cur][0]]
-                    if sm.kind == OpKind.Softmax:
-                        chain.append(sm.id)
-                break
-            break
-        kinds = [g.nodes[i].kind for i in chain]
-        if OpKind.Dense not in kinds or kinds[-2 if kinds[-1] == OpKind.Softmax else -1] != OpKind.Dense:
-            return None
-        if OpKind.Flatten not in kinds:
-            return None
-        dense = next(i for i in chain if g.nodes[i].kind == OpKind.Dense)
-        wt = g.nodes[g.nodes[dense].inputs[1][0]].attrs["value"]
-        if wt.ndim != 2 or wt.shape[1] != c:
-            return None
-        return {"anchor": chain[-1], "skip": chain[:-1], "src": src, "dense": dense,
-                "softmax": kinds[-1] == OpKind.Softmax}
-
-    def _stem_fold_info(self, nid) -> dict | None:
-        """Fold parameters if ``nid`` packs a few-channel graph input that
-        only feeds convs sharing one kernel width / stride / pad along w."""
-        g = self.g
-        node = g.nodes[nid]
-        if node.kind != OpKind.LayoutTransform or nid in g.outputs or nid in self.keep:
-            return None
-        if Layout.parse(node.attrs["src_layout"]).tag != "NCHW" or \
-                Layout.parse(node.attrs["dst_layout"]).tag != "NCHWc":
-            return None
-        src = node.inputs[0][0]
-        if g.nodes[src].kind != OpKind.Input:
-            return None
-        n, c, h, w = self.specs[src].logical_nchw
-        us = self.users[nid]
-        if not us or c > 4:
-            return None
-        geo = set()
-        for u in us:
-            un = g.nodes[u]
-            if un.kind != OpKind.Conv2d or un.inputs[0][0] != nid:
-                return None
-            wt = g.nodes[un.inputs[1][0]].attrs["value"]
-            geo.add((wt.shape[3], hw_pair(un.attrs["stride"])[1], hw_pair(un.attrs["pad"])[1]))
-        if len(geo) != 1:
-            return None
-        S, sw, pw = geo.pop()
-        F = S * c
-        lanes = [x for x in (8, 16, 32, 64, 4) if tc_legal_block(x, self.dense_mode)]
-        fits = [x for x in sorted(lanes) if x >= F]
-        if S == 1 or not fits:
-            return None
-        ow = (w + 2 * pw - S) // sw + 1
-        return {"S": S, "sw": sw, "pw": pw, "ow": ow, "C": c, "F": F, "xf": fits[0],
-                "n": n, "h": h, "w": w}
+        return conv_kcrs(self.g, nid)
 
     def _storage(self, nid) -> _Val | None:
         v = self.vals.get(nid)
@@ -711,7 +357,7 @@ class DeviceProgram:
         spec = self.specs[nid]
         node = self.g.nodes[nid]
         layout = spec.layout
-        if nid in getattr(self, "bf16_inputs", ()):
+        if nid in self.bf16_inputs:
             return _Val(nid, tuple(spec.shape), torch.bfloat16, layout)
         if node.kind == OpKind.Input and layout.tag == "NHWC":
             layout = Layout("NCHW")
@@ -741,11 +387,7 @@ class DeviceProgram:
         return _Val(nid, tuple(spec.shape), dtype, layout)
 
     def _dense_block(self, width: int) -> int:
-        """Legal tensor-core block dividing a dense input width (0 if none)."""
-        for x in (64, 32, 16, 8, 4):
-            if width % x == 0 and tc_legal_block(x, self.dense_mode):
-                return x
-        return 0
+        return dense_block(width, self.dense_mode)
 
     def _feeds_tc_dense(self, nid: int) -> bool:
         """A non-blocked value is kept in the activation type when every use

@@ -50,7 +50,7 @@ def act_scale(absmax: float, margin: float = CALIB_MARGIN) -> float:
 
 def _global_pool(g: Graph, nid: int) -> bool:
     """A global average pool the fused classifier head absorbs (C % 256 ==
-    0, executor._fused_head_info): the head pools the e4m3 map at its
+    0, fusion._Analysis._fused_head_info): the head pools the e4m3 map at its
     input's scale, so the pool itself stores nothing and needs no scale."""
     from .graph import hw_pair, infer_shapes
     n = g.nodes[nid]
