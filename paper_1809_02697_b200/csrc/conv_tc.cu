@@ -139,6 +139,7 @@ struct ConvTCParams {
   // output channel blocks -- nothing else is left for the idle group to do,
   // and the last epilogue is the launch's tail
   int share_last;
+  int epi_warps;      // epilogue warps of this launch: 16, or 8 in half-SM mode (320 threads)
   int dbg_slot;     // NEOB200_DBG & 256: per-launch timeline slot (g_tl)
 };
 
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int epi_warps = p.pro ? kEpiWarps - kProWarps : kEpiWarps;   // warps 2 .. 2+epi_warps-1
+  const int epi_warps = p.pro ? kEpiWarps - kProWarps : p.epi_warps;   // warps 2 .. 2+epi_warps-1
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const bool leader_cta = rank == 0;
 #ifdef NEO_TRACE
@@ -1410,19 +1411,36 @@ CUtensorMapSwizzle swizzle_code_tma(int rowb) {
 
 int64_t conv_out_dim(int64_t in, int64_t k, int st, int pad) { return (in + 2 * pad - k) / st + 1; }
 
+// Half-SM mode (NEOB200_HALF=1): every conv CTA takes at most half an SM --
+// 320 threads (8 epilogue warps), <= 113 KB of shared memory, <= 256 TMEM
+// columns -- so two CTAs are co-resident per SM: CTAs of the next launch
+// (PDL) or of a second stream's launch set up and run beside this one's
+// fill / drain phases.
+bool half_sm_mode() {
+  static const bool on = getenv("NEOB200_HALF") && atoi(getenv("NEOB200_HALF")) > 0;
+  return on;
+}
+int64_t smem_budget() { return half_sm_mode() ? 113 * 1024 : kSmemBudget; }
+
 struct Geometry {
   int BW, BH, BNI;
 };
 
-// M-tile geometry maximising useful rows of the 128-row MMA tile
-Geometry pick_geometry(int64_t N, int64_t OH, int64_t OW) {
+// M-tile geometry maximising useful rows of the 128-row MMA tile.
+// ``local``: tiles of ONE image only (tile_img = 1).  On odd maps at batch
+// 128 the unrestricted pick is one pixel x 128 images (all 128 rows useful),
+// which is fine for 1x1 convs and small maps but loses 22-29% on windowed
+// convs over large maps (Inception-v3's 147x147 / 73x73 3x3 layers,
+// tools/geo_sweep.py): every tap's A box is 128 rows scattered over 128
+// images instead of a few contiguous row segments.
+Geometry pick_geometry(int64_t N, int64_t OH, int64_t OW, bool local = false) {
   Geometry best{1, 1, 1};
   double best_eff = -1.0;
   const int bw_max = (int)std::min<int64_t>(OW, kTileM);
   for (int bw = 1; bw <= bw_max; ++bw) {
     const int bh_max = (int)std::min<int64_t>(OH, kTileM / bw);
     for (int bh = 1; bh <= bh_max; ++bh) {
-      const int bni_max = (int)std::min<int64_t>(N, kTileM / (bw * bh));
+      const int bni_max = local ? 1 : (int)std::min<int64_t>(N, kTileM / (bw * bh));
       for (int bni = 1; bni <= bni_max; ++bni) {
         const double tiles =
             (double)neo_ceil_div(OW, bw) * neo_ceil_div(OH, bh) * neo_ceil_div(N, bni);
@@ -1441,6 +1459,10 @@ Geometry pick_geometry(int64_t N, int64_t OH, int64_t OW) {
 }
 
 int pick_tile_n(int64_t K) {
+  if (half_sm_mode()) {                  // 2 accumulators in 256 TMEM columns
+    if (K <= 128) return (int)neo_ceil_div(K, 16) * 16;
+    return 128;
+  }
   if (K <= 256) return (int)neo_ceil_div(K, 16) * 16;
   int best = 256;
   int64_t best_waste = neo_ceil_div(K, 256) * 256 - K;
@@ -1496,6 +1518,7 @@ int64_t neo_conv_umma_slices(int mode, int64_t c, int64_t r, int64_t s, int x,
 // else two (long K loops want the shared memory for pipeline stages)
 static int epi_groups(const neo_conv_params* p, int tile_n) {
   if (p->pro_scale) return 2;            // prologue mode: 8 epilogue warps, 2 groups
+  if (half_sm_mode()) return 2;          // 8 epilogue warps, 2 x 128 TMEM columns
   static const int forced = getenv("NEOB200_EPI_GROUPS") ? atoi(getenv("NEOB200_EPI_GROUPS")) : 0;
   if (forced == 2 || (forced == 4 && tile_n <= 128)) return forced;
   const int64_t slices = p->r * p->s * neo_ceil_div(p->c, std::max(1, p->ic_bn));
@@ -1583,11 +1606,20 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
   const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
   NEO_CHECK_ARG(OH >= 1 && OW >= 1, NEO_ERR_SHAPE_MISMATCH, "conv has empty output");
+  if (half_sm_mode() && p->tile_n > 128) p->tile_n = 128;   // 2 accumulators in 256 TMEM columns
   const bool auto_geom = p->tile_w <= 0 || p->tile_h <= 0 || p->tile_img <= 0;
   const bool auto_tn = p->tile_n <= 0;
   Geometry g0{0, 0, 0};
   if (auto_geom) {
     Geometry g = pick_geometry(p->n, OH, OW);
+    if (g.BNI > 1 && g.BW * g.BH < 16 && p->r * p->s > 1 && OW >= 64) {
+      // image-scattered tile on a large windowed map: keep the tile's pixels
+      // in one image when that still fills >= 85% of the MMA rows
+      const Geometry gl = pick_geometry(p->n, OH, OW, true);
+      const double eff_l = (double)OW * OH /
+                           ((double)neo_ceil_div(OW, gl.BW) * neo_ceil_div(OH, gl.BH) * kTileM);
+      if (eff_l >= 0.85) g = gl;
+    }
     g0 = g;
     p->tile_w = g.BW;
     p->tile_h = g.BH;
@@ -1611,7 +1643,7 @@ int neo_conv_default_tiles(neo_conv_params* p) {
   bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
   int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
                     neo_ceil_div(p->n, p->tile_img);
-  const int64_t budget = kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4;
+  const int64_t budget = smem_budget() - 2048 - kMaxGroups * kParamFloats * 4;
   auto staging_of = [&](int tn) -> int64_t {
     const int rbo = epi_rowb_out(p, tn);
     return rbo ? (int64_t)epi_groups(p, tn) * kTileM * rbo * (tn / std::max(1, p->oc_bn)) : 0;
@@ -1999,6 +2031,10 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   uint32_t cols = 32;
   while (cols < (uint32_t)(kp.ngroups * BN)) cols <<= 1;
   kp.tmem_cols = cols;
+  NEO_CHECK_ARG(!half_sm_mode() || cols <= 256, NEO_ERR_SCHEDULE_INVALID,
+                "half-SM mode: tile_n=%d needs %u TMEM columns (> 256)", BN, cols);
+  kp.epi_warps = half_sm_mode() && !p->pro_scale ? 8 : kEpiWarps;
+  const int threads = half_sm_mode() && !p->pro_scale ? 32 * (2 + 8) : kThreads;
   kp.scale = p->scale;
   kp.shift = p->shift;
   kp.bias = p->bias;
@@ -2044,7 +2080,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   // TMA-store epilogue: output / residual tensor maps over (y, OW, OH, Kb_total, N)
   const int rb_out = epi_rowb_out(p, BN);
   {
-    const int64_t left = (int64_t)kSmemBudget - 2048 - kMaxGroups * kParamFloats * 4 -
+    const int64_t left = smem_budget() - 2048 - kMaxGroups * kParamFloats * 4 -
                          (int64_t)p->stages * kp.a_stage - kp.b_region;
     const int64_t slots = rb_out ? left / ((int64_t)kp.ngroups * kTileM * rb_out) : 0;
     const int64_t per_tile = BN / std::max(1, p->oc_bn);
@@ -2104,9 +2140,10 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   const size_t smem = 1024 + (size_t)p->stages * kp.a_stage + kp.b_region +
                      (size_t)kp.ngroups * kp.nslot * kp.stage_out + 512 +
                      (size_t)kp.ngroups * kParamFloats * 4;
-  NEO_CHECK_ARG(smem <= (size_t)kSmemBudget, NEO_ERR_SCHEDULE_INVALID,
+  NEO_CHECK_ARG(smem <= (size_t)smem_budget(), NEO_ERR_SCHEDULE_INVALID,
                 "conv tile needs %zu bytes of shared memory", smem);
-  const int sms = sm_count_of_current_device();
+  static const int half_ctas = getenv("NEOB200_HALF_CTAS") ? atoi(getenv("NEOB200_HALF_CTAS")) : 1;
+  const int sms = sm_count_of_current_device() * (half_sm_mode() ? half_ctas : 1);
   // weight-stationary: grid % tiles_k == 0 keeps each CTA on one N block
   const int grid = pair  ? (int)std::min<int64_t>(kp.num_groups, sms / 2) * 2
                    : wst ? (int)(std::min<int64_t>(kp.num_units, sms) / kp.tiles_k * kp.tiles_k)
@@ -2127,12 +2164,16 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   if (!done) {
     NEO_CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemBudget));
+    if (half_sm_mode())
+      NEO_CUDA_TRY(cudaFuncSetAttribute((const void*)fn,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared));
     done = true;
   }
   if (pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
@@ -2146,7 +2187,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     cfg.numAttrs = neo_pdl_enabled() ? 2 : 1;
     NEO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, kp));
   } else {
-    neo_launch(fn, grid, kThreads, smem, stream, kp);
+    neo_launch(fn, grid, threads, smem, stream, kp);
   }
   NEO_LAUNCH_CHECK();
   return NEO_OK;

@@ -467,3 +467,62 @@ def test_tc_conv_two_outputs(cuda, mode_name, ka, kb, tile_n, stride):
     tol = 2e-2 if mode_name == "bf16" else 1e-3
     assert oracle.rel_err(got_a, ref_a) < tol and oracle.rel_err(got_b, ref_b) < tol
     assert np.all(obn[:, :2] == 5.0) and np.all(obn[:, 2 + kb // y:] == 5.0)
+
+
+@pytest.mark.gpu
+def test_tc_conv_default_geometry_large_odd_maps(cuda):
+    """Windowed conv over a large odd map with several images, too wide for
+    halo tiles (Inception-v3's 147x147 3x3 layers at batch 128): the kernel's
+    own geometry keeps an M tile inside ONE image (the unrestricted pick is a
+    few pixels x many images, 22-29% slower there, tools/geo_sweep.py), and
+    stays exact; a 1x1 conv over the same map keeps the image-spanning tile."""
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    rng = np.random.default_rng(11)
+    n, c, k, hw = 16, 32, 32, 131
+    x = bf16_round(rng.standard_normal((n, c, hw, hw)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((k, c, 1, 3)) * 0.1).astype(np.float32))
+    dev = torch.device("cuda:0")
+    xb = torch.from_numpy(pack_nchw(x, 32)).to(dev).bfloat16()
+    wd = D.pack_weights_umma(torch.from_numpy(wt).to(dev), 32, L.MODE_BF16)
+    out = torch.empty((n, 1, hw, hw - 2, 32), dtype=torch.float32, device=dev)
+    p = D.conv_params(L.MODE_BF16, xb, wd, out, n, c, hw, hw, k, 1, 3, (1, 1), (0, 0), 32, 32)
+    cfg = D.default_tiles(p)
+    assert cfg["tile_img"] == 1 and cfg["tile_w"] <= hw - 2, cfg
+    assert cfg["tile_w"] * cfg["tile_h"] >= 0.85 * 128, cfg
+    w1 = bf16_round((rng.standard_normal((k, c, 1, 1)) * 0.2).astype(np.float32))
+    wd1 = D.pack_weights_umma(torch.from_numpy(w1).to(dev), 32, L.MODE_BF16)
+    out1 = torch.empty((n, 1, hw, hw, 32), dtype=torch.float32, device=dev)
+    p1 = D.conv_params(L.MODE_BF16, xb, wd1, out1, n, c, hw, hw, k, 1, 1, (1, 1), (0, 0), 32, 32)
+    assert D.default_tiles(p1)["tile_img"] > 1
+    ref = oracle.conv2d(x, wt, (1, 1), (0, 0), relu=True)
+    got = run_conv(L.MODE_BF16, x, wt, (1, 1), (0, 0), 32, 32, relu=True)
+    assert oracle.rel_err(got, ref) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("shape,stride", [((3, 64, 29, 31), (2, 2)), ((2, 128, 28, 28), (2, 2)),
+                                          ((2, 64, 17, 23), (3, 2)), ((5, 64, 8, 8), (2, 1))])
+def test_tc_conv_strided_1x1(cuda, mode_name, shape, stride):
+    """Strided unpadded 1x1 convs (the downsampling projections): odd sizes,
+    unequal strides, residual + relu epilogue.  (A strided-VIEW tensor map --
+    map strides = conv strides, dense boxes -- was measured against the
+    element-stride boxes used here: identical times, not kept.)"""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w = shape
+    k = 128
+    rng = np.random.default_rng(h * 100 + w)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x = rnd(rng.standard_normal(shape).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, 1, 1)) * np.sqrt(2.0 / c)).astype(np.float32))
+    oh, ow = (h - 1) // stride[0] + 1, (w - 1) // stride[1] + 1
+    res = rng.standard_normal((n, k, oh, ow)).astype(np.float32)
+    bias = rng.standard_normal(k).astype(np.float32)
+    ref = oracle.conv2d(x, wt, stride, (0, 0), bias=bias, residual=res, relu=True)
+    got = run_conv(mode, x, wt, stride, (0, 0), 64 if mode_name == "bf16" else 32, 32, bias=bias,
+                   residual=res, relu=True)
+    assert got.shape == ref.shape
+    assert oracle.rel_err(got, ref) < 1e-4
