@@ -36,6 +36,19 @@ INCEPTION = [
 ]
 
 
+def exact_geometries(n, oh, ow, min_eff=0.93):
+    """Every (bw, bh, bni) box of <= 128 pixels with >= min_eff useful rows,
+    image-spanning boxes included (``--exact``)."""
+    out = [None]
+    for bw in range(1, min(ow, 128) + 1):
+        for bh in range(1, min(oh, 128 // bw) + 1):
+            for bni in range(1, min(n, 128 // (bw * bh)) + 1):
+                eff = n * oh * ow / (-(-ow // bw) * -(-oh // bh) * -(-n // bni) * 128)
+                if eff >= min_eff:
+                    out.append({"tile_w": bw, "tile_h": bh, "tile_img": bni})
+    return out
+
+
 def geometries(n, oh, ow):
     out = [None]
     seen = set()
@@ -64,6 +77,9 @@ def main():
     ap.add_argument("--mode", default="bf16")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--extra", default="", help="json dict merged into every explicit tile")
+    ap.add_argument("--exact", action="store_true",
+                    help="sweep every box with >= 93%% useful rows (image-spanning included)")
+    ap.add_argument("--res", action="store_true", help="fused residual + relu epilogue")
     args = ap.parse_args()
     shapes = [tuple(int(v) for v in s.split(",")) for s in args.shape]
     if args.shapes == "inception":
@@ -85,17 +101,18 @@ def main():
         wd = D.pack_weights_umma(w, bx, lmode, pad_channels=c % bx != 0)
         out = torch.empty((n, k // by, oh, ow, by), dtype=act, device=dev)
         bias = torch.randn(k, device=dev)
+        res = torch.randn(out.shape, device=dev).to(act) if args.res else None
         flops = 2 * n * k * c * r * s * oh * ow
         byts = (x.numel() + out.numel()) * x.element_size()
         print(f"== n{n} C{c} K{k} {H}x{W} {r}x{s}/{st} pad({ph},{pw}) x{bx} y{by}: "
               f"{flops / 1e9:.1f} GFLOP, {byts / 1e6:.0f} MB "
               f"(hbm {byts / 6.5e6:.0f} us, tensor {flops / 1.65e9:.0f} us)", flush=True)
         rows = []
-        for geo in geometries(n, oh, ow):
+        for geo in (exact_geometries(n, oh, ow) if args.exact else geometries(n, oh, ow)):
             tile = None if geo is None else {**geo, **extra}
             try:
                 p = D.conv_params(lmode, x, wd, out, n, c, H, W, k, r, s, (st, st), (ph, pw), bx,
-                                  by, bias=bias, relu=True, tile=tile,
+                                  by, bias=bias, residual=res, relu=True, tile=tile,
                                   flags=L.FLAG_PAD_CHANNELS if c % bx else 0)
                 cfg = D.default_tiles(p)
                 ws = torch.zeros(max(D.conv_workspace_bytes(p), 4) // 4, device=dev)
@@ -116,7 +133,7 @@ def main():
                 print(f"   {tile}: {type(exc).__name__}: {str(exc)[:100]}")
                 continue
             rows.append((us, geo is None, cfg))
-        for us, dflt, cfg in sorted(rows, key=lambda r: r[0])[:6] + [r for r in rows if r[1]]:
+        for us, dflt, cfg in sorted(rows, key=lambda r: r[0])[:8] + [r for r in rows if r[1]]:
             print(f"   {us:8.1f} us {flops / us / 1e6:6.0f} TF/s {byts / us / 1e3:6.0f} GB/s "
                   f"{'DEFAULT ' if dflt else ''}{json.dumps(cfg)}", flush=True)
 
