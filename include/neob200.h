@@ -77,6 +77,11 @@ typedef enum {
  * running (e.g. packed at load time), so a programmatically launched conv may
  * fetch its resident weight image before griddepcontrol.wait */
 #define NEO_FLAG_STATIC_WEIGHTS 0x4
+/* conv tile geometry: tile_w is the BAND width of a halo strip (tile_w - (s-1)
+ * output columns per tile, see conv_tc.cu); set by neo_conv_default_tiles when
+ * it picks strips for a map wider than one tile, or by a caller passing an
+ * explicit strip geometry */
+#define NEO_FLAG_HALO_STRIPS 0x8
 
 const char* neo_last_error(void);
 int neo_abi_version(void);

@@ -38,6 +38,7 @@ ELT_RELU, ELT_ADD, ELT_ADD_RELU, ELT_SCALE_SHIFT, ELT_SCALE_SHIFT_RELU = range(5
 FLAG_ROUND_TF32 = 0x1
 FLAG_PAD_CHANNELS = 0x2
 FLAG_STATIC_WEIGHTS = 0x4
+FLAG_HALO_STRIPS = 0x8
 
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int

@@ -62,6 +62,7 @@ struct ConvTCParams {
   CUtensorMap tmO2; // second output (k_split > 0), same geometry      (tma_epi)
   int N, OH, OW, K;
   int BW, BH, BNI, BN;
+  int BWo;       // output columns a tile advances by: BW, or BW - (S-1) for halo strips
   int tiles_w, tiles_h, tiles_k;
   int num_tiles;
   int G, kstages, Cb, S, nslices;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void decode_tile(const ConvTCParams& p, int t, int& n
   const uint32_t hi = q2 - ni * th;
   n0 = (int)ni * p.BNI;
   oh0 = hi * p.BH;
-  ow0 = wi * p.BW;
+  ow0 = wi * p.BWo;
   k0 = kt * p.BN;
 }
 
@@ -297,7 +298,7 @@ template <int OUT, bool HAS_RES, bool AFFINE>
 __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int col0,
                                               int m, uint8_t* sbuf_gen, const float* par,
                                               float relu_floor, bool round, int c_begin,
-                                              int c_step, float qs) {
+                                              int c_step, float qs, bool store) {
   constexpr bool OUT_F32 = OUT == kOutF32;
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : OUT == kOutBF16 ? 2 : 1;   // 16-byte pieces per 16 values
@@ -342,6 +343,7 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
       }
       const uint32_t off = srow + ((((uint32_t)(c * kChunks16 + q)) ^ sxr) << 4);
       uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
+      if (!store) continue;      // halo strip: accumulator row of a band column past the strip
       if constexpr (OUT_F32) {
         float o[4];
         float4 rv = HAS_RES ? *reinterpret_cast<float4*>(slot) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -440,7 +442,9 @@ __device__ __noinline__ void splitk_fixup(const ConvTCParams& p, int t, int sp, 
     const int kb0 = k0 + c * 16;
     const int wl = mr % p.BW, hl = (mr / p.BW) % p.BH, nl = mr / (p.BW * p.BH);
     const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
-    if (kb0 >= p.K || mr >= p.BW * p.BH * p.BNI || ow >= p.OW || oh >= p.OH || n >= p.N) continue;
+    if (kb0 >= p.K || mr >= p.BW * p.BH * p.BNI || wl >= p.BWo || ow >= p.OW || oh >= p.OH ||
+        n >= p.N)
+      continue;
     const float4* src = tile_ws + ((size_t)c * kTileM + mr) * 4;
     float f[16];
 #pragma unroll
@@ -1047,6 +1051,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const int half = ((warp - 2) >> 2) % nsub;      // which channel blocks of a tile
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int m = q * 32 + lane;            // accumulator row = tile pixel
+    // halo strips: accumulator row m = (tile row h, band column w) with a
+    // pitch of BW band columns; only w < BWo belongs to the strip, and its
+    // staging row is compacted to h * BWo + w (the store / residual boxes are
+    // BWo columns wide)
+    int ms = m;
+    bool mvalid = true;
+    if (p.BWo != p.BW) {
+      const int hh = m / p.BW, ww = m - hh * p.BW;
+      ms = hh * p.BWo + ww;
+      mvalid = ww < p.BWo;
+    }
     const bool leader = (warp == 2 + gwarps * grp) && lane == 0;
     const uint32_t bar_id = 1 + grp;
     const size_t plane = (size_t)p.OH * p.OW * p.y;
@@ -1238,7 +1253,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
 #define NEO_EPI(OUT, RES, AFF) \
-  epi_block_tma<OUT, RES, AFF>(p, tcol, col0, m, sg, par, floor_v, rnd, cbeg, cstep, qs)
+  epi_block_tma<OUT, RES, AFF>(p, tcol, col0, ms, sg, par, floor_v, rnd, cbeg, cstep, qs, mvalid)
 #define NEO_EPI_OUT(OUT)                       \
   if (affine) {                                \
     if (has_res) NEO_EPI(OUT, true, true);     \
@@ -1304,7 +1319,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         tc_fence_after();
         const int wl = m % p.BW, hl = (m / p.BW) % p.BH, nl = m / (p.BW * p.BH);
         const int ow = ow0 + wl, oh = oh0 + hl, n = n0 + nl;
-        const bool valid = (m < p.BW * p.BH * p.BNI) && ow < p.OW && oh < p.OH && n < p.N;
+        const bool valid = (m < p.BW * p.BH * p.BNI) && wl < p.BWo && ow < p.OW && oh < p.OH &&
+                           n < p.N;
         EpiAccess ea;
         ea.plane = plane;
         const size_t pix = ((size_t)oh * p.OW + ow) * p.y;
@@ -1544,11 +1560,41 @@ static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
 // SW64 shifted views: the swizzle follows absolute shared-memory address
 // bits, so a view shifted by whole rows reads what TMA wrote) and a padded
 // width that fits the 128-row M tile
-static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
+static bool halo_format_ok(const neo_conv_params* p, int rowb) {
   static const bool disabled = getenv("NEOB200_NO_HALO") != nullptr;
   static const bool no64 = getenv("NEOB200_NO_HALO64") != nullptr;
   return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 &&
-         (rowb == 128 || (rowb == 64 && !no64)) && OW + p->s - 1 <= kTileM;
+         (rowb == 128 || (rowb == 64 && !no64));
+}
+static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
+  return halo_format_ok(p, rowb) && OW + p->s - 1 <= kTileM;
+}
+// Halo STRIPS (NEO_FLAG_HALO_STRIPS): maps wider than one 128-row tile
+// (VGG's 224 / 112 maps, SSD's 128, Inception's 147) are cut into column
+// strips of BWo output columns; a tile's band is BW = BWo + S - 1 input
+// columns of BH (+ R - 1) rows, the S taps are the same shifted views, and the
+// epilogue drops the S - 1 band columns past the strip (compacted staging
+// rows, BWo-wide store / residual boxes).  Without strips those layers run
+// plain tiles that fetch every tap's box separately (R*S-fold A traffic).
+static bool halo_strips_on() {
+  static const bool off = getenv("NEOB200_NO_HALO_STRIPS") != nullptr;
+  return !off;
+}
+struct StripGeom { int BWo, BH; double eff; };
+static StripGeom pick_strips(int64_t OH, int64_t OW, int S) {
+  StripGeom best{0, 0, 0.0};
+  const int ns0 = (int)neo_ceil_div(OW, kTileM - (S - 1));
+  for (int ns = ns0; ns <= ns0 + 24; ++ns) {
+    const int bwo = (int)neo_ceil_div(OW, ns);
+    if (bwo < 8) break;
+    const int bw = bwo + S - 1;
+    const int bh = (int)std::min<int64_t>(OH, kTileM / bw);
+    if (bh < 1) continue;
+    const double eff = (double)OW * OH / ((double)neo_ceil_div(OW, bwo) * neo_ceil_div(OH, bh) * kTileM);
+    // most useful rows; ties -> taller tiles (a band carries R - 1 extra rows)
+    if (eff > best.eff + 1e-9 || (eff > best.eff - 1e-9 && bh > best.BH)) best = {bwo, bh, eff};
+  }
+  return best;
 }
 // halo bands are whole 1024-byte swizzle periods (8 rows of 128 B, 16 of
 // 64 B): TMA's SWIZZLE_64B pattern is laid out on 1024-byte boundaries, and
@@ -1627,6 +1673,12 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     p->tile_w = g.BW;
     p->tile_h = g.BH;
     p->tile_img = g.BNI;
+    // halo strips only where the full padded width does not fit one tile:
+    // forcing them onto 112 / 56 / 28-wide maps (taller bands, fewer band
+    // rows per output) measured 0-3% slower than full-width halo tiles
+    const bool strips_ok = halo_strips_on() && halo_format_ok(p, rowb) && p->tile_n <= 0 &&
+                           p->slices_per_stage <= 0 && p->stages <= 0 && p->split_k <= 1 &&
+                           p->cta_pair != 2 && !p->pro_scale;
     if (halo_eligible(p, rowb, OW)) {
       // halo tiles: full padded width, as many output rows as fit in 128
       const int bwp = (int)(OW + p->s - 1);
@@ -1641,11 +1693,22 @@ int neo_conv_default_tiles(neo_conv_params* p) {
         p->tile_h = bh;
         p->tile_img = 1;
       }
+    } else if (strips_ok && OW + p->s - 1 > kTileM) {
+      // wide map, nothing but the geometry left to the kernel: halo strips
+      // (explicit tile parameters were tuned for plain tiles and keep them)
+      const StripGeom sg = pick_strips(OH, OW, (int)p->s);
+      if (sg.BWo > 0 && sg.eff >= 0.7) {
+        p->tile_w = sg.BWo + (int)p->s - 1;
+        p->tile_h = sg.BH;
+        p->tile_img = 1;
+        p->flags |= NEO_FLAG_HALO_STRIPS;
+      }
     }
   }
-  bool halo = p->tile_w > OW;   // only halo geometry is wider than the output
-  int64_t m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
-                    neo_ceil_div(p->n, p->tile_img);
+  const bool strips = (p->flags & NEO_FLAG_HALO_STRIPS) != 0;
+  bool halo = p->tile_w > OW || strips;   // halo geometry: wider than the output, or strips
+  int64_t m_tiles = neo_ceil_div(OW, strips ? p->tile_w - (p->s - 1) : p->tile_w) *
+                    neo_ceil_div(OH, p->tile_h) * neo_ceil_div(p->n, p->tile_img);
   const int64_t budget = smem_budget() - 2048 - kMaxGroups * kParamFloats * 4;
   auto staging_of = [&](int tn) -> int64_t {
     const int rbo = epi_rowb_out(p, tn);
@@ -1684,6 +1747,7 @@ int neo_conv_default_tiles(neo_conv_params* p) {
       p->tile_w = g0.BW;
       p->tile_h = g0.BH;
       p->tile_img = g0.BNI;
+      p->flags &= ~NEO_FLAG_HALO_STRIPS;
       halo = false;
       m_tiles = neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
                 neo_ceil_div(p->n, p->tile_img);
@@ -1803,7 +1867,8 @@ int64_t conv_kstages(const neo_conv_params* p, bool halo) {
 int64_t conv_num_tiles(const neo_conv_params* p) {
   const int64_t OH = conv_out_dim(p->h, p->r, p->stride_h, p->pad_h);
   const int64_t OW = conv_out_dim(p->w_in, p->s, p->stride_w, p->pad_w);
-  return neo_ceil_div(OW, p->tile_w) * neo_ceil_div(OH, p->tile_h) *
+  const int64_t bwo = (p->flags & NEO_FLAG_HALO_STRIPS) ? p->tile_w - (p->s - 1) : p->tile_w;
+  return neo_ceil_div(OW, bwo) * neo_ceil_div(OH, p->tile_h) *
          neo_ceil_div(p->n, p->tile_img) * neo_ceil_div(p->k, p->tile_n);
 }
 }  // namespace
@@ -1820,7 +1885,7 @@ int neo_conv_workspace_bytes(const neo_conv_params* pin, int64_t* bytes) {
   const int st = neo_conv_default_tiles(&pc);
   if (st != NEO_OK) return st;
   const int64_t OW = conv_out_dim(pc.w_in, pc.s, pc.stride_w, pc.pad_w);
-  const bool halo = pc.tile_w > OW;
+  const bool halo = pc.tile_w > OW || (pc.flags & NEO_FLAG_HALO_STRIPS);
   *bytes = split_plan(&pc, conv_kstages(&pc, halo), conv_num_tiles(&pc)).ws_bytes;
   return NEO_OK;
 }
@@ -1872,12 +1937,19 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
 
   const int64_t Cb = neo_ceil_div(p->c, x);
   const int64_t cbt = p->x_cb_total > 0 ? p->x_cb_total : Cb;
-  const bool halo = BW > OW;
+  const bool strips = (p->flags & NEO_FLAG_HALO_STRIPS) != 0;
+  const bool halo = BW > OW || strips;
   const bool wst = p->weight_stationary == 2;
-  NEO_CHECK_ARG(!halo || halo_eligible(p, rowb, OW), NEO_ERR_SCHEDULE_INVALID,
+  const int BWo = strips ? BW - (int)(p->s - 1) : BW;   // output columns per tile
+  NEO_CHECK_ARG(!halo || (strips ? halo_format_ok(p, rowb) : halo_eligible(p, rowb, OW)),
+                NEO_ERR_SCHEDULE_INVALID,
                 "tile_w=%d wider than the output needs a stride-1, 128-byte-row conv", BW);
-  NEO_CHECK_ARG(!halo || (BW == OW + p->s - 1 && BNI == 1), NEO_ERR_SCHEDULE_INVALID,
+  NEO_CHECK_ARG(!halo || strips || (BW == OW + p->s - 1 && BNI == 1), NEO_ERR_SCHEDULE_INVALID,
                 "halo tiles must span the padded width OW+S-1 of one image");
+  NEO_CHECK_ARG(!strips || (BWo >= 1 && BNI == 1 && p->split_k <= 1 && p->cta_pair != 2 &&
+                            !p->pro_scale),
+                NEO_ERR_SCHEDULE_INVALID,
+                "halo strips: one image per tile, no split-K / CTA pair / prologue");
   const int64_t nslices = halo ? (wst ? Cb : p->r * Cb) : p->r * p->s * Cb;
   NEO_CHECK_ARG(!(wst && halo && G != 1), NEO_ERR_SCHEDULE_INVALID,
                 "weight-stationary halo tiles take one channel block per stage");
@@ -1892,7 +1964,7 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     NEO_CHECK_ARG(BN <= 128 && p->cta_pair != 2, NEO_ERR_SCHEDULE_INVALID,
                   "BN-ReLU prologue runs single-CTA tiles with tile_n <= 128 (tile_n=%d)", BN);
   }
-  const int64_t tiles_m_all = neo_ceil_div(OW, BW) * neo_ceil_div(OH, BH) * neo_ceil_div(p->n, BNI);
+  const int64_t tiles_m_all = neo_ceil_div(OW, BWo) * neo_ceil_div(OH, BH) * neo_ceil_div(p->n, BNI);
   const bool pair = !p->pro_scale && use_pair(p, BN, tiles_m_all);
   NEO_CHECK_ARG(!wst || wst_allowed(p, BN, tiles_m_all), NEO_ERR_SCHEDULE_INVALID,
                 "weight-stationary tiles need single-CTA tiles, no split-K, no prologue");
@@ -1953,10 +2025,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
   kp.OW = (int)OW;
   kp.K = (int)p->k;
   kp.BW = BW;
+  kp.BWo = BWo;
   kp.BH = BH;
   kp.BNI = BNI;
   kp.BN = BN;
-  kp.tiles_w = (int)neo_ceil_div(OW, BW);
+  kp.tiles_w = (int)neo_ceil_div(OW, BWo);
   kp.tiles_h = (int)neo_ceil_div(OH, BH);
   kp.tiles_k = (int)neo_ceil_div(p->k, BN);
   const int64_t tiles_n = neo_ceil_div(p->n, BNI);
@@ -2107,11 +2180,11 @@ int neo_conv_tc_launch(const neo_conv_params* pin, cudaStream_t stream) {
     const int y = p->oc_bn;
     kp.rowb_out = rb_out;
     kp.stage_out = (uint32_t)(kTileM * kp.rowb_out);
-    kp.out_box_bytes = (uint32_t)(BW * BH * BNI * kp.rowb_out);
+    kp.out_box_bytes = (uint32_t)(BWo * BH * BNI * kp.rowb_out);
     const CUtensorMapDataType odt = kp.out_f32                  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                     : kp.out_kind == kOutFP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    cuuint32_t box[5] = {(cuuint32_t)y, (cuuint32_t)BW, (cuuint32_t)BH, 1u, (cuuint32_t)BNI};
+    cuuint32_t box[5] = {(cuuint32_t)y, (cuuint32_t)BWo, (cuuint32_t)BH, 1u, (cuuint32_t)BNI};
     cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
     auto encode_fm = [&](CUtensorMap* map, const void* base, int64_t cb_total) {
       cuuint64_t dims[5] = {(cuuint64_t)y, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)cb_total,

@@ -3,6 +3,8 @@ CPU oracle, through the C-ABI.  Reference tests mirrored:
 tests/test_kernels.py:71-125 (workload/schedule edge cases), :167-186
 (epilogue order and residual)."""
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -526,3 +528,70 @@ def test_tc_conv_strided_1x1(cuda, mode_name, shape, stride):
                    residual=res, relu=True)
     assert got.shape == ref.shape
     assert oracle.rel_err(got, ref) < 1e-4
+
+
+STRIP_CASES = [
+    # (n, c, h, w, k, r, s, pad, ic_bn_bf16) -- maps wider than one 128-row halo tile
+    (2, 64, 40, 150, 64, 3, 3, (1, 1), 64),      # 128-byte rows, 2 strips
+    (1, 64, 33, 224, 128, 3, 3, (1, 1), 64),     # VGG width, several strips x rows
+    (2, 32, 37, 147, 32, 3, 3, (0, 0), 32),      # Inception conv10: 64-byte rows, no pad
+    (1, 64, 20, 140, 256, 1, 7, (0, 3), 64),     # 7 horizontal taps, two N tiles
+    (3, 128, 9, 129, 64, 3, 3, (1, 1), 64),      # few rows, two channel blocks
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", STRIP_CASES)
+@pytest.mark.parametrize("mode_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("wst", [0, 1])
+def test_tc_conv_halo_strips(cuda, case, mode_name, wst):
+    """Halo column strips (NEO_FLAG_HALO_STRIPS): stride-1 windowed convs over
+    maps wider than one 128-row tile; the kernel picks the strips itself when
+    only the geometry is left to it.  Residual + relu epilogue, exact
+    accumulation check, and the picked geometry really is a strip."""
+    import torch
+    from paper_1809_02697_b200 import _lib as L
+    from paper_1809_02697_b200 import device as D
+    n, c, h, w, k, r, s, pd, xb16 = case
+    rng = np.random.default_rng(h * 1000 + w)
+    rnd = bf16_round if mode_name == "bf16" else tf32_round
+    mode = L.MODE_BF16 if mode_name == "bf16" else L.MODE_TF32
+    x_bn = xb16 if mode_name == "bf16" else min(32, xb16)
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32))
+    oh, ow = h + 2 * pd[0] - r + 1, w + 2 * pd[1] - s + 1
+    res = rng.standard_normal((n, k, oh, ow)).astype(np.float32)
+    bias = rng.standard_normal(k).astype(np.float32)
+    ref = oracle.conv2d(x, wt, (1, 1), pd, bias=bias, residual=res, relu=True)
+    tile = {"weight_stationary": wst} if wst else None
+    got = run_conv(mode, x, wt, (1, 1), pd, x_bn, 32, bias=bias, residual=res, relu=True,
+                   tile=tile)
+    assert got.shape == ref.shape
+    assert oracle.rel_err(got, ref) < 1e-4
+    # the kernel's own geometry for this shape: band narrower than the map,
+    # at most 128 rows, one image
+    dev = torch.device("cuda:0")
+    act = torch.bfloat16 if mode_name == "bf16" else torch.float32
+    xb = torch.empty((n, c // x_bn, h, w, x_bn), dtype=act, device=dev)
+    wd = D.pack_weights_umma(torch.from_numpy(wt).to(dev), x_bn, mode)
+    out = torch.empty((n, k // 32, oh, ow, 32), dtype=torch.float32, device=dev)
+    p = D.conv_params(mode, xb, wd, out, n, c, h, w, k, r, s, (1, 1), pd, x_bn, 32)
+    q = L.ConvParams.from_buffer_copy(p)
+    L.check(L.load().neo_conv_default_tiles(ctypes.byref(q)), "neo_conv_default_tiles")
+    assert q.flags & L.FLAG_HALO_STRIPS, "wide stride-1 windowed conv should run halo strips"
+    assert q.tile_img == 1 and s <= q.tile_w < ow and q.tile_w * q.tile_h <= 128
+
+
+@pytest.mark.gpu
+def test_tc_conv_halo_strips_keep_explicit_tiles(cuda):
+    """Explicit tile parameters (tuned for plain tiles) switch the automatic
+    strips off; the result is the same conv either way."""
+    from paper_1809_02697_b200 import _lib as L
+    rng = np.random.default_rng(5)
+    x = bf16_round(rng.standard_normal((1, 64, 24, 160)).astype(np.float32))
+    wt = bf16_round((rng.standard_normal((64, 64, 3, 3)) * 0.06).astype(np.float32))
+    ref = oracle.conv2d(x, wt, (1, 1), (1, 1), relu=True)
+    a = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, relu=True)
+    b = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, relu=True,
+                 tile={"tile_n": 64, "slices_per_stage": 1, "stages": 3})
+    assert oracle.rel_err(a, ref) < 1e-4 and oracle.rel_err(b, ref) < 1e-4

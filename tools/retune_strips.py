@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""Re-measure the DB entries of the workloads that the halo-strip geometry
+applies to (stride-1 windowed convs over maps wider than one 128-row tile:
+VGG-16's 224-wide layers, SSD-512's 128-wide 3x3s, Inception-v3's 147-wide
+3x3s).  Their entries carry explicit tile parameters tuned for plain tiles,
+which also switch the automatic strips off; for each one this times the head
+entry against the kernel's own choice (no explicit tile parameters) and, when
+the latter is faster by ``--min-gain``, records it as the new head entry.
+
+  python tools/retune_strips.py [--dry-run]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--db", default=None)
+    ap.add_argument("--min-gain", type=float, default=0.03)
+    ap.add_argument("--dry-run", action="store_true")
+    args = ap.parse_args()
+    from paper_1809_02697_b200 import tuning
+    from paper_1809_02697_b200.kernels import ConvSchedule
+    from paper_1809_02697_b200.runtime import DevicePool
+    from paper_1809_02697_b200.tuning import MeasuredScheme
+    db = tuning.ScheduleDb(args.db or tuning.DEFAULT_DB)
+    es = {"bf16": 2, "tf32": 4, "fp8": 1}
+    changed = 0
+    for (cpu, key), schemes in sorted(db._data.items()):
+        mode, btag = cpu.split("/")[-2:]
+        if mode not in es or not btag.startswith("b"):
+            continue
+        batch = int(btag[1:])
+        wl = tuning._workload_from_key(key)
+        sh, sw = wl.stride_hw
+        head = schemes[0]
+        rowb = head.schedule.ic_bn * es[mode]
+        if not (sh == 1 and sw == 1 and wl.kernel_w > 1 and rowb in (64, 128)
+                and wl.out_w + wl.kernel_w - 1 > 128):
+            continue
+        if not any(head.schedule.tile().values()):
+            continue                               # already the kernel's own choice
+        pool = DevicePool(0, mode)
+        plain = ConvSchedule(head.schedule.ic_bn, head.schedule.oc_bn, head.schedule.reg_n,
+                             head.schedule.unroll_ker)
+        try:
+            m_old = tuning.measure(wl, head.schedule, repeats=10, pool=pool, batch=batch)
+            m_new = tuning.measure(wl, plain, repeats=10, pool=pool, batch=batch)
+        except Exception as exc:  # noqa: BLE001
+            print(f"{mode} b{batch} {key}: {type(exc).__name__}: {exc}")
+            continue
+        gain = 1.0 - m_new.mean_ns / m_old.mean_ns
+        take = gain >= args.min_gain
+        print(f"{mode} b{batch} {key}: DB head {m_old.mean_ns / 1e3:.1f} us -> strips "
+              f"{m_new.mean_ns / 1e3:.1f} us ({gain * 100:+.1f}%) {'TAKEN' if take else 'kept'}",
+              flush=True)
+        if take and not args.dry_run:
+            kept = [MeasuredScheme(m.schedule, max(m.mean_ns, m_new.mean_ns * 1.001), m.stderr_ns,
+                                   m.repeats) for m in schemes]
+            kept[0] = MeasuredScheme(head.schedule, max(m_old.mean_ns, m_new.mean_ns * 1.001),
+                                     m_old.stderr_ns, m_old.repeats)
+            db.put(cpu, wl, [m_new] + kept)
+            changed += 1
+    print(f"{changed} entries updated")
+
+
+if __name__ == "__main__":
+    main()
