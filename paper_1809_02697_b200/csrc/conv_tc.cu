@@ -298,7 +298,7 @@ template <int OUT, bool HAS_RES, bool AFFINE>
 __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tcol, int col0,
                                               int m, uint8_t* sbuf_gen, const float* par,
                                               float relu_floor, bool round, int c_begin,
-                                              int c_step, float qs, bool store) {
+                                              int c_step, float qs) {
   constexpr bool OUT_F32 = OUT == kOutF32;
   const int nchunk = p.y / 16;  // 16-column TMEM loads
   constexpr int kChunks16 = OUT_F32 ? 4 : OUT == kOutBF16 ? 2 : 1;   // 16-byte pieces per 16 values
@@ -343,7 +343,6 @@ __device__ __forceinline__ void epi_block_tma(const ConvTCParams& p, uint32_t tc
       }
       const uint32_t off = srow + ((((uint32_t)(c * kChunks16 + q)) ^ sxr) << 4);
       uint4* slot = reinterpret_cast<uint4*>(sbuf_gen + off);
-      if (!store) continue;      // halo strip: accumulator row of a band column past the strip
       if constexpr (OUT_F32) {
         float o[4];
         float4 rv = HAS_RES ? *reinterpret_cast<float4*>(slot) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1054,13 +1053,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     // halo strips: accumulator row m = (tile row h, band column w) with a
     // pitch of BW band columns; only w < BWo belongs to the strip, and its
     // staging row is compacted to h * BWo + w (the store / residual boxes are
-    // BWo columns wide)
+    // BWo columns wide).  Rows of band columns past the strip are parked in
+    // the staging rows behind the box (BWo*BH + h*(S-1) + w - BWo < BW*BH <=
+    // 128): they are computed like any other row and never stored, so the
+    // per-piece epilogue loop carries no predicate
     int ms = m;
-    bool mvalid = true;
     if (p.BWo != p.BW) {
       const int hh = m / p.BW, ww = m - hh * p.BW;
-      ms = hh * p.BWo + ww;
-      mvalid = ww < p.BWo;
+      ms = ww < p.BWo ? hh * p.BWo + ww
+                      : min(kTileM - 1, p.BWo * p.BH + hh * (p.BW - p.BWo) + (ww - p.BWo));
     }
     const bool leader = (warp == 2 + gwarps * grp) && lane == 0;
     const uint32_t bar_id = 1 + grp;
@@ -1253,7 +1254,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const int col0 = (b0 + i) * p.y;
             uint8_t* sg = sgrp_gen + i * p.stage_out;
 #define NEO_EPI(OUT, RES, AFF) \
-  epi_block_tma<OUT, RES, AFF>(p, tcol, col0, ms, sg, par, floor_v, rnd, cbeg, cstep, qs, mvalid)
+  epi_block_tma<OUT, RES, AFF>(p, tcol, col0, ms, sg, par, floor_v, rnd, cbeg, cstep, qs)
 #define NEO_EPI_OUT(OUT)                       \
   if (affine) {                                \
     if (has_res) NEO_EPI(OUT, true, true);     \
