@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--flat", action="store_true", help="1x1 conv as a 1 x (H*W) image")
     ap.add_argument("--once", action="store_true", help="one plain launch (tracing)")
     ap.add_argument("--prologue", action="store_true", help="BN-ReLU prologue on the input")
+    ap.add_argument("--strips", action="store_true",
+                    help="explicit --tile geometry is a halo strip (tile_w = band width)")
     args = ap.parse_args()
 
     import torch
@@ -77,7 +79,8 @@ def main():
         pro = (torch.ones(c, device=dev), torch.zeros(c, device=dev), True) if args.prologue else None
         p = D.conv_params(lmode, x, wd, out, n, c, hh, ww, k, r, s_, (st, sw), (ph, pw), args.x,
                           args.y, bias=bias, residual=res, relu=True, tile=tile,
-                          flags=L2.FLAG_PAD_CHANNELS if c % args.x else 0, prologue=pro)
+                          flags=(L2.FLAG_PAD_CHANNELS if c % args.x else 0)
+                          | (L2.FLAG_HALO_STRIPS if args.strips else 0), prologue=pro)
         cfg = D.default_tiles(p)
         ws = torch.zeros(max(D.conv_workspace_bytes(p), 4) // 4, device=dev)
         D.set_workspace(p, ws)
