@@ -561,7 +561,8 @@ __device__ __forceinline__ void mma_slices(uint32_t d, uint32_t alo, uint32_t ah
 }
 
 // MMA issue modes of mma_tiles
-enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst, kMmaHalo64, kMmaHaloWst64 };
+enum { kMmaK4 = 0, kMmaK2, kMmaK1, kMmaNarrow, kMmaHalo, kMmaHaloWst, kMmaHalo64, kMmaHaloWst64,
+       kMmaHalo32, kMmaHaloWst32 };
 
 // The MMA issuer's tile loop.  Barrier map as in conv_tc_kernel.  Stage and
 // accumulator indices advance by counters; MODE fixes the operand layout:
@@ -579,15 +580,19 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
   const uint32_t idesc = umma_idesc(KIND == kKindTF32 ? 2u : KIND == kKindFP8 ? 0u : 1u,
                                     PAIR ? 2 * kTileM : kTileM, p.BN);
   constexpr bool halo64 = MODE == kMmaHalo64 || MODE == kMmaHaloWst64;
-  const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst || halo64;
-  // halo row: 128 bytes (SW128, 4 K steps per row) or 64 (SW64, 2 K steps)
-  constexpr uint32_t hrow_u = halo64 ? 4u : 8u;        // one row in descriptor units
-  constexpr int HKPR = halo64 ? 2 : 4;
+  constexpr bool halo32 = MODE == kMmaHalo32 || MODE == kMmaHaloWst32;
+  const bool halo_mode = MODE == kMmaHalo || MODE == kMmaHaloWst || halo64 || halo32;
+  // halo row: 128 bytes (SW128, 4 K steps per row), 64 (SW64, 2) or 32 (SW32, 1)
+  constexpr uint32_t hrowb = halo32 ? 32u : halo64 ? 64u : 128u;
+  constexpr uint32_t hrow_u = hrowb / 16u;             // one row in descriptor units
+  constexpr int HKPR = (int)(hrowb / 32u);
+  constexpr uint32_t hsbo = 8u * hrowb;                // 8-row core-matrix group
+  constexpr uint32_t hlay = halo32 ? 6u : halo64 ? 4u : 2u;   // UMMA SWIZZLE_32B / 64B / 128B
   const uint64_t adesc0 = MODE == kMmaNarrow ? umma_smem_desc(sA, p.a_sub, 128, 0)
-                          : halo_mode ? umma_smem_desc(sA, 16, halo64 ? 512 : 1024, halo64 ? 4 : 2)
+                          : halo_mode ? umma_smem_desc(sA, 16, hsbo, hlay)
                                       : umma_smem_desc(sA, 16, 8 * p.rowb, p.swz);
   const uint64_t bdesc0 = MODE == kMmaNarrow ? umma_smem_desc(sB, p.b_sub, 128, 0)
-                          : halo_mode ? umma_smem_desc(sB, 16, halo64 ? 512 : 1024, halo64 ? 4 : 2)
+                          : halo_mode ? umma_smem_desc(sB, 16, hsbo, hlay)
                                       : umma_smem_desc(sB, 16, 8 * p.rowb, p.swz);
   const uint32_t a0lo = (uint32_t)adesc0, ahi = (uint32_t)(adesc0 >> 32);
   const uint32_t b0lo = (uint32_t)bdesc0, bhi = (uint32_t)(bdesc0 >> 32);
@@ -630,12 +635,12 @@ __device__ __forceinline__ void mma_tiles(const ConvTCParams& p, int rank, uint3
         c_x = c;
       }
       const uint32_t acc0 = ks != ks0 ? 1u : 0u;
-      if constexpr (MODE == kMmaHaloWst || MODE == kMmaHaloWst64) {
+      if constexpr (MODE == kMmaHaloWst || MODE == kMmaHaloWst64 || MODE == kMmaHaloWst32) {
         const uint32_t bw = b0lo + (uint32_t)ks * R * b_sub_u;
         for (int r = 0; r < R; ++r)
           mma_slices<KIND, PAIR, HKPR>(d_tmem, ad + r * band_r_u, ahi, bw + r * b_sub_u, bhi,
                                        hrow_u, b_tap_u, S, idesc, (acc0 | (uint32_t)r) ? 1u : 0u);
-      } else if constexpr (MODE == kMmaHalo || MODE == kMmaHalo64) {
+      } else if constexpr (MODE == kMmaHalo || MODE == kMmaHalo64 || MODE == kMmaHalo32) {
         for (int g = 0; g < G; ++g)
           mma_slices<KIND, PAIR, HKPR>(d_tmem, ad + g * a_sub_u, ahi, bd + g * b_sub_u, bhi,
                                        hrow_u, b_tap_u, S, idesc, (acc0 | (uint32_t)g) ? 1u : 0u);
@@ -924,8 +929,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
       }
       if (p.dbg & 256) tl_stamp(p, 2);
-      const int mode = p.halo ? (p.rowb == 64 ? (p.wst ? kMmaHaloWst64 : kMmaHalo64)
-                                              : (p.wst ? kMmaHaloWst : kMmaHalo))
+      const int mode = p.halo ? (p.rowb == 32   ? (p.wst ? kMmaHaloWst32 : kMmaHalo32)
+                                 : p.rowb == 64 ? (p.wst ? kMmaHaloWst64 : kMmaHalo64)
+                                                : (p.wst ? kMmaHaloWst : kMmaHalo))
                        : p.rowb == 16 ? kMmaNarrow
                        : p.rowb >= 128 ? kMmaK4
                        : p.rowb == 64 ? kMmaK2 : kMmaK1;
@@ -937,6 +943,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         case kMmaHalo: mma_tiles<KIND, PAIR, kMmaHalo>(p, rank, tmem_base, sA, sB, sBar); break;
         case kMmaHalo64: mma_tiles<KIND, PAIR, kMmaHalo64>(p, rank, tmem_base, sA, sB, sBar); break;
         case kMmaHaloWst64: mma_tiles<KIND, PAIR, kMmaHaloWst64>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHalo32: mma_tiles<KIND, PAIR, kMmaHalo32>(p, rank, tmem_base, sA, sB, sBar); break;
+        case kMmaHaloWst32: mma_tiles<KIND, PAIR, kMmaHaloWst32>(p, rank, tmem_base, sA, sB, sBar); break;
         default: mma_tiles<KIND, PAIR, kMmaHaloWst>(p, rank, tmem_base, sA, sB, sBar); break;
       }
       if (p.dbg & 256) tl_stamp(p, 3);
@@ -1564,8 +1572,9 @@ static int epi_rowb_out(const neo_conv_params* p, int tile_n) {
 static bool halo_format_ok(const neo_conv_params* p, int rowb) {
   static const bool disabled = getenv("NEOB200_NO_HALO") != nullptr;
   static const bool no64 = getenv("NEOB200_NO_HALO64") != nullptr;
+  static const bool no32 = getenv("NEOB200_NO_HALO32") != nullptr;
   return !disabled && p->stride_h == 1 && p->stride_w == 1 && p->s > 1 &&
-         (rowb == 128 || (rowb == 64 && !no64));
+         (rowb == 128 || (rowb == 64 && !no64) || (rowb == 32 && !no32));
 }
 static bool halo_eligible(const neo_conv_params* p, int rowb, int64_t OW) {
   return halo_format_ok(p, rowb) && OW + p->s - 1 <= kTileM;
@@ -1680,19 +1689,34 @@ int neo_conv_default_tiles(neo_conv_params* p) {
     const bool strips_ok = halo_strips_on() && halo_format_ok(p, rowb) && p->tile_n <= 0 &&
                            p->slices_per_stage <= 0 && p->stages <= 0 && p->split_k <= 1 &&
                            p->cta_pair != 2 && !p->pro_scale;
-    if (halo_eligible(p, rowb, OW)) {
+    // 32-byte rows (SW32 shifted views: bf16 maps of 16 channels, Inception's
+    // 48 / 80-channel tensors) joined the halo mainloop after the schedule DB
+    // was tuned, so they only take it when no explicit tile parameter (tuned
+    // for plain tiles) comes with the launch
+    if (halo_eligible(p, rowb, OW) && (rowb != 32 || strips_ok)) {
       // halo tiles: full padded width, as many output rows as fit in 128
       const int bwp = (int)(OW + p->s - 1);
       const int bh = (int)std::min<int64_t>(OH, kTileM / bwp);
       const double eff_h = (double)OW * OH / ((double)neo_ceil_div(OH, bh) * kTileM);
-      const double eff_s = (double)OW * OH * p->n /
-                           ((double)neo_ceil_div(OW, g.BW) * neo_ceil_div(OH, g.BH) *
-                            neo_ceil_div(p->n, g.BNI) * kTileM);
-      // the band reuse cuts A traffic ~S-fold, which outweighs idle rows
-      if (eff_h >= 0.35 * eff_s) {
-        p->tile_w = bwp;
-        p->tile_h = bh;
+      // a width that fills little of the 128 rows (71 of 128 at 73 padded
+      // columns) is better cut into strips; at equal fill full-width tiles
+      // measured 0-3% faster
+      const StripGeom sg = strips_ok ? pick_strips(OH, OW, (int)p->s) : StripGeom{0, 0, 0.0};
+      if (sg.BWo > 0 && sg.BWo < OW && sg.eff >= eff_h + 0.08) {
+        p->tile_w = sg.BWo + (int)p->s - 1;
+        p->tile_h = sg.BH;
         p->tile_img = 1;
+        p->flags |= NEO_FLAG_HALO_STRIPS;
+      } else {
+        const double eff_s = (double)OW * OH * p->n /
+                             ((double)neo_ceil_div(OW, g.BW) * neo_ceil_div(OH, g.BH) *
+                              neo_ceil_div(p->n, g.BNI) * kTileM);
+        // the band reuse cuts A traffic ~S-fold, which outweighs idle rows
+        if (eff_h >= 0.35 * eff_s) {
+          p->tile_w = bwp;
+          p->tile_h = bh;
+          p->tile_img = 1;
+        }
       }
     } else if (strips_ok && OW + p->s - 1 > kTileM) {
       // wide map, nothing but the geometry left to the kernel: halo strips

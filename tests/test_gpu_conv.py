@@ -595,3 +595,42 @@ def test_tc_conv_halo_strips_keep_explicit_tiles(cuda):
     b = run_conv(L.MODE_BF16, x, wt, (1, 1), (1, 1), 64, 64, relu=True,
                  tile={"tile_n": 64, "slices_per_stage": 1, "stages": 3})
     assert oracle.rel_err(a, ref) < 1e-4 and oracle.rel_err(b, ref) < 1e-4
+
+
+HALO32_CASES = [
+    # (n, c, h, w, k, r, s, pad, x_bn, mode): stride-1 windowed convs over 32-byte rows
+    (2, 48, 35, 35, 64, 5, 5, (2, 2), 16, "bf16"),     # Inception 5x5 over 48 channels
+    (2, 80, 37, 37, 192, 3, 3, (0, 0), 16, "bf16"),    # 80 channels = 5 x 16, two N tiles
+    (1, 32, 17, 17, 96, 1, 7, (0, 3), 16, "bf16"),     # 7 horizontal taps
+    (3, 16, 20, 50, 32, 3, 3, (1, 1), 16, "bf16"),     # one channel block
+    (2, 32, 30, 140, 64, 3, 3, (1, 1), 16, "bf16"),    # wide map: strips over 32-byte rows
+    (2, 80, 30, 73, 64, 3, 3, (0, 0), 16, "bf16"),     # 71 of 128 rows full-width -> strips
+    (2, 24, 28, 28, 64, 3, 3, (1, 1), 8, "tf32"),      # tf32 blocks of 8 channels
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", HALO32_CASES)
+@pytest.mark.parametrize("wst", [0, 1, 2])
+def test_tc_conv_halo_32_byte_rows(cuda, case, wst):
+    """Halo (band-reuse) mainloop over 32-byte rows (SWIZZLE_32B shifted
+    views: kMmaHalo32 / kMmaHaloWst32), full-width tiles and strips, with the
+    weight-stationary choice left to the kernel, forced off and forced on."""
+    from paper_1809_02697_b200 import _lib as L
+    n, c, h, w, k, r, s, pd, xb, mode = case
+    rng = np.random.default_rng(c * 7 + h)
+    rnd = bf16_round if mode == "bf16" else tf32_round
+    x = rnd(rng.standard_normal((n, c, h, w)).astype(np.float32))
+    wt = rnd((rng.standard_normal((k, c, r, s)) * np.sqrt(2.0 / (c * r * s))).astype(np.float32))
+    bias = rng.standard_normal(k).astype(np.float32)
+    ref = oracle.conv2d(x, wt, (1, 1), pd, bias=bias, relu=True)
+    tile = {"weight_stationary": wst} if wst else None
+    try:
+        got = run_conv(L.MODE_BF16 if mode == "bf16" else L.MODE_TF32, x, wt, (1, 1), pd, xb, 32,
+                       bias=bias, relu=True, tile=tile)
+    except Exception as exc:       # forced weight-stationary tiles may not fit shared memory
+        from paper_1809_02697_b200.errors import ScheduleInvalid
+        if wst == 2 and isinstance(exc, ScheduleInvalid):
+            pytest.skip(str(exc)[:80])
+        raise
+    assert oracle.rel_err(got, ref) < 1e-4

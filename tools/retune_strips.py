@@ -1,11 +1,14 @@
 #!/usr/bin/env python
-"""Re-measure the DB entries of the workloads that the halo-strip geometry
-applies to (stride-1 windowed convs over maps wider than one 128-row tile:
-VGG-16's 224-wide layers, SSD-512's 128-wide 3x3s, Inception-v3's 147-wide
-3x3s).  Their entries carry explicit tile parameters tuned for plain tiles,
-which also switch the automatic strips off; for each one this times the head
-entry against the kernel's own choice (no explicit tile parameters) and, when
-the latter is faster by ``--min-gain``, records it as the new head entry.
+"""Re-measure the DB entries of the workloads that this round's additions
+to the halo (band-reuse) mainloop apply to: stride-1 windowed convs over maps
+wider than one 128-row tile (halo strips: VGG-16's 224-wide layers, SSD-512's
+128-wide 3x3s, Inception-v3's 147-wide 3x3s), widths that fill little of a
+full-width tile (strips), and 32-byte-row operands (SW32 shifted views:
+Inception's 48 / 80-channel tensors).  Entries with explicit tile parameters
+were tuned for the mainloops of their time and switch the automatic choice
+off; for each one this times the head entry against the kernel's own choice
+(no explicit tile parameters) and, when the latter is faster by
+``--min-gain``, records it as the new head entry.
 
   python tools/retune_strips.py [--dry-run]
 """
@@ -22,6 +25,7 @@ def main():
     ap.add_argument("--db", default=None)
     ap.add_argument("--min-gain", type=float, default=0.03)
     ap.add_argument("--dry-run", action="store_true")
+    ap.add_argument("--only", default="", help="substring of the machine key, e.g. bf16/b128")
     args = ap.parse_args()
     from paper_1809_02697_b200 import tuning
     from paper_1809_02697_b200.kernels import ConvSchedule
@@ -39,8 +43,11 @@ def main():
         sh, sw = wl.stride_hw
         head = schemes[0]
         rowb = head.schedule.ic_bn * es[mode]
-        if not (sh == 1 and sw == 1 and wl.kernel_w > 1 and rowb in (64, 128)
-                and wl.out_w + wl.kernel_w - 1 > 128):
+        # candidates: stride-1 convs with a horizontal window (the halo
+        # mainloop's domain: 128 / 64 / 32-byte rows, full-width tiles or strips)
+        if not (sh == 1 and sw == 1 and wl.kernel_w > 1 and rowb in (32, 64, 128)):
+            continue
+        if args.only and args.only not in cpu:
             continue
         if not any(head.schedule.tile().values()):
             continue                               # already the kernel's own choice
