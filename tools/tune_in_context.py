@@ -73,12 +73,22 @@ def main():
         from paper_1809_02697_b200.quant import calibrate
         scales = calibrate(g)
 
+    from paper_1809_02697_b200.errors import ScheduleInvalid
+
     def step_ms(d) -> float:
         kw = {"fp8_scales": scales} if scales is not None else {}
         prog = DeviceProgram(ExecutablePlan.compile(compile_graph(g, mode=args.mode, db=d, **kw)),
                              0, args.mode)
         prog.set_inputs(feeds)
-        for _ in range(3):
+        try:
+            prog.launch()
+        except ScheduleInvalid as exc:
+            # a stored candidate the kernel no longer accepts (e.g. measured as a
+            # plain tile before its row format joined the halo mainloop)
+            print(f"  skipped: {str(exc)[:120]}")
+            del prog
+            return float("inf")
+        for _ in range(2):
             prog.launch()
         prog.stream.synchronize()
         ts = []
