@@ -597,7 +597,7 @@ class DeviceProgram:
                           hw_pair(na.attrs["stride"]), (0, 0), ic_bn, oc_bn, vec(scale),
                           vec(shift), vec(bias), None, parts[0]["relu"],
                           x_cb=self._window(data), out_cb=self._window(oa), flags=flags,
-                          tile={"tile_n": tile_n},
+                          tile=self._sibling_tile_params(tile_n, c, ic_bn),
                           second=(ob.tensor, ka, parts[1]["relu"], self._window(ob)),
                           qscales=qscales)
         self.tc_params.append(p)
@@ -605,6 +605,20 @@ class DeviceProgram:
         fl, nbytes, desc = self._conv_work(n, c, h, wd, k, 1, 1, hw_pair(na.attrs["stride"]),
                                            (0, 0), es, kb=f"{ka}+{k - ka}")
         self._emit(f"conv{na.id}+{nb.id}", lambda p=p: D.conv2d(p, self.stream), nbytes, fl, desc)
+
+    def _sibling_tile_params(self, tile_n: int, c: int, ic_bn: int) -> dict:
+        """Tile parameters of a merged sibling launch (it has no schedule-DB
+        entry of its own).  Short reductions (<= 4 channel-block slices: the
+        56x56 stride-2 pair of ResNet-50, C = 256) get two slices per stage
+        and two stages: the kernel's own choice keeps the full four-group
+        epilogue staging and squeezes the ring to 2 x 32 KB (42.5 us isolated
+        at b64 against 30.1 us; `tools/conv_bench.py --sweep` on the merged
+        C256 -> K640 workload); longer reductions keep the kernel's choice,
+        which the same sweep finds best."""
+        tile = {"tile_n": tile_n}
+        if self.mode == "bf16" and tile_n <= 128 and -(-c // ic_bn) <= 4:
+            tile.update({"slices_per_stage": 2, "stages": 2})
+        return tile
 
     def _bind_junction(self, ne, nr) -> bool:
         """Expand conv ``ne`` (+ residual) and reduce conv ``nr`` as one
