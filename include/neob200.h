@@ -220,11 +220,16 @@ typedef struct neo_conv_params {
   int out_cb_offset, out_cb_total; /* concat-in-place destination window      */
   int res_cb_offset, res_cb_total;
   int out_dtype;       /* NEO_F32 / NEO_BF16 / NEO_FP8 (residual: same dtype) */
-  int flags;           /* NEO_FLAG_ROUND_TF32 | NEO_FLAG_PAD_CHANNELS          */
+  int flags;           /* NEO_FLAG_ROUND_TF32 | NEO_FLAG_PAD_CHANNELS |
+                        * NEO_FLAG_STATIC_WEIGHTS | NEO_FLAG_HALO_STRIPS      */
   /* tile configuration (0 = automatic).  tile_w x tile_h x tile_img output
    * pixels (<= 128) form the M tile; tile_n output channels (multiple of 16,
    * <= 256) the N tile; slices_per_stage (r, s, channel-block) slices per
-   * pipeline stage; stages = pipeline depth (<= 8). */
+   * pipeline stage; stages = pipeline depth (<= 8).  Halo (band-reuse) tiles of
+   * stride-1 convs with a horizontal window (32/64/128-byte rows): tile_w =
+   * ow + s - 1 > ow, tile_img = 1 (one band per kernel row and channel block,
+   * the s taps are shifted views of it); with NEO_FLAG_HALO_STRIPS tile_w is
+   * the band width of a column strip of tile_w - (s - 1) output columns. */
   int tile_w, tile_h, tile_img, tile_n, slices_per_stage, stages;
   /* split-K: the reduction is cut into split_k ranges run by separate CTAs
    * (0 = automatic: only when the output tiles leave most SMs idle; 1 = off).
