@@ -288,3 +288,21 @@ def test_f32_upload_equals_host_rounded_upload(cuda):
     b.pipeline(pinned, outs)
     torch.cuda.synchronize()
     assert np.array_equal(outs[1].numpy(), a.run({name: pinned[1].numpy()})[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model,batch", [("inception_v3", 3), ("vgg16", 2)])
+def test_default_tiles_small_batch_vs_oracle(cuda, model, batch):
+    """Kernel-picked tiles (no schedule DB: a batch size nobody tuned) on the
+    families whose maps are wider than one 128-row tile: halo strips, 32-byte
+    row halo tiles, image-spanning and one-image geometries all come from
+    neo_conv_default_tiles here; every image's logits against the oracle."""
+    from paper_1809_02697_b200 import (DevicePool, build_model, compile_graph, execute,
+                                       model_input)
+    g = build_model(model, batch=batch, softmax=False)
+    feeds = model_input(g, seed=3)
+    ref = oracle.execute_reference(g, feeds)[0]
+    got = execute(compile_graph(g, mode="bf16"), feeds, DevicePool(0, "bf16"))[0]
+    assert got.shape == ref.shape
+    assert oracle.rel_err(got, ref) < 2e-2
+    assert (got.argmax(1) == ref.argmax(1)).all()
